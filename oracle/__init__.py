@@ -1,0 +1,143 @@
+"""CPU oracle for the sparse gated-FFN forward — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2603_23198_b200``) never imports it and shares no code with it.
+
+Thin numpy/ctypes wrapper over ``oracle.c`` (plain fp64 C loops, each function citing
+the PAPER.md passage it follows).  See oracle.c's header for the pins.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+        # -O2 without -ffast-math: fp64 sums keep the literal k-ascending order.
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fno-fast-math", "-ffp-contract=off", "-shared",
+                               "-fPIC", "-o", _LIB, src, "-lm"])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        lib.oracle_bf16_to_double.argtypes = [ctypes.c_uint16]
+        lib.oracle_bf16_to_double.restype = ctypes.c_double
+        lib.oracle_f32_to_bf16_rne.argtypes = [ctypes.c_float]
+        lib.oracle_f32_to_bf16_rne.restype = ctypes.c_uint16
+        lib.oracle_gate_preact.argtypes = [vp, vp, i64, i64, i64, vp]
+        lib.oracle_gate_preact_f32.argtypes = [vp, vp, i64, i64, i64, vp]
+        lib.oracle_pack.argtypes = [vp, i64, i64, ci, ci, vp, vp]
+        lib.oracle_pack.restype = i64
+        lib.oracle_unpack.argtypes = [vp, i64, i64, ci, ci, vp]
+        lib.oracle_ffn_dense.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp]
+        lib.oracle_ffn_twell.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, ci, ci, vp, vp]
+        _lib = lib
+    return _lib
+
+
+def _u16(a):
+    a = np.ascontiguousarray(a)
+    assert a.dtype == np.uint16, a.dtype
+    return a
+
+
+def bf16_rne(f: np.ndarray) -> np.ndarray:
+    lib = _load()
+    f = np.asarray(f, dtype=np.float32).ravel()
+    return np.array([lib.oracle_f32_to_bf16_rne(float(v)) for v in f], dtype=np.uint16)
+
+
+def gate_preact(X, Wg) -> np.ndarray:
+    """A = X W_g^T in fp64 (Eq.1), X [M,K] and W_g [N,K] as bf16 bits."""
+    X, Wg = _u16(X), _u16(Wg)
+    M, K = X.shape
+    N = Wg.shape[0]
+    A = np.empty((M, N), dtype=np.float64)
+    _load().oracle_gate_preact(X.ctypes.data, Wg.ctypes.data, M, K, N, A.ctypes.data)
+    return A
+
+
+def pack(S, T: int, C: int):
+    """Alg.1 lines 7-17 packed as P:869 on fp32 S [M,N] -> (words uint32 [M,N/C], counts [M,N/T], n_overflow).
+    Slots beyond each block's count are zero-initialised here (unspecified in the format)."""
+    S = np.ascontiguousarray(S, dtype=np.float32)
+    M, N = S.shape
+    assert N % T == 0 and T % C == 0 and T // C >= 2
+    words = np.zeros((M, N // C), dtype=np.uint32)
+    counts = np.zeros((M, N // T), dtype=np.uint32)
+    ov = _load().oracle_pack(S.ctypes.data, M, N, T, C, words.ctypes.data, counts.ctypes.data)
+    return words, counts, int(ov)
+
+
+def unpack(words, N: int, T: int, C: int) -> np.ndarray:
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    M = words.shape[0]
+    H = np.empty((M, N), dtype=np.float32)
+    _load().oracle_unpack(words.ctypes.data, M, N, T, C, H.ctypes.data)
+    return H
+
+
+def ffn_dense(X, Wg, Wu, Wd, want_h: bool = False):
+    """Eq.1 with ReLU gate, fp64.  Returns Y [M,K] (and h [M,N])."""
+    X, Wg, Wu, Wd = map(_u16, (X, Wg, Wu, Wd))
+    M, K = X.shape
+    N = Wg.shape[0]
+    Y = np.empty((M, K), dtype=np.float64)
+    H = np.empty((M, N), dtype=np.float64) if want_h else None
+    _load().oracle_ffn_dense(X.ctypes.data, Wg.ctypes.data, Wu.ctypes.data, Wd.ctypes.data, M, K, N,
+                             Y.ctypes.data, H.ctypes.data if want_h else None)
+    return (Y, H) if want_h else Y
+
+
+def ffn_twell(X, words, Wu, Wd, N: int, T: int, C: int, A=None) -> np.ndarray:
+    """Eq.3 over a packed TwELL; gate = stored bf16 value, or exact A if given."""
+    X, Wu, Wd = map(_u16, (X, Wu, Wd))
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    M, K = X.shape
+    Y = np.empty((M, K), dtype=np.float64)
+    mode = 0
+    Ap = None
+    if A is not None:
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        mode, Ap = 1, A.ctypes.data
+    _load().oracle_ffn_twell(X.ctypes.data, words.ctypes.data, Wu.ctypes.data, Wd.ctypes.data, M, K, N, T, C,
+                             mode, Ap, Y.ctypes.data)
+    return Y
+
+
+def pack_from_inputs(X, Wg, T: int, C: int):
+    """The oracle's TwELL for relu(X W_g^T): fp64 pre-activation -> fp32 (exact on grid inputs) -> Alg.1."""
+    A = gate_preact(X, Wg)
+    words, counts, ov = pack(A.astype(np.float32), T, C)
+    return words, counts, ov, A
+
+
+def valid_prefix_equal(w_a: np.ndarray, w_b: np.ndarray, T: int, C: int) -> np.ndarray:
+    """Per (row, tile) block: counts equal and the stored prefix min(count, cap) equal.
+    Returns a bool array [M, N/T]."""
+    W = T // C
+    M = w_a.shape[0]
+    a = w_a.reshape(M, -1, W)
+    b = w_b.reshape(M, -1, W)
+    cnt_eq = a[:, :, 0] == b[:, :, 0]
+    cap = W - 1
+    z = np.minimum(a[:, :, 0], cap)
+    slot = np.arange(1, W)[None, None, :]
+    valid = slot <= z[:, :, None]
+    slots_eq = np.all((a[:, :, 1:] == b[:, :, 1:]) | ~valid, axis=2)
+    return cnt_eq & slots_eq

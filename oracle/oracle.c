@@ -1,0 +1,187 @@
+/*
+ * oracle.c — CPU ORACLE for the sparse gated-FFN forward (TEST INFRASTRUCTURE ONLY).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load this library.  The product path (paper_2603_23198_b200/) never links,
+ * imports or calls it, and shares no code with it.
+ *
+ * Plain, slow, obviously-correct definitions, written from /root/reference/PAPER.md
+ * (cited as P:<line>).  Floating point is fp64 with k ascending; no blocking, fusion or
+ * reordering beyond what the cited definition states.  Rows are independent (OpenMP over
+ * rows only), so results do not depend on the thread count.
+ *
+ * Conventions:
+ *   - all weights are stored hidden-major [N, K] row-major (R11: P:55, P:1078, L1 P:464)
+ *   - inputs are bf16 bit patterns (uint16), widened exactly to double
+ *   - TwELL packed word layout (P:869, L1 P:817-834): per (row, tile) block of T/C
+ *     uint32 words, word 0 = count, word 1+j = col | bf16(value) << 16; capacity T/C-1
+ *
+ * Pins (tests/test_oracle_pins.py): the paper's / SPEC's worked examples
+ * (tests/golden/), exact integer arithmetic on dyadic-grid inputs, brute-force
+ * compaction, permutation-matrix closed forms, Eq.1 == Eq.3 identity, invariants.
+ * Parity unpinned: nothing.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+/* bf16 is the upper 16 bits of an IEEE binary32 ("bfloat16"); widening is exact. */
+double oracle_bf16_to_double(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+/* float -> bf16, round to nearest even: the paper stores __float2bfloat16(C_accum)
+ * (L1 P:824-826), which is IEEE round-to-nearest-even.  NaN is not produced here. */
+uint16_t oracle_f32_to_bf16_rne(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    uint32_t lsb = (u >> 16) & 1u;
+    uint32_t rounded = u + 0x7FFFu + lsb;
+    return (uint16_t)(rounded >> 16);
+}
+
+/* Gate pre-activation of Eq.1: A[m,n] = sum_k x[m,k] * W_g[n,k]  (fp64, k ascending). */
+void oracle_gate_preact(const uint16_t* X, const uint16_t* Wg, int64_t M, int64_t K, int64_t N, double* A) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t n = 0; n < N; ++n) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k)
+                acc += oracle_bf16_to_double(X[m * K + k]) * oracle_bf16_to_double(Wg[n * K + k]);
+            A[m * N + n] = acc;
+        }
+    }
+}
+
+/*
+ * Alg.1 lines 7-17 for every row, on the fp32 tile values S (the paper
+ * thresholds the fp32 accumulator, L1 P:803-808), packed as in P:869 / L1 P:817-834:
+ *
+ *   for r: for each tile n0 (T = T_n columns):
+ *     z <- 0
+ *     for c in 0..T-1:  if S[r, n0+c] > 0:            (strict, Alg.1 line 11)
+ *        if z < cap: h_I <- n0+c ; h_v <- S           (lines 12-14; cap = T/C - 1)
+ *        z <- z + 1                                   (line 15)
+ *     h_nz[r, n0/T] <- z                              (line 17; true count, reading R5)
+ *
+ * words: uint32 [M, N/C]; counts (may be NULL): uint32 [M, N/T].  Slots beyond the count
+ * are left untouched (no padding value).  Returns the number of (row, tile)
+ * blocks whose count exceeded the capacity.
+ */
+int64_t oracle_pack(const float* S, int64_t M, int64_t N, int T, int C, uint32_t* words, uint32_t* counts) {
+    const int64_t NT = N / T, W = T / C, cap = W - 1;
+    int64_t overflow = 0;
+#pragma omp parallel for schedule(static) reduction(+ : overflow)
+    for (int64_t r = 0; r < M; ++r) {
+        for (int64_t t = 0; t < NT; ++t) {
+            const int64_t n0 = t * T;
+            uint32_t* blk = words + r * (N / C) + t * W;
+            int64_t z = 0;
+            for (int64_t c = 0; c < T; ++c) {
+                float s = S[r * N + n0 + c];
+                if (s > 0.0f) {
+                    if (z < cap) {
+                        uint32_t idx = (uint32_t)(n0 + c);
+                        uint32_t val = oracle_f32_to_bf16_rne(s);
+                        blk[1 + z] = (idx & 0xFFFFu) | (val << 16);
+                    }
+                    z += 1;
+                }
+            }
+            blk[0] = (uint32_t)z;
+            if (counts) counts[r * NT + t] = (uint32_t)z;
+            if (z > cap) overflow += 1;
+        }
+    }
+    return overflow;
+}
+
+/* TwELL -> dense (SPEC S:167-175 twell_to_dense): H[m, col] = value for the valid prefix
+ * min(count, cap) of every (row, tile) block, +0 elsewhere.  H is float [M, N]. */
+void oracle_unpack(const uint32_t* words, int64_t M, int64_t N, int T, int C, float* H) {
+    const int64_t NT = N / T, W = T / C, cap = W - 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t n = 0; n < N; ++n) H[m * N + n] = 0.0f;
+        for (int64_t t = 0; t < NT; ++t) {
+            const uint32_t* blk = words + m * (N / C) + t * W;
+            int64_t z = blk[0];
+            if (z > cap) z = cap;
+            for (int64_t j = 0; j < z; ++j) {
+                uint32_t w = blk[1 + j];
+                H[m * N + (w & 0xFFFFu)] = (float)oracle_bf16_to_double((uint16_t)(w >> 16));
+            }
+        }
+    }
+}
+
+/* Eq.1 with sigma = relu, fp64:
+ *   h_g = relu(x W_g), h_u = x W_u, h = h_u * h_g, y = h W_d.
+ * With hidden-major storage, (x W_g)[m,n] = sum_k x[m,k] Wg[n,k] and (h W_d)[m,j] = sum_n h[m,n] Wd[n,j].
+ * Y is double [M, K]; H (optional, may be NULL) receives h as double [M, N]. */
+void oracle_ffn_dense(const uint16_t* X, const uint16_t* Wg, const uint16_t* Wu, const uint16_t* Wd, int64_t M,
+                      int64_t K, int64_t N, double* Y, double* H) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t j = 0; j < K; ++j) Y[m * K + j] = 0.0;
+        for (int64_t n = 0; n < N; ++n) {
+            double g = 0.0, u = 0.0;
+            for (int64_t k = 0; k < K; ++k) {
+                double x = oracle_bf16_to_double(X[m * K + k]);
+                g += x * oracle_bf16_to_double(Wg[n * K + k]);
+                u += x * oracle_bf16_to_double(Wu[n * K + k]);
+            }
+            double hg = g > 0.0 ? g : 0.0;
+            double h = u * hg;
+            if (H) H[m * N + n] = h;
+            if (h != 0.0)
+                for (int64_t j = 0; j < K; ++j) Y[m * K + j] += h * oracle_bf16_to_double(Wd[n * K + j]);
+        }
+    }
+}
+
+/*
+ * Eq.3 / Alg.2 over a packed TwELL:
+ *   y[m,:] = sum_t sum_{c < h_nz[m,t]} h_v[m, t T/C + c] * (x[m,:] . W_u[n,:]) * W_d[n,:],  n = h_I[...]
+ * Only the stored prefix min(h_nz, cap) exists (reading R5).  gate_mode 0: h_v is the stored bf16
+ * value (the paper's pipeline, L2 P:994-1002 multiplies by it); gate_mode 1: h_v is replaced by the
+ * exact fp64 pre-activation A[m, n] (A must then be given) — the form that equals Eq.1 exactly.
+ * Y is double [M, K]. fp64, entries in stored (ascending column) order.
+ */
+void oracle_ffn_twell(const uint16_t* X, const uint32_t* words, const uint16_t* Wu, const uint16_t* Wd, int64_t M,
+                      int64_t K, int64_t N, int T, int C, int gate_mode, const double* A, double* Y) {
+    const int64_t NT = N / T, W = T / C, cap = W - 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t j = 0; j < K; ++j) Y[m * K + j] = 0.0;
+        for (int64_t t = 0; t < NT; ++t) {
+            const uint32_t* blk = words + m * (N / C) + t * W;
+            int64_t z = blk[0];
+            if (z > cap) z = cap;
+            for (int64_t c = 0; c < z; ++c) {
+                uint32_t w = blk[1 + c];
+                int64_t n = (int64_t)(w & 0xFFFFu);
+                double hv = gate_mode == 1 ? A[m * N + n] : oracle_bf16_to_double((uint16_t)(w >> 16));
+                double u = 0.0;
+                for (int64_t k = 0; k < K; ++k)
+                    u += oracle_bf16_to_double(X[m * K + k]) * oracle_bf16_to_double(Wu[n * K + k]);
+                double h = hv * u;
+                for (int64_t j = 0; j < K; ++j) Y[m * K + j] += h * oracle_bf16_to_double(Wd[n * K + j]);
+            }
+        }
+    }
+}
+
+/* fp32-input variants of the gate pre-activation and dense FFN (fp32 mode, reading R19). */
+void oracle_gate_preact_f32(const float* X, const float* Wg, int64_t M, int64_t K, int64_t N, double* A) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t n = 0; n < N; ++n) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k) acc += (double)X[m * K + k] * (double)Wg[n * K + k];
+            A[m * N + n] = acc;
+        }
+}
