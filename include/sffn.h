@@ -1,0 +1,160 @@
+/*
+ * sffn.h — C ABI of the B200-native (sm_100a) sparse gated-FFN forward (TwELL).
+ *
+ * Method: arxiv 2603.23198, /root/reference/PAPER.md (cited P:<line>).
+ *   Eq.1      h_u = x W_u, h_g = relu(x W_g), h = h_u * h_g, y = h W_d
+ *   Alg.1    gate GEMM whose epilogue stores relu(x W_g) in TwELL
+ *   Alg.2 / Eq.3  fused up+down projection over the TwELL non-zeros
+ *   TwELL, packed 32-bit layout (Listing 1)
+ *
+ * Conventions (every call):
+ *   - All tensor pointers are DEVICE pointers to caller-owned memory.  The library never allocates
+ *     device memory, never frees caller memory and never synchronizes the device (except
+ *     sffn_overflow_check, which synchronizes the given stream by design).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every call is
+ *     stream-ordered and asynchronous; calls on distinct streams are thread-safe.
+ *   - Notation M (tokens), K (model dim), N (hidden dim) as in P:55.
+ *   - Weights are hidden-major, [N, K] row-major, for W_g, W_u and W_d alike (DESIGN.md reading
+ *     R11: "up projection weight matrix is stored in transposed format" P:1078, Listing 1 NT
+ *     GEMM P:464).  W_g and W_u are therefore nn.Linear weights; W_d is [N, K] = the paper's W_d.
+ *   - X, W_*, Y, H are bf16 (IEEE bfloat16 bit patterns), row-major, 16-byte aligned.
+ *   - Return value: an sffn_status.  Argument/shape errors are detected on the host BEFORE any
+ *     launch (nothing is enqueued).  SFFN_ERR_CUDA means a launch failed (cudaGetLastError).
+ *   - Data-dependent results (TwELL tile overflow) are never returned synchronously: they are
+ *     counted into a caller-owned device uint32 (`d_overflow`, may be NULL), which the caller zeroes
+ *     and reads after its own synchronization — the paper's "flag that is reported to the CPU at the
+ *     next GPU synchronization point".  sffn_overflow_check does that read for you.
+ *
+ * TwELL packed layout (bf16 mode): uint32 matrix [M, N/C], row-major.  Row m, tile t
+ * (columns [tT, tT+T)) owns words [m*N/C + t*T/C, +T/C): word 0 = count of strictly positive
+ * pre-activations in the tile (the TRUE count, may exceed the capacity; reading R5); words 1..
+ * = (column & 0xFFFF) | (bf16_rne(value) << 16) in ascending column order (reading R3); capacity
+ * T/C - 1 ("the first 31 TwELL indices" at T=256, C=8).  Column indices are local to the
+ * weight rows passed in (a shard's row 0 is index 0).  Words past the count are unspecified.
+ */
+#ifndef SFFN_H_
+#define SFFN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SFFN_OK = 0,
+    SFFN_ERR_INVALID_ARG = 1,   /* NULL pointer, misaligned pointer (< 16 B), bad T/C combination      */
+    SFFN_ERR_SHAPE = 2,         /* M < 0, K % 64 != 0, N % T != 0, N > 65536, workspace too small, ...  */
+    SFFN_ERR_TILE_OVERFLOW = 3, /* (sffn_overflow_check only) some (row, tile) had > T/C-1 positives   */
+    SFFN_ERR_CUDA = 4,          /* a CUDA runtime / driver call or kernel launch failed                 */
+    SFFN_ERR_NCCL = 5,          /* an NCCL call failed                                                  */
+    SFFN_ERR_UNSUPPORTED = 6    /* not a B200 (sm_100) device, or a feature not built                   */
+} sffn_status;
+
+/* Human-readable name of a status code (static storage). */
+const char* sffn_status_string(int status);
+/* Library version / build string (static storage). */
+const char* sffn_version(void);
+
+/* Number of uint32 words of a packed TwELL for [M, N] with tile T and compression C: M * N / C. */
+int64_t sffn_twell_words(int64_t M, int64_t N, int T, int C);
+/* Bytes of device workspace sffn_forward needs (the TwELL of the gate): 4 * sffn_twell_words. */
+size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C);
+
+/*
+ * sffn_pack — Alg.1: TwELL of relu(X W_g^T), computed by a tcgen05/TMEM tensor-core GEMM
+ * (bf16 x bf16 -> fp32 accumulators in TMEM) whose epilogue thresholds the fp32 accumulator with a
+ * strict > 0 (Alg.1 line 11; reading R1-R2) and compacts each row-tile in ascending column order.
+ *   X      [M, K] bf16            Wg  [N, K] bf16 (hidden-major)
+ *   twell  [M, N/C] uint32 (output, packed layout above)
+ *   d_overflow  optional device uint32, += 1 per (row, tile) whose count exceeded T/C - 1
+ * Constraints: M >= 0, K >= 64, K % 64 == 0, N % T == 0, N % 16 == 0, N <= 65536,
+ *              T in {32, 64, 128, 256}, C in {1, 2, 4, 8, 16}, T / C >= 2.
+ */
+int sffn_pack(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
+              uint32_t* d_overflow, void* stream);
+
+/*
+ * sffn_unpack — verification: TwELL -> dense bf16 (SPEC S:167-175 twell_to_dense).
+ * dense[m, col_offset + n] = stored value for the valid prefix min(count, T/C-1) of each tile,
+ * +0 for every other n in [0, N).  dense has row stride ld_dense elements (>= col_offset + N);
+ * columns outside [col_offset, col_offset + N) are not touched.
+ */
+int sffn_unpack(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int64_t col_offset, int64_t ld_dense,
+                void* dense, void* stream);
+
+/*
+ * sffn_up_down — Alg.2 / Eq.3 from an existing TwELL:
+ *   Y[m, :] = sum_t sum_{c < min(h_nz, T/C-1)} h_v * (X[m, :] . Wu[n, :]) * Wd[n, :]
+ * h_v = the stored bf16 gate value; products and sums in fp32 (FMA); Y rounded to bf16 (RN).
+ *   X [M, K] bf16, twell [M, N/C] uint32, Wu [N, K] bf16, Wd [N, K] bf16, Y [M, K] bf16 (output)
+ */
+int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const void* Wd, int64_t M, int64_t K,
+                 int64_t N, int T, int C, void* Y, void* stream);
+
+/*
+ * sffn_forward — the whole sparse FFN forward (the paper's two launches):
+ * sffn_pack into `workspace` (>= sffn_forward_workspace_bytes) then sffn_up_down.
+ * The TwELL left in the workspace is valid after the call (stream-ordered).
+ */
+int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                 int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, void* stream);
+
+/*
+ * sffn_dense_forward — the library's own dense tcgen05 FFN (Eq.1 without sparsity): the speedup
+ * denominator.  Launch 1: fused gate||up GEMM with epilogue H = bf16(relu(g) * u)   (H [M, N] bf16,
+ * caller-owned).  Launch 2: Y = H W_d as a GEMM against WdT = W_d^T stored [K, N] row-major (a
+ * one-time weight layout for the dense model; sffn_transpose_bf16 produces it).
+ */
+int sffn_dense_forward(const void* X, const void* Wg, const void* Wu, const void* WdT, int64_t M, int64_t K,
+                       int64_t N, void* H, void* Y, void* stream);
+
+/* out[c, r] = in[r, c] for a bf16 [rows, cols] matrix (weight-layout utility). */
+int sffn_transpose_bf16(const void* in, int64_t rows, int64_t cols, void* out, void* stream);
+
+/*
+ * sffn_gate_gemm_f32 — verification: the raw fp32 accumulators S = X W_g^T of the same tcgen05
+ * mainloop sffn_pack uses (S [M, N] float, output).  Used to prove the tensor-core accumulation is
+ * exact on dyadic-grid inputs.
+ */
+int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, float* S, void* stream);
+
+/*
+ * sffn_overflow_check — synchronizes `stream`, copies *d_overflow to *host_count (if non-NULL) and
+ * returns SFFN_ERR_TILE_OVERFLOW if it is non-zero, else SFFN_OK.
+ */
+int sffn_overflow_check(const uint32_t* d_overflow, void* stream, uint32_t* host_count);
+
+/* ---------------------------------------------------------------- multi-GPU (hidden-dim shards)
+ * One process per GPU.  Rank r owns hidden units [n_offset, n_offset + N_local) — contiguous row
+ * blocks of all three [N, K] weights — packs its own TwELL (local indices), computes the partial
+ * Y_r = sum_{n in shard} h W_d[n, :], and the partials are summed with ONE NCCL all-reduce (bf16,
+ * sum) over NVLink / NVSwitch (north_star (5)).  X is replicated on every rank.
+ */
+typedef struct sffn_comm sffn_comm;
+
+/* Fills 128 bytes with a new NCCL unique id (call on rank 0, broadcast it yourself). */
+int sffn_comm_unique_id(void* id128);
+/* Creates the library's own NCCL communicator on `cuda_device` (must be the current device). */
+int sffn_comm_init(sffn_comm** out, int nranks, int rank, const void* id128, int cuda_device);
+int sffn_comm_destroy(sffn_comm* comm);
+int sffn_comm_size(const sffn_comm* comm);
+
+/*
+ * sffn_sharded_forward — sffn_forward on the local shard, then one in-place NCCL all-reduce (sum)
+ * of Y [M, K] bf16 on `stream`.  With n_chunks > 1 the M dimension is processed in chunks and the
+ * all-reduce of chunk i overlaps the compute of chunk i+1 (the library orders them with events on
+ * an internal communication stream; still no host synchronization).
+ */
+int sffn_sharded_forward(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
+                         int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
+                         size_t ws_bytes, uint32_t* d_overflow, int n_chunks, void* stream);
+
+/* Plain in-place all-reduce (sum) of a bf16 buffer on the communicator (used by tests). */
+int sffn_allreduce_bf16(sffn_comm* comm, void* buf, int64_t count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFFN_H_ */

@@ -1,0 +1,7 @@
+"""B200-native (sm_100a) sparse gated-FFN forward with the TwELL format (arxiv 2603.23198).
+
+The compute path is the C-ABI library ``libsffn.so`` (include/sffn.h); ``sffn`` is its thin binding.
+"""
+from . import sffn  # noqa: F401
+from .sffn import (Comm, SffnError, dense_forward, forward, gate_gemm_f32, overflow_check, pack,  # noqa: F401
+                   transpose, twell_words, unpack, up_down, workspace_bytes)

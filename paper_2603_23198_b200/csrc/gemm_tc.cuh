@@ -1,0 +1,327 @@
+// gemm_tc.cuh — persistent, warp-specialized tcgen05 GEMM for sm_100a:  D = A · B^T
+//   A [M, K] bf16 row-major (K-major), B [Nout, K] bf16 row-major (K-major), fp32 accumulate in TMEM.
+//
+// Roles (256 threads):
+//   warp 0  lane 0 : TMA producer — 128x64 A tile + 256x64 B tile per k-block into a SMEM ring
+//   warp 1  lane 0 : MMA issuer   — 4 x tcgen05.mma (M=128, N=256, K=16) per k-block into one of two
+//                                   TMEM accumulators (2 x 256 columns = all 512), commit -> mbarriers
+//   warp 2         : TMEM allocator
+//   warps 4..7     : epilogue — tcgen05.ld 32x32b (thread = output row), per-mode epilogue, TMA store
+// TMEM double buffering lets the epilogue of tile i run under the mainloop of tile i+1.
+//
+// Epilogue modes:
+//   EPI_TWELL : Alg.1 — strict > 0 on the fp32 accumulator, ascending-
+//               column compaction per row and per TwELL tile of T columns, packed 32-bit words
+//               (count first, idx | bf16 << 16; P:869, L1 P:817-834).  Each thread owns one row of
+//               the tile, so the compaction is thread-local (no atomics, deterministic order).
+//   EPI_F32   : raw fp32 accumulators (verification of the mainloop).
+//   EPI_GLU   : dense baseline launch 1: B = [W_g rows n0..n0+127 ; W_u rows n0..n0+127], epilogue
+//               H = bf16(relu(g) * u)  (Eq.1 P:57-60 without sparsity).
+//   EPI_BF16  : dense baseline launch 2: plain bf16 store of the 128x256 tile.
+#pragma once
+#include "ptx.cuh"
+
+namespace sffn {
+
+constexpr int GEMM_BM = 128, GEMM_BN = 256, GEMM_BK = 64;
+constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;  // 16 KB
+constexpr int GEMM_B_BYTES = GEMM_BN * GEMM_BK * 2;  // 32 KB
+constexpr int GEMM_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES;
+constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_SMEM_LIMIT = 232448;  // max dynamic shared memory per block (227 KB)
+constexpr int GEMM_GROUP_M = 16;         // tile raster: 16 M-tiles sweep all N-tiles together (L2 reuse)
+
+enum { EPI_TWELL = 0, EPI_F32 = 1, EPI_GLU = 2, EPI_BF16 = 3 };
+
+template <int EPI, int C>
+__host__ __device__ constexpr int gemm_epi_warp_bytes() {
+    return EPI == EPI_TWELL ? 32 * (GEMM_BN / C) * 4 : (EPI == EPI_F32 ? 0 : 32 * 128 * 2);
+}
+template <int EPI, int C>
+__host__ __device__ constexpr int gemm_stages() {
+    return (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / GEMM_STAGE_BYTES > 6
+               ? 6
+               : (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / GEMM_STAGE_BYTES;
+}
+template <int EPI, int C>
+__host__ __device__ constexpr int gemm_smem_bytes() {
+    return 1024 + gemm_stages<EPI, C>() * GEMM_STAGE_BYTES + 4 * gemm_epi_warp_bytes<EPI, C>() + 256;
+}
+
+struct GemmArgs {
+    int M;          // rows of A / D
+    int N;          // valid output columns (TwELL: hidden units; GLU: hidden units; BF16: Nout)
+    int K;          // reduction length (multiple of 64 after zero fill)
+    int num_m, num_n;
+    int T;          // TwELL tile (EPI_TWELL)
+    uint32_t* overflow;  // EPI_TWELL, may be null
+    float* out_f32;      // EPI_F32
+    int64_t ld_out;      // EPI_F32 row stride (elements)
+};
+
+__device__ __forceinline__ void gemm_tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+    const int group = tile / (GEMM_GROUP_M * num_n);
+    const int first_m = group * GEMM_GROUP_M;
+    const int gm = min(GEMM_GROUP_M, num_m - first_m);
+    const int in = tile - group * GEMM_GROUP_M * num_n;
+    mb = first_m + in % gm;
+    nb = in / gm;
+}
+
+template <int EPI, int C>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmOut,
+                   const GemmArgs args) {
+    constexpr int S = gemm_stages<EPI, C>();
+    constexpr int EWB = gemm_epi_warp_bytes<EPI, C>();
+    static_assert(S >= 2, "not enough shared memory for a 2-stage ring");
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stA = smem;
+    uint8_t* stB = smem + S * GEMM_A_BYTES;
+    uint8_t* epi = stB + S * GEMM_B_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * EWB);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int num_tiles = args.num_m * args.num_n;
+    const int nk = (args.K + GEMM_BK - 1) / GEMM_BK;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        if (EPI == EPI_GLU) tma_prefetch(&tmB2);
+        if (EPI != EPI_F32) tma_prefetch(&tmOut);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int mb, nb;
+                gemm_tile_coords(tile, args.num_m, args.num_n, mb, nb);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], GEMM_STAGE_BYTES);
+                    tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, pol);
+                    if (EPI == EPI_GLU) {
+                        tma_load_2d(stB + stage * GEMM_B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * 128, pol);
+                        tma_load_2d(stB + stage * GEMM_B_BYTES + GEMM_B_BYTES / 2, &tmB2, &full[stage], kb * GEMM_BK,
+                                    nb * 128, pol);
+                    } else {
+                        tma_load_2d(stB + stage * GEMM_B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN, pol);
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, GEMM_BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
+                    const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < GEMM_BK / 16; ++k)
+                        umma_f16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
+                                 (kb | k) != 0);
+                    umma_commit(&empty[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
+        const int ew = warp - 4;  // TMEM lane quarter accessible to this warp (warp % 4)
+        uint8_t* stg = epi + ew * EWB;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int mb, nb;
+            gemm_tile_coords(tile, args.num_m, args.num_n, mb, nb);
+            const int row0 = mb * GEMM_BM + ew * 32;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
+            if (EPI != EPI_F32) {
+                if (lane == 0) bulk_wait_read0();  // staging buffer free (previous TMA store has read it)
+                __syncwarp();
+            }
+            if constexpr (EPI == EPI_TWELL) {
+                constexpr int ROW_WORDS = GEMM_BN / C;
+                const int T = args.T;
+                const int WPT = T / C;
+                const int cap = WPT - 1;
+                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * ROW_WORDS;
+                const int col_base = nb * GEMM_BN;
+                const bool row_ok = row0 + lane < args.M;
+                int z = 0;
+#pragma unroll 1
+                for (int ch = 0; ch < GEMM_BN / 32; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tb + ch * 32, v);
+                    tmem_wait_ld();
+                    const int tcol = ch * 32;
+                    if (tcol % T == 0) z = 0;
+                    uint32_t* blk = srow + (tcol / T) * WPT;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float f = __uint_as_float(v[i]);
+                        if (f > 0.0f) {  // Alg.1 line 11 (strict)
+                            if (z < cap) {
+                                const uint32_t bf = __bfloat16_as_ushort(__float2bfloat16_rn(f));
+                                blk[1 + z] = static_cast<uint32_t>(col_base + tcol + i) | (bf << 16);
+                            }
+                            ++z;
+                        }
+                    }
+                    if ((tcol + 32) % T == 0) {
+                        blk[0] = static_cast<uint32_t>(z);  // Alg.1 line 17: true count
+                        if (z > cap && row_ok && args.overflow) atomicAdd(args.overflow, 1u);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmOut, stg, nb * ROW_WORDS, row0);
+                    bulk_commit();
+                }
+            } else if constexpr (EPI == EPI_F32) {
+                const int row = row0 + lane;
+#pragma unroll 1
+                for (int ch = 0; ch < GEMM_BN / 32; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tb + ch * 32, v);
+                    tmem_wait_ld();
+                    const int col = nb * GEMM_BN + ch * 32;
+                    if (row < args.M) {
+                        float* o = args.out_f32 + static_cast<int64_t>(row) * args.ld_out + col;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if (col + 4 * j < args.N)
+                                *reinterpret_cast<uint4*>(o + 4 * j) = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+            } else if constexpr (EPI == EPI_GLU) {
+                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;  // 128 bf16 per row
+#pragma unroll 1
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t g[32], u[32];
+                    tmem_ld32(tb + ch * 32, g);
+                    tmem_ld32(tb + 128 + ch * 32, u);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float h0 = fmaxf(__uint_as_float(g[2 * j]), 0.0f) * __uint_as_float(u[2 * j]);
+                        const float h1 = fmaxf(__uint_as_float(g[2 * j + 1]), 0.0f) * __uint_as_float(u[2 * j + 1]);
+                        srow[ch * 16 + j] = pack_bf16x2(h0, h1);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmOut, stg, nb * 128, row0);
+                    bulk_commit();
+                }
+            } else {  // EPI_BF16
+                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                    if (half == 1) {
+                        if (lane == 0) bulk_wait_read0();
+                        __syncwarp();
+                    }
+#pragma unroll 1
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[32];
+                        tmem_ld32(tb + half * 128 + ch * 32, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            srow[ch * 16 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                    }
+                    if (half == 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    }
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmOut, stg, nb * GEMM_BN + half * 128, row0);
+                        bulk_commit();
+                    }
+                }
+            }
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (lane == 0) bulk_wait0();
+    }
+
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+}  // namespace sffn

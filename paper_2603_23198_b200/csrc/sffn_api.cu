@@ -1,0 +1,313 @@
+// sffn_api.cu — host side of the C ABI declared in include/sffn.h: argument validation, TMA tensor-map
+// encoding (cuTensorMapEncodeTiled via the runtime's driver entry point, no -lcuda), launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/sffn.h"
+#include "gemm_tc.cuh"
+#include "updown.cuh"
+
+using namespace sffn;
+
+namespace {
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_encodeTiled_t>(p);
+    }();
+    return fn;
+}
+
+// 2-D row-major tensor [outer, inner] of `esize`-byte elements, box [box_outer, box_inner].
+bool tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* ptr, uint64_t inner, uint64_t outer,
+             uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+    PFN_encodeTiled_t enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * static_cast<uint64_t>(esize)};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+struct DevInfo {
+    int sms = 0;
+    int major = 0;
+};
+DevInfo dev_info() {
+    int dev = 0;
+    DevInfo d;
+    if (cudaGetDevice(&dev) != cudaSuccess) return d;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+    return d;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bool valid_TC(int T, int C) {
+    if (!(T == 32 || T == 64 || T == 128 || T == 256)) return false;
+    if (!(C == 1 || C == 2 || C == 4 || C == 8 || C == 16)) return false;
+    return T / C >= 2;
+}
+
+template <int EPI, int C>
+int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const CUtensorMap& o,
+                GemmArgs args, int n_tile_cols, cudaStream_t st) {
+    auto kern = gemm_tc_kernel<EPI, C>;
+    constexpr int smem = gemm_smem_bytes<EPI, C>();
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+    if (attr_err != cudaSuccess) return SFFN_ERR_CUDA;
+    args.num_m = (args.M + GEMM_BM - 1) / GEMM_BM;
+    args.num_n = (args.N + n_tile_cols - 1) / n_tile_cols;
+    const int tiles = args.num_m * args.num_n;
+    if (tiles == 0) return SFFN_OK;
+    DevInfo d = dev_info();
+    const int grid = tiles < d.sms ? tiles : d.sms;
+    kern<<<grid, GEMM_THREADS, smem, st>>>(a, b, b2, o, args);
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int check_device() {
+    DevInfo d = dev_info();
+    if (d.sms == 0) return SFFN_ERR_CUDA;
+    if (d.major != 10) return SFFN_ERR_UNSUPPORTED;
+    return SFFN_OK;
+}
+
+int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
+              uint32_t* d_overflow, cudaStream_t st) {
+    CUtensorMap ta, tb, to;
+    if (!tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, GEMM_BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, twell, N / C, M, GEMM_BN / C, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return SFFN_ERR_CUDA;
+    GemmArgs args{};
+    args.M = static_cast<int>(M);
+    args.N = static_cast<int>(N);
+    args.K = static_cast<int>(K);
+    args.T = T;
+    args.overflow = d_overflow;
+    switch (C) {
+        case 1: return launch_gemm<EPI_TWELL, 1>(ta, tb, tb, to, args, GEMM_BN, st);
+        case 2: return launch_gemm<EPI_TWELL, 2>(ta, tb, tb, to, args, GEMM_BN, st);
+        case 4: return launch_gemm<EPI_TWELL, 4>(ta, tb, tb, to, args, GEMM_BN, st);
+        case 8: return launch_gemm<EPI_TWELL, 8>(ta, tb, tb, to, args, GEMM_BN, st);
+        case 16: return launch_gemm<EPI_TWELL, 16>(ta, tb, tb, to, args, GEMM_BN, st);
+    }
+    return SFFN_ERR_INVALID_ARG;
+}
+
+int pack_checks(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, const void* out) {
+    if (!X || !Wg || !out) return SFFN_ERR_INVALID_ARG;
+    if (!aligned16(X) || !aligned16(Wg) || !aligned16(out)) return SFFN_ERR_INVALID_ARG;
+    if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || K < 64 || K % 64 != 0 || N <= 0 || N % T != 0 || N % 16 != 0 || N > 65536) return SFFN_ERR_SHAPE;
+    if (M > (int64_t(1) << 31) - GEMM_BM || K > (int64_t(1) << 30)) return SFFN_ERR_SHAPE;
+    return SFFN_OK;
+}
+
+int updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                int T, int C, void* Y, cudaStream_t st) {
+    if (M == 0) return SFFN_OK;
+    const int64_t K8 = K / 8;
+    const int64_t per_warp = (K8 + UD_WARPS - 1) / UD_WARPS;  // chunks per warp
+    const int nch_needed = static_cast<int>((per_warp + 31) / 32);
+    dim3 grid(static_cast<unsigned>(M)), block(UD_WARPS * 32);
+    const uint4* x = static_cast<const uint4*>(X);
+    const uint4* wu = static_cast<const uint4*>(Wu);
+    const uint4* wd = static_cast<const uint4*>(Wd);
+    uint4* y = static_cast<uint4*>(Y);
+    if (nch_needed <= 1)
+        updown_kernel<1><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch_needed <= 2)
+        updown_kernel<2><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch_needed <= 4)
+        updown_kernel<4><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch_needed <= 8)
+        updown_kernel<8><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else
+        return SFFN_ERR_SHAPE;
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                  int T, int C, const void* Y) {
+    if (!X || !tw || !Wu || !Wd || !Y) return SFFN_ERR_INVALID_ARG;
+    if (!aligned16(X) || !aligned16(tw) || !aligned16(Wu) || !aligned16(Wd) || !aligned16(Y))
+        return SFFN_ERR_INVALID_ARG;
+    if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || K < 64 || K % 64 != 0 || K > 8192 || N <= 0 || N % T != 0 || N > 65536) return SFFN_ERR_SHAPE;
+    if (M > 2147483647) return SFFN_ERR_SHAPE;
+    return SFFN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sffn_status_string(int s) {
+    switch (s) {
+        case SFFN_OK: return "SFFN_OK";
+        case SFFN_ERR_INVALID_ARG: return "SFFN_ERR_INVALID_ARG";
+        case SFFN_ERR_SHAPE: return "SFFN_ERR_SHAPE";
+        case SFFN_ERR_TILE_OVERFLOW: return "SFFN_ERR_TILE_OVERFLOW";
+        case SFFN_ERR_CUDA: return "SFFN_ERR_CUDA";
+        case SFFN_ERR_NCCL: return "SFFN_ERR_NCCL";
+        case SFFN_ERR_UNSUPPORTED: return "SFFN_ERR_UNSUPPORTED";
+    }
+    return "SFFN_ERR_UNKNOWN";
+}
+
+const char* sffn_version(void) { return "sffn 0.1 (sm_100a tcgen05/TMEM/TMA)"; }
+
+int64_t sffn_twell_words(int64_t M, int64_t N, int T, int C) {
+    if (M < 0 || N < 0 || C <= 0 || T <= 0) return -1;
+    (void)T;
+    return M * (N / C);
+}
+
+size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C) {
+    int64_t w = sffn_twell_words(M, N, T, C);
+    return w < 0 ? 0 : static_cast<size_t>(w) * 4;
+}
+
+int sffn_pack(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
+              uint32_t* d_overflow, void* stream) {
+    int r = pack_checks(X, Wg, M, K, N, T, C, twell);
+    if (r != SFFN_OK) return r;
+    if ((r = check_device()) != SFFN_OK) return r;
+    if (M == 0) return SFFN_OK;
+    return pack_impl(X, Wg, M, K, N, T, C, twell, d_overflow, S(stream));
+}
+
+int sffn_unpack(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int64_t col_offset, int64_t ld_dense,
+                void* dense, void* stream) {
+    if (!twell || !dense) return SFFN_ERR_INVALID_ARG;
+    if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || N <= 0 || N % T != 0 || N > 65536 || col_offset < 0 || ld_dense < col_offset + N)
+        return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    const int64_t warps = M * (N / T);
+    if (warps == 0) return SFFN_OK;
+    const int64_t blocks = (warps * 32 + 255) / 256;
+    if (blocks > 2147483647) return SFFN_ERR_SHAPE;
+    unpack_kernel<<<static_cast<unsigned>(blocks), 256, 0, S(stream)>>>(twell, (int)M, (int)N, T, C, col_offset,
+                                                                         ld_dense, static_cast<__nv_bfloat16*>(dense));
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                 int T, int C, void* Y, void* stream) {
+    int r = updown_checks(X, twell, Wu, Wd, M, K, N, T, C, Y);
+    if (r != SFFN_OK) return r;
+    if ((r = check_device()) != SFFN_OK) return r;
+    return updown_impl(X, twell, Wu, Wd, M, K, N, T, C, Y, S(stream));
+}
+
+int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N, int T,
+                 int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, void* stream) {
+    int r = pack_checks(X, Wg, M, K, N, T, C, workspace);
+    if (r != SFFN_OK) return r;
+    if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
+    if (ws_bytes < sffn_forward_workspace_bytes(M, N, T, C)) return SFFN_ERR_SHAPE;
+    if ((r = check_device()) != SFFN_OK) return r;
+    if (M == 0) return SFFN_OK;
+    uint32_t* tw = static_cast<uint32_t*>(workspace);
+    if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
+    return updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, S(stream));
+}
+
+int sffn_dense_forward(const void* X, const void* Wg, const void* Wu, const void* WdT, int64_t M, int64_t K, int64_t N,
+                       void* H, void* Y, void* stream) {
+    if (!X || !Wg || !Wu || !WdT || !H || !Y) return SFFN_ERR_INVALID_ARG;
+    if (!aligned16(X) || !aligned16(Wg) || !aligned16(Wu) || !aligned16(WdT) || !aligned16(H) || !aligned16(Y))
+        return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || K < 64 || K % 64 != 0 || N < 128 || N % 128 != 0) return SFFN_ERR_SHAPE;
+    if (M > (int64_t(1) << 31) - GEMM_BM || K > (int64_t(1) << 30) || N > (int64_t(1) << 30)) return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    if (M == 0) return SFFN_OK;
+    CUtensorMap tx, tg, tu, th_out, th_in, twd, ty;
+    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&th_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, H, N, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !tmap_2d(&th_in, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, H, N, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, WdT, N, K, GEMM_BK, GEMM_BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, K, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return SFFN_ERR_CUDA;
+    GemmArgs a1{};
+    a1.M = (int)M;
+    a1.N = (int)N;
+    a1.K = (int)K;
+    if ((r = launch_gemm<EPI_GLU, 1>(tx, tg, tu, th_out, a1, 128, S(stream))) != SFFN_OK) return r;
+    GemmArgs a2{};
+    a2.M = (int)M;
+    a2.N = (int)K;
+    a2.K = (int)N;
+    return launch_gemm<EPI_BF16, 1>(th_in, twd, twd, ty, a2, GEMM_BN, S(stream));
+}
+
+int sffn_transpose_bf16(const void* in, int64_t rows, int64_t cols, void* out, void* stream) {
+    if (!in || !out) return SFFN_ERR_INVALID_ARG;
+    if (rows < 0 || cols < 0 || (rows + 31) / 32 > 65535) return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    if (rows == 0 || cols == 0) return SFFN_OK;
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32)), block(32, 8);
+    transpose_bf16_kernel<<<grid, block, 0, S(stream)>>>(static_cast<const __nv_bfloat16*>(in), rows, cols,
+                                                         static_cast<__nv_bfloat16*>(out));
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, float* Sout, void* stream) {
+    if (!X || !Wg || !Sout) return SFFN_ERR_INVALID_ARG;
+    if (!aligned16(X) || !aligned16(Wg) || !aligned16(Sout)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || K < 64 || K % 64 != 0 || N <= 0 || N % 16 != 0) return SFFN_ERR_SHAPE;
+    if (M > (int64_t(1) << 31) - GEMM_BM || N > (int64_t(1) << 30)) return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    if (M == 0) return SFFN_OK;
+    CUtensorMap ta, tb;
+    if (!tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, GEMM_BN, CU_TENSOR_MAP_SWIZZLE_128B))
+        return SFFN_ERR_CUDA;
+    GemmArgs args{};
+    args.M = (int)M;
+    args.N = (int)N;
+    args.K = (int)K;
+    args.out_f32 = Sout;
+    args.ld_out = N;
+    return launch_gemm<EPI_F32, 1>(ta, tb, tb, tb, args, GEMM_BN, S(stream));
+}
+
+int sffn_overflow_check(const uint32_t* d_overflow, void* stream, uint32_t* host_count) {
+    if (!d_overflow) return SFFN_ERR_INVALID_ARG;
+    uint32_t h = 0;
+    if (cudaMemcpyAsync(&h, d_overflow, 4, cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+    if (cudaStreamSynchronize(S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+    if (host_count) *host_count = h;
+    return h ? SFFN_ERR_TILE_OVERFLOW : SFFN_OK;
+}
+
+}  // extern "C"

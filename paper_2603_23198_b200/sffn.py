@@ -1,0 +1,237 @@
+"""Thin ctypes binding over libsffn.so (include/sffn.h) — argument marshalling only.
+
+Every step of the path runs in the library's sm_100a kernels; this module only turns torch tensors into
+device pointers + sizes and the current CUDA stream into a ``cudaStream_t``.  There is no CPU fallback:
+if the shared library is missing or the device is not a B200 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsffn.so")
+
+OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_TILE_OVERFLOW, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(7)
+
+_lib = None
+
+# name -> (restype, argtypes); mirrors include/sffn.h
+_vp, _i64, _int, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+_SIGS = {
+    "sffn_status_string": (ctypes.c_char_p, [_int]),
+    "sffn_version": (ctypes.c_char_p, []),
+    "sffn_twell_words": (_i64, [_i64, _i64, _int, _int]),
+    "sffn_forward_workspace_bytes": (_sz, [_i64, _i64, _int, _int]),
+    "sffn_pack": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp]),
+    "sffn_unpack": (_int, [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp, _vp]),
+    "sffn_up_down": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp]),
+    "sffn_forward": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _vp]),
+    "sffn_dense_forward": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "sffn_transpose_bf16": (_int, [_vp, _i64, _i64, _vp, _vp]),
+    "sffn_gate_gemm_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "sffn_overflow_check": (_int, [_vp, _vp, ctypes.POINTER(ctypes.c_uint32)]),
+    "sffn_comm_unique_id": (_int, [_vp]),
+    "sffn_comm_init": (_int, [ctypes.POINTER(_vp), _int, _int, _vp, _int]),
+    "sffn_comm_destroy": (_int, [_vp]),
+    "sffn_comm_size": (_int, [_vp]),
+    "sffn_sharded_forward": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
+                                    _int, _vp]),
+    "sffn_allreduce_bf16": (_int, [_vp, _vp, _i64, _vp]),
+}
+
+
+class SffnError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build()); "
+                              "there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def status_string(s: int) -> str:
+    return lib().sffn_status_string(s).decode()
+
+
+def version() -> str:
+    return lib().sffn_version().decode()
+
+
+def _chk(status: int, what: str):
+    if status != OK:
+        raise SffnError(status, what)
+
+
+def _p(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("sffn: tensors must be CUDA tensors (device memory)")
+    if not t.is_contiguous():
+        raise ValueError("sffn: tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _bf16(t: torch.Tensor, name: str):
+    if t.dtype != torch.bfloat16:
+        raise TypeError(f"sffn: {name} must be bfloat16, got {t.dtype}")
+    return _p(t)
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def twell_words(M: int, N: int, T: int, C: int) -> int:
+    return int(lib().sffn_twell_words(M, N, T, C))
+
+
+def workspace_bytes(M: int, N: int, T: int, C: int) -> int:
+    return int(lib().sffn_forward_workspace_bytes(M, N, T, C))
+
+
+def pack(x: torch.Tensor, wg: torch.Tensor, T: int = 256, C: int = 8, out: torch.Tensor | None = None,
+         overflow: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """TwELL of relu(x wg^T) (Alg.1).  Returns int32 [M, N/C] holding the packed uint32 words."""
+    M, K = x.shape
+    N = wg.shape[0]
+    if out is None:
+        out = torch.empty((M, N // C), dtype=torch.int32, device=x.device)
+    _chk(lib().sffn_pack(_bf16(x, "x"), _bf16(wg, "wg"), M, K, N, T, C, _p(out), _p(overflow), _stream(stream)),
+         "sffn_pack")
+    return out
+
+
+def unpack(tw: torch.Tensor, N: int, T: int = 256, C: int = 8, out: torch.Tensor | None = None,
+           col_offset: int = 0, stream=None) -> torch.Tensor:
+    M = tw.shape[0]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=tw.device)
+    _chk(lib().sffn_unpack(_p(tw), M, N, T, C, col_offset, out.shape[1], _bf16(out, "out"), _stream(stream)),
+         "sffn_unpack")
+    return out
+
+
+def up_down(x, tw, wu, wd, T: int = 256, C: int = 8, out=None, stream=None) -> torch.Tensor:
+    M, K = x.shape
+    N = wu.shape[0]
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+    _chk(lib().sffn_up_down(_bf16(x, "x"), _p(tw), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
+                            _bf16(out, "out"), _stream(stream)), "sffn_up_down")
+    return out
+
+
+def forward(x, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, overflow=None,
+            stream=None) -> torch.Tensor:
+    """Sparse FFN forward (pack + fused up/down).  workspace: uint8/int32 device buffer >= workspace_bytes."""
+    M, K = x.shape
+    N = wg.shape[0]
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+    if workspace is None:
+        workspace = torch.empty((M, N // C), dtype=torch.int32, device=x.device)
+    _chk(lib().sffn_forward(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
+                            _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(),
+                            _p(overflow), _stream(stream)), "sffn_forward")
+    return out
+
+
+def dense_forward(x, wg, wu, wdT, h=None, out=None, stream=None) -> torch.Tensor:
+    """The library's dense tcgen05 FFN (speedup denominator).  wdT = W_d^T, [K, N]."""
+    M, K = x.shape
+    N = wg.shape[0]
+    if h is None:
+        h = torch.empty((M, N), dtype=torch.bfloat16, device=x.device)
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+    _chk(lib().sffn_dense_forward(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wdT, "wdT"), M, K, N,
+                                  _bf16(h, "h"), _bf16(out, "out"), _stream(stream)), "sffn_dense_forward")
+    return out
+
+
+def transpose(a: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    R, Cc = a.shape
+    if out is None:
+        out = torch.empty((Cc, R), dtype=torch.bfloat16, device=a.device)
+    _chk(lib().sffn_transpose_bf16(_bf16(a, "a"), R, Cc, _bf16(out, "out"), _stream(stream)), "sffn_transpose_bf16")
+    return out
+
+
+def gate_gemm_f32(x, wg, out=None, stream=None) -> torch.Tensor:
+    M, K = x.shape
+    N = wg.shape[0]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=x.device)
+    _chk(lib().sffn_gate_gemm_f32(_bf16(x, "x"), _bf16(wg, "wg"), M, K, N, _p(out), _stream(stream)),
+         "sffn_gate_gemm_f32")
+    return out
+
+
+def overflow_check(overflow: torch.Tensor, stream=None) -> int:
+    """Synchronizes the stream and returns the device overflow count (0 = OK)."""
+    h = ctypes.c_uint32(0)
+    s = lib().sffn_overflow_check(_p(overflow), _stream(stream), ctypes.byref(h))
+    if s not in (OK, ERR_TILE_OVERFLOW):
+        _chk(s, "sffn_overflow_check")
+    return int(h.value)
+
+
+class Comm:
+    """The library's own NCCL communicator for hidden-dim sharding; torch.distributed only broadcasts the id."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+        idt = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            _chk(lib().sffn_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)), "sffn_comm_unique_id")
+            idt = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if world > 1:
+            obj = [idt.tolist()]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            idt = torch.tensor(obj[0], dtype=torch.uint8)
+        raw = (ctypes.c_uint8 * 128)(*idt.tolist())
+        h = ctypes.c_void_p()
+        _chk(lib().sffn_comm_init(ctypes.byref(h), world, rank, ctypes.cast(raw, ctypes.c_void_p), device),
+             "sffn_comm_init")
+        self.h, self.rank, self.world = h, rank, world
+
+    def sharded_forward(self, x, wg_s, wu_s, wd_s, T=256, C=8, out=None, workspace=None, overflow=None,
+                        n_chunks=1, stream=None):
+        M, K = x.shape
+        N_local = wg_s.shape[0]
+        if out is None:
+            out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+        if workspace is None:
+            workspace = torch.empty((M, N_local // C), dtype=torch.int32, device=x.device)
+        _chk(lib().sffn_sharded_forward(self.h, _bf16(x, "x"), _bf16(wg_s, "wg"), _bf16(wu_s, "wu"),
+                                        _bf16(wd_s, "wd"), M, K, N_local, T, C, _bf16(out, "out"), _p(workspace),
+                                        workspace.numel() * workspace.element_size(), _p(overflow), n_chunks,
+                                        _stream(stream)), "sffn_sharded_forward")
+        return out
+
+    def allreduce(self, buf, stream=None):
+        _chk(lib().sffn_allreduce_bf16(self.h, _bf16(buf, "buf"), buf.numel(), _stream(stream)),
+             "sffn_allreduce_bf16")
+        return buf
+
+    def close(self):
+        if self.h:
+            lib().sffn_comm_destroy(self.h)
+            self.h = None

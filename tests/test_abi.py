@@ -1,0 +1,74 @@
+"""CPU-side checks of the C-ABI library: it loads and exports every symbol include/sffn.h declares;
+host-only calls (no device compute) behave as documented."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "sffn.h")
+
+
+def declared_functions():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sffn_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2603_23198_b200 import sffn
+    if not os.path.exists(sffn.LIB_PATH):
+        import subprocess
+        subprocess.check_call(["make", "-C", ROOT, "paper_2603_23198_b200/libsffn.so"])
+    return sffn.lib()
+
+
+def test_header_symbols_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_binding_covers_header():
+    from paper_2603_23198_b200 import sffn
+    assert set(declared_functions()) == set(sffn._SIGS)
+
+
+def test_host_only_calls(lib):
+    from paper_2603_23198_b200 import sffn
+    assert sffn.status_string(0) == "SFFN_OK"
+    assert sffn.status_string(3) == "SFFN_ERR_TILE_OVERFLOW"
+    assert sffn.twell_words(32768, 14336, 256, 8) == 32768 * 1792
+    assert sffn.workspace_bytes(16, 512, 256, 8) == 16 * 64 * 4
+    assert "sm_100a" in sffn.version()
+
+
+def test_argument_errors_before_launch(lib):
+    """Shape / argument errors are reported on the host without touching a device (none here)."""
+    vp = ctypes.c_void_p
+    p = vp(4096)  # never dereferenced: validation fails first
+    # K % 64 != 0 -> SHAPE
+    assert lib.sffn_pack(p, p, 16, 100, 512, 256, 8, p, None, None) == 2
+    # bad C -> INVALID_ARG
+    assert lib.sffn_pack(p, p, 16, 128, 512, 256, 3, p, None, None) == 1
+    # N not a multiple of T -> SHAPE
+    assert lib.sffn_pack(p, p, 16, 128, 500, 256, 8, p, None, None) == 2
+    # NULL -> INVALID_ARG
+    assert lib.sffn_up_down(None, p, p, p, 16, 128, 512, 256, 8, p, None) == 1
+    # misaligned -> INVALID_ARG
+    assert lib.sffn_pack(vp(4098), p, 16, 128, 512, 256, 8, p, None, None) == 1
+    # workspace too small -> SHAPE
+    assert lib.sffn_forward(p, p, p, p, 16, 128, 512, 256, 8, p, p, 10, None, None) == 2
+
+
+def test_product_path_does_not_import_oracle():
+    """The product package must not import, link or call anything under oracle/."""
+    pkg = os.path.join(ROOT, "paper_2603_23198_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                s = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in s and "from oracle" not in s and "oracle_" not in s, f

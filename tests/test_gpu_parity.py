@@ -1,0 +1,230 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same seeded inputs.
+
+Bars (north_star): TwELL counts / indices / values bit-exact (on dyadic-grid inputs the tensor-core
+fp32 accumulation is exact), Y within relative Frobenius 1e-2 (bf16 inputs,
+fp32 accumulation, bf16 output).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import bf16_np, rel_fro, to_dev, twell_invariants, words_np
+
+pytestmark = pytest.mark.gpu
+
+Y_TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def sffn():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_23198_b200 as pkg
+    return pkg
+
+
+def small(name, **kw):
+    return synth.CONFIGS[name].replace(**kw)
+
+
+def inputs(cfg, rows=None):
+    X = synth.gen_x(cfg) if rows is None else synth.gen_x(cfg, 0, rows)
+    return X, synth.gen_w(cfg, "g"), synth.gen_w(cfg, "u"), synth.gen_w(cfg, "d")
+
+
+# ----------------------------------------------------------------- mainloop exactness
+@pytest.mark.parametrize("M,K,N", [(128, 64, 256), (300, 256, 512), (1, 128, 256), (257, 2048, 768), (130, 4096, 272)])
+def test_gate_gemm_exact(sffn, M, K, N):
+    """tcgen05 fp32 accumulators == the oracle's fp64 pre-activation, bitwise, on grid inputs
+    (ragged M, N not a multiple of the 256 tile, K from 64 to 4096)."""
+    cfg = synth.CONFIGS["1B"].replace(M=M, K=K, N=N, Kb=min(64, K // 4))
+    X, Wg = synth.gen_x(cfg), synth.gen_w(cfg, "g")
+    S = sffn.gate_gemm_f32(to_dev(X), to_dev(Wg))
+    torch.cuda.synchronize()
+    A = oracle.gate_preact(X, Wg)
+    assert np.array_equal(S.cpu().numpy().astype(np.float64), A)
+
+
+# ----------------------------------------------------------------- pack (Alg.1 epilogue)
+@pytest.mark.parametrize("T,C", [(32, 2), (32, 1), (64, 4), (128, 8), (256, 8), (256, 4), (256, 16), (256, 1)])
+def test_pack_bitexact(sffn, T, C):
+    cfg = synth.CONFIGS["1B"].replace(M=333, K=512, N=1024, Kb=32, sparsity=0.97, T=T, C=C)
+    X, Wg = synth.gen_x(cfg), synth.gen_w(cfg, "g")
+    ov = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tw = sffn.pack(to_dev(X), to_dev(Wg), T, C, overflow=ov)
+    n_ov = sffn.overflow_check(ov)
+    wg = words_np(tw)
+    wo, counts, n_ov_ref, A = oracle.pack_from_inputs(X, Wg, T, C)
+    assert oracle.valid_prefix_equal(wg, wo, T, C).all()
+    assert n_ov == n_ov_ref
+    twell_invariants(wg, cfg.N, T, C)
+
+
+@pytest.mark.parametrize("name", ["tiny", "1B"])
+def test_pack_configs(sffn, name):
+    """Config-shaped pack: tiny in full; 1B in full M (16384 rows), oracle on a row sample + invariants on all rows."""
+    cfg = synth.CONFIGS[name]
+    X, Wg = synth.gen_x(cfg), synth.gen_w(cfg, "g")
+    tw = words_np(sffn.pack(to_dev(X), to_dev(Wg), cfg.T, cfg.C))
+    twell_invariants(tw, cfg.N, cfg.T, cfg.C)
+    if cfg.M <= 1024:
+        rows = np.arange(cfg.M)
+    else:
+        rng = np.random.default_rng(0)
+        rows = np.unique(np.concatenate([np.arange(64), np.arange(cfg.M - 64, cfg.M), rng.choice(cfg.M, 128, replace=False)]))
+    wo, counts, ov, A = oracle.pack_from_inputs(X[rows], Wg, cfg.T, cfg.C)
+    assert oracle.valid_prefix_equal(tw[rows], wo, cfg.T, cfg.C).all()
+
+
+def test_pack_identity_gate(sffn):
+    """W_g = I (N = K): the pack is plain stream compaction of relu(X)."""
+    cfg = synth.CONFIGS["tiny"].replace(K=256, N=256, Kb=8)
+    X = synth.gen_x(cfg)
+    eye = torch.eye(256, dtype=torch.bfloat16, device="cuda")
+    tw = words_np(sffn.pack(to_dev(X), eye, 32, 1))
+    wo, _, _ = oracle.pack(synth.bf16_to_f32(X), 32, 1)
+    assert oracle.valid_prefix_equal(tw, wo, 32, 1).all()
+
+
+def test_pack_all_negative_and_empty(sffn):
+    cfg = synth.CONFIGS["tiny"]
+    X = torch.ones((130, 64), dtype=torch.bfloat16, device="cuda")
+    Wg = -torch.ones((256, 64), dtype=torch.bfloat16, device="cuda")
+    tw = words_np(sffn.pack(X, Wg, 32, 2))
+    assert (tw.reshape(130, 8, 16)[:, :, 0] == 0).all()
+    # M = 0 is a no-op
+    out = torch.empty((0, 128), dtype=torch.int32, device="cuda")
+    sffn.pack(X[:0], Wg, 32, 2, out=out)
+
+
+def test_pack_forced_overflow(sffn):
+    """A tile with more positives than T/C-1: true count kept, first cap entries in column order,
+    overflow counter incremented (reading R5)."""
+    M, K, N, T, C = 128, 64, 256, 256, 8
+    X = torch.zeros((M, K), dtype=torch.bfloat16, device="cuda")
+    X[:, 0] = 1.0
+    Wg = torch.zeros((N, K), dtype=torch.bfloat16, device="cuda")
+    Wg[::5, 0] = 0.5  # 52 positives per row-tile > 31
+    ov = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tw = words_np(sffn.pack(X, Wg, T, C, overflow=ov))
+    assert sffn.overflow_check(ov) == M
+    wo, _, n = oracle.pack(np.where(np.arange(N) % 5 == 0, 0.5, 0.0)[None, :].repeat(M, 0).astype(np.float32), T, C)
+    assert n == M and oracle.valid_prefix_equal(tw, wo, T, C).all()
+
+
+# ----------------------------------------------------------------- unpack
+def test_unpack_roundtrip(sffn):
+    cfg = synth.CONFIGS["tiny"]
+    X, Wg = synth.gen_x(cfg), synth.gen_w(cfg, "g")
+    tw = sffn.pack(to_dev(X), to_dev(Wg), cfg.T, cfg.C)
+    H = sffn.unpack(tw, cfg.N, cfg.T, cfg.C)
+    A = oracle.gate_preact(X, Wg)
+    relu = np.where(A > 0, A, 0.0).astype(np.float32)
+    ref = torch.from_numpy(relu).to(torch.bfloat16)
+    assert torch.equal(H.cpu().view(torch.int16), ref.view(torch.int16))
+    # col_offset / ld into a wider matrix
+    big = torch.full((cfg.M, cfg.N + 64), 7.0, dtype=torch.bfloat16, device="cuda")
+    sffn.unpack(tw, cfg.N, cfg.T, cfg.C, out=big, col_offset=32)
+    assert torch.equal(big[:, 32:32 + cfg.N].cpu().view(torch.int16), ref.view(torch.int16))
+    assert (big[:, :32] == 7).all() and (big[:, 32 + cfg.N:] == 7).all()
+
+
+# ----------------------------------------------------------------- fused up/down and forward
+@pytest.mark.parametrize("K", [64, 512, 2048, 4096, 8192])
+def test_up_down_vs_oracle(sffn, K):
+    """sffn_up_down fed the ORACLE's TwELL (isolates the kernel): Y vs Eq.3 with the stored bf16 gate."""
+    cfg = synth.CONFIGS["1B"].replace(M=200, K=K, N=1024, Kb=min(64, K // 4), sparsity=0.97)
+    X, Wg, Wu, Wd = inputs(cfg)
+    wo, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    tw = torch.from_numpy(wo.view(np.int32)).cuda()
+    Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), cfg.T, cfg.C)
+    Yref = oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)
+    assert rel_fro(bf16_np(Y), Yref) < Y_TOL
+
+
+@pytest.mark.parametrize("name,M", [("tiny", None), ("1B", 512), ("7B", 160)])
+def test_forward_vs_oracle(sffn, name, M):
+    cfg = synth.CONFIGS[name]
+    if M is not None:
+        cfg = cfg.replace(M=M)
+    X, Wg, Wu, Wd = inputs(cfg)
+    ov = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, overflow=ov)
+    assert sffn.overflow_check(ov) == 0
+    wo, counts, n_ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    Y3 = oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)      # Eq.3 with stored h_v
+    Y1 = oracle.ffn_dense(X, Wg, Wu, Wd)                           # Eq.1
+    y = bf16_np(Y)
+    assert rel_fro(y, Y3) < Y_TOL
+    assert rel_fro(y, Y1) < Y_TOL
+
+
+def test_forward_empty_pattern_is_zero(sffn):
+    X = torch.ones((300, 128), dtype=torch.bfloat16, device="cuda")
+    Wg = -torch.ones((256, 128), dtype=torch.bfloat16, device="cuda")
+    Wu = torch.ones((256, 128), dtype=torch.bfloat16, device="cuda")
+    Y = sffn.forward(X, Wg, Wu, Wu, 256, 8)
+    assert torch.equal(Y.view(torch.int16), torch.zeros_like(Y).view(torch.int16))
+
+
+def test_forward_single_active_neuron(sffn):
+    """One active neuron per row: y_m = bf16(g) * (x_m . W_u[n]) * W_d[n] (closed form), n = m % N."""
+    cfg = synth.CONFIGS["1B"].replace(M=256, K=1024, N=512, Kb=16)
+    X, _, Wu, Wd = inputs(cfg)
+    M, K, N = cfg.M, cfg.K, cfg.N
+    # gate: W_g row n = e_0 * 0.25 for n == target, big negative on channel 0 otherwise; x[:,0] = 1
+    Xf = synth.bf16_to_f32(X).copy()
+    Xf[:, 0] = 1.0
+    Xf[:, 1] = np.arange(M) % N / 64.0  # selects the neuron
+    Xb = torch.from_numpy(Xf).to(torch.bfloat16)
+    Wgf = np.zeros((N, K), dtype=np.float32)
+    # a[m, n] = 0.25 - |x1 - n/64| * big  -> positive only at n == m % N
+    # use two channels: a = x0 * (0.25 - n^2/64^2 ...) is messy; build the TwELL directly instead
+    tw = np.zeros((M, N // 8), dtype=np.uint32)
+    for m in range(M):
+        n = m % N
+        t = n // 256
+        tw[m, t * 32] = 1
+        tw[m, t * 32 + 1] = n | (0x3E80 << 16)  # bf16 0.25
+    Xn = Xb.view(torch.int16).numpy().view(np.uint16)
+    Y = sffn.up_down(to_dev(Xn), torch.from_numpy(tw.view(np.int32)).cuda(), to_dev(Wu), to_dev(Wd), 256, 8)
+    Yref = oracle.ffn_twell(Xn, tw, Wu, Wd, N, 256, 8)
+    assert rel_fro(bf16_np(Y), Yref) < 4e-3
+
+
+def test_forward_ragged_and_tiny_M(sffn):
+    for M in (1, 127, 129, 383):
+        cfg = synth.CONFIGS["1B"].replace(M=M, K=256, N=512, Kb=16, sparsity=0.95)
+        X, Wg, Wu, Wd = inputs(cfg)
+        Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8)
+        wo, _, _, _ = oracle.pack_from_inputs(X, Wg, 256, 8)
+        assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8)) < Y_TOL
+
+
+# ----------------------------------------------------------------- dense baseline
+@pytest.mark.parametrize("name,M", [("tiny", None), ("1B", 256)])
+def test_dense_forward_vs_oracle(sffn, name, M):
+    cfg = synth.CONFIGS[name]
+    if M is not None:
+        cfg = cfg.replace(M=M)
+    X, Wg, Wu, Wd = inputs(cfg)
+    wdT = sffn.transpose(to_dev(Wd))
+    assert torch.equal(wdT.cpu(), to_dev(Wd).cpu().t().contiguous())
+    Y = sffn.dense_forward(to_dev(X), to_dev(Wg), to_dev(Wu), wdT)
+    Y1 = oracle.ffn_dense(X, Wg, Wu, Wd)
+    assert rel_fro(bf16_np(Y), Y1) < Y_TOL
+
+
+def test_errors_do_not_launch(sffn):
+    x = torch.zeros((8, 100), dtype=torch.bfloat16, device="cuda")
+    w = torch.zeros((256, 100), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(sffn.SffnError) as e:
+        sffn.pack(x, w, 256, 8)
+    assert e.value.status == 2  # K % 64
+    x = torch.zeros((8, 128), dtype=torch.bfloat16, device="cuda")
+    w = torch.zeros((256, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(sffn.SffnError) as e:
+        sffn.pack(x, w, 256, 3)
+    assert e.value.status == 1
