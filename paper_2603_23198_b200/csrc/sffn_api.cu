@@ -117,6 +117,7 @@ int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, in
 }
 
 int pack_checks(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, const void* out) {
+    if (M == 0 && valid_TC(T, C)) X = out = Wg;  // empty batch: X / out may be NULL (nothing is touched)
     if (!X || !Wg || !out) return SFFN_ERR_INVALID_ARG;
     if (!aligned16(X) || !aligned16(Wg) || !aligned16(out)) return SFFN_ERR_INVALID_ARG;
     if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
@@ -151,6 +152,7 @@ int updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* W
 
 int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
                   int T, int C, const void* Y) {
+    if (M == 0) X = tw = Y = Wu;  // empty batch: X / twell / Y may be NULL
     if (!X || !tw || !Wu || !Wd || !Y) return SFFN_ERR_INVALID_ARG;
     if (!aligned16(X) || !aligned16(tw) || !aligned16(Wu) || !aligned16(Wd) || !aligned16(Y))
         return SFFN_ERR_INVALID_ARG;
