@@ -1,0 +1,29 @@
+"""Minimal driver for ncu: one forward (pack + up_down) and one dense forward on a config, after warm-up."""
+import argparse, os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import synth
+import paper_2603_23198_b200 as sffn
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="7B")
+ap.add_argument("--iters", type=int, default=2)
+ap.add_argument("--dense", action="store_true")
+a = ap.parse_args()
+cfg = synth.CONFIGS[a.config]
+dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
+X = dev(synth.gen_x(cfg)); Wg, Wu, Wd = (dev(synth.gen_w(cfg, w)) for w in "gud")
+ws = torch.empty((cfg.M, cfg.N // cfg.C), dtype=torch.int32, device="cuda")
+Y = torch.empty((cfg.M, cfg.K), dtype=torch.bfloat16, device="cuda")
+for _ in range(a.iters):
+    sffn.pack(X, Wg, cfg.T, cfg.C, out=ws)
+    sffn.up_down(X, ws, Wu, Wd, cfg.T, cfg.C, out=Y)
+if a.dense:
+    wdT = sffn.transpose(Wd)
+    H = torch.empty((cfg.M, cfg.N), dtype=torch.bfloat16, device="cuda")
+    for _ in range(a.iters):
+        sffn.dense_forward(X, Wg, Wu, wdT, h=H, out=Y)
+torch.cuda.synchronize()
+print("done")
