@@ -162,6 +162,7 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunks", type=int, default=4, help="M chunks overlapping compute and all-reduce (N>1)")
+    ap.add_argument("--algo", default="auto", choices=["auto", "gather", "union"], help="fused up/down algorithm")
     ap.add_argument("--json-out", default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -200,7 +201,9 @@ def main():
     X = to_dev(X_host)
     Wg, Wu, Wd = (to_dev(synth.gen_w(cfg, w, n0, Nl)) for w in "gud")
     Y = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
-    ws = torch.empty((M, Nl // C), dtype=torch.int32, device=dev)
+    ws = torch.empty(sffn.workspace_bytes(M, Nl, T, C, args.algo), dtype=torch.uint8, device=dev)
+    tw_view = sffn.twell_view(ws, M, Nl, C)
+    ud_ws = torch.empty(max(16, sffn.up_down_workspace_bytes(M, Nl, T, C, args.algo)), dtype=torch.uint8, device=dev)
     ov = torch.zeros(1, dtype=torch.int32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -208,9 +211,10 @@ def main():
 
     def step():
         if comm is None:
-            sffn.forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov)
+            sffn.forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
         else:
-            comm.sharded_forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, n_chunks=args.chunks)
+            comm.sharded_forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo,
+                                 n_chunks=args.chunks)
 
     def barrier():
         if world > 1:
@@ -249,11 +253,13 @@ def main():
 
     # ------------------------------------------------------------------ per-kernel timing (roofline)
     peaks = load_peaks()
-    ms_pack = timed(lambda: sffn.pack(X, Wg, T, C, out=ws), max(5, args.steps // 2), 3)
-    ms_ud = timed(lambda: sffn.up_down(X, ws, Wu, Wd, T, C, out=Y), max(5, args.steps // 2), 3)
+    tw = torch.empty((M, Nl // C), dtype=torch.int32, device=dev)
+    ms_pack = timed(lambda: sffn.pack(X, Wg, T, C, out=tw), max(5, args.steps // 2), 3)
+    ms_ud = timed(lambda: sffn.up_down(X, tw, Wu, Wd, T, C, out=Y, workspace=ud_ws, algo=args.algo),
+                  max(5, args.steps // 2), 3)
     t_pack = float(np.median(ms_pack)) / 1e3
     t_ud = float(np.median(ms_ud)) / 1e3
-    twords = ws.cpu().numpy().view(np.uint32).reshape(M, Nl // T, T // C)
+    twords = tw.cpu().numpy().view(np.uint32).reshape(M, Nl // T, T // C)
     nnz_total = int(np.minimum(twords[:, :, 0], T // C - 1).sum())
     gate_flop = 2.0 * M * K * Nl
     ud_flop = 4.0 * K * nnz_total
@@ -305,7 +311,7 @@ def main():
 
         def e2e_step():
             Xd.copy_(Xh, non_blocking=True)
-            sffn.forward(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov)
+            sffn.forward(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
             Yh.copy_(Y, non_blocking=True)
 
         ms_e = timed(e2e_step, max(3, args.steps // 3), 3)

@@ -52,6 +52,17 @@ typedef enum {
     SFFN_ERR_UNSUPPORTED = 6    /* not a B200 (sm_100) device, or a feature not built                   */
 } sffn_status;
 
+/* Algorithm of the fused sparse up/down (Alg.2 / Eq.3).  Both compute the same Eq.3 sum:
+ *   SFFN_ALGO_GATHER: one CTA per token row, fp32 FMA over coalesced 16-byte gathers of the active
+ *                     W_u / W_d rows (the paper's Listing 2 design); needs no workspace.
+ *   SFFN_ALGO_UNION : per block of 128 rows, the union U_b of their active neurons; the up projection
+ *                     X_b W_u[U_b]^T and the down projection H_b W_d[U_b] run on tcgen05 tensor cores
+ *                     with the gate applied in the epilogue (zero off-pattern, so skipped terms are
+ *                     exactly the h_g = 0 terms of Alg.2); W_u / W_d rows gathered by TMA gather4.
+ *                     Needs workspace (sffn_up_down_workspace_bytes) and N % 64 == 0.
+ *   SFFN_ALGO_AUTO  : UNION when N % 64 == 0, else GATHER. */
+typedef enum { SFFN_ALGO_AUTO = 0, SFFN_ALGO_GATHER = 1, SFFN_ALGO_UNION = 2 } sffn_algo;
+
 /* Human-readable name of a status code (static storage). */
 const char* sffn_status_string(int status);
 /* Library version / build string (static storage). */
@@ -59,8 +70,11 @@ const char* sffn_version(void);
 
 /* Number of uint32 words of a packed TwELL for [M, N] with tile T and compression C: M * N / C. */
 int64_t sffn_twell_words(int64_t M, int64_t N, int T, int C);
-/* Bytes of device workspace sffn_forward needs (the TwELL of the gate): 4 * sffn_twell_words. */
-size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C);
+/* Bytes of device workspace sffn_up_down needs for `algo` (0 for GATHER). */
+size_t sffn_up_down_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo);
+/* Bytes of device workspace sffn_forward needs: the TwELL of the gate (4 * sffn_twell_words, rounded
+ * to 1 KiB) followed by the up/down workspace of `algo`. */
+size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo);
 
 /*
  * sffn_pack — Alg.1: TwELL of relu(X W_g^T), computed by a tcgen05/TMEM tensor-core GEMM
@@ -87,19 +101,24 @@ int sffn_unpack(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int64
 /*
  * sffn_up_down — Alg.2 / Eq.3 from an existing TwELL:
  *   Y[m, :] = sum_t sum_{c < min(h_nz, T/C-1)} h_v * (X[m, :] . Wu[n, :]) * Wd[n, :]
- * h_v = the stored bf16 gate value; products and sums in fp32 (FMA); Y rounded to bf16 (RN).
+ * h_v = the stored bf16 gate value; fp32 accumulation; Y rounded to bf16 (RN).  GATHER keeps h = h_v * u
+ * in fp32; UNION rounds h to bf16 before the down GEMM (as the paper's kernel does, L2 P:994-1002).
  *   X [M, K] bf16, twell [M, N/C] uint32, Wu [N, K] bf16, Wd [N, K] bf16, Y [M, K] bf16 (output)
+ *   workspace / ws_bytes: >= sffn_up_down_workspace_bytes(M, N, T, C, algo) (may be NULL for GATHER)
+ * Constraints: those of sffn_pack, and K <= 8192 for GATHER.
  */
 int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const void* Wd, int64_t M, int64_t K,
-                 int64_t N, int T, int C, void* Y, void* stream);
+                 int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes, int algo, void* stream);
 
 /*
- * sffn_forward — the whole sparse FFN forward (the paper's two launches):
- * sffn_pack into `workspace` (>= sffn_forward_workspace_bytes) then sffn_up_down.
- * The TwELL left in the workspace is valid after the call (stream-ordered).
+ * sffn_forward — the whole sparse FFN forward: sffn_pack into `workspace` (>= sffn_forward_workspace_bytes)
+ * then sffn_up_down with the rest of the workspace.  GATHER = the paper's two launches; UNION
+ * adds two small metadata launches (4 total).  The TwELL left at the start of the workspace is valid
+ * after the call (stream-ordered).
  */
 int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
-                 int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, void* stream);
+                 int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo,
+                 void* stream);
 
 /*
  * sffn_dense_forward — the library's own dense tcgen05 FFN (Eq.1 without sparsity): the speedup
@@ -143,13 +162,14 @@ int sffn_comm_size(const sffn_comm* comm);
 
 /*
  * sffn_sharded_forward — sffn_forward on the local shard, then one in-place NCCL all-reduce (sum)
- * of Y [M, K] bf16 on `stream`.  With n_chunks > 1 the M dimension is processed in chunks and the
- * all-reduce of chunk i overlaps the compute of chunk i+1 (the library orders them with events on
- * an internal communication stream; still no host synchronization).
+ * of Y [M, K] bf16 on `stream`.  With n_chunks > 1 the M dimension is processed in chunks (multiples
+ * of 128 rows) and the all-reduce of chunk i overlaps the compute of chunk i+1 (the library orders
+ * them with events on an internal communication stream; still no host synchronization).  The
+ * workspace (>= sffn_forward_workspace_bytes(M, N_local, T, C, algo)) is reused chunk after chunk.
  */
 int sffn_sharded_forward(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
                          int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
-                         size_t ws_bytes, uint32_t* d_overflow, int n_chunks, void* stream);
+                         size_t ws_bytes, uint32_t* d_overflow, int algo, int n_chunks, void* stream);
 
 /* Plain in-place all-reduce (sum) of a bf16 buffer on the communicator (used by tests). */
 int sffn_allreduce_bf16(sffn_comm* comm, void* buf, int64_t count, void* stream);

@@ -4,4 +4,5 @@ The compute path is the C-ABI library ``libsffn.so`` (include/sffn.h); ``sffn`` 
 """
 from . import sffn  # noqa: F401
 from .sffn import (Comm, SffnError, dense_forward, forward, gate_gemm_f32, overflow_check, pack,  # noqa: F401
+                   twell_view, up_down_workspace_bytes,
                    transpose, twell_words, unpack, up_down, workspace_bytes)

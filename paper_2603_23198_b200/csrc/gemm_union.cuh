@@ -1,0 +1,365 @@
+// gemm_union.cuh — tensor-core sparse up/down over per-block neuron unions.
+//
+// Eq.3 regrouped: for a block b of 128 token rows and U_b = union of their active neurons,
+//   H_b = G_b ⊙ (X_b · W_u[U_b]^T)        (UP kernel;  G_b = TwELL gate values scattered into U_b
+//                                           coordinates, 0 where (m, n) is not stored)
+//   Y_b = H_b · W_d[U_b, :]               (DOWN kernel)
+// Every term skipped relative to Eq.1 has h_g = 0, exactly as in Alg.2; the terms computed
+// with G = 0 add exact zeros.  Both kernels are persistent warp-specialized tcgen05 GEMMs like
+// gemm_tc.cuh; the weight rows of U_b are gathered by TMA tile::gather4 (4 rows of 128 B per
+// instruction, 128-byte swizzle applied by address, so 4-row groups land directly in UMMA layout):
+//   UP   B operand: W_u[U_b[256c + r], k0:k0+64]       K-major   (gather4 over rows)
+//   DOWN B operand: W_d[U_b[k0 + r], 256j:256j+256]     MN-major  (gather4 over rows, 4 x 64-col atoms)
+#pragma once
+#include "gemm_tc.cuh"
+#include "union.cuh"
+
+namespace sffn {
+
+struct UnionArgs {
+    int M, K, N, T, C;
+    int NB;             // token blocks of 128
+    int NJ;             // DOWN: output column tiles of 256
+    const uint32_t* tw;  // UP: packed TwELL [M, N/C]
+    UnionMeta um;
+};
+
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t col, int32_t r0,
+                                            int32_t r1, int32_t r2, int32_t r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
+// MN-major operand, 128-byte swizzle: 64-element MN atoms LBO apart, 8-row K groups SBO apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+__device__ __forceinline__ int upper_bound_i32(const int32_t* a, int n, int key) {  // first i with a[i] > key
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) <= key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// byte offset of element (r, c) in a [32 rows x 64 bf16] 128B-swizzled TMA box (1024-aligned base)
+__device__ __forceinline__ uint32_t sw128_off(int r, int c) {
+    return static_cast<uint32_t>(r * 128 + ((((c >> 3) ^ r) & 7) << 4) + ((c & 7) << 1));
+}
+
+constexpr int UG_STAGES = 4;
+constexpr int UG_EWB = 8192;  // epilogue staging per warp
+constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 256;
+
+template <bool UP>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    union_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmOut, const UnionArgs args) {
+    constexpr int S = UG_STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stA = smem;
+    uint8_t* stB = smem + S * GEMM_A_BYTES;
+    uint8_t* epi = stB + S * GEMM_B_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * UG_EWB);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int N = args.N;
+    const int NB = args.NB;
+    const int num_tiles = UP ? __ldg(args.um.chunk_off + NB) : NB * args.NJ;
+    const int nk_up = (args.K + GEMM_BK - 1) / GEMM_BK;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        tma_prefetch(&tmOut);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    // tile -> (b, c | j, rows/len)
+    auto tile_info = [&](int tile, int& b, int& cj, int& len) {
+        if (UP) {
+            b = upper_bound_i32(args.um.chunk_off, NB + 1, tile) - 1;
+            cj = tile - __ldg(args.um.chunk_off + b);
+            len = min(256, __ldg(args.um.ulen + b) - 256 * cj);  // rows of this chunk (multiple of 64)
+        } else {
+            b = tile / args.NJ;
+            cj = tile - b * args.NJ;
+            len = __ldg(args.um.ulen + b);  // reduction length (multiple of 64)
+        }
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer (whole warp issues gathers)
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int b, cj, len;
+            tile_info(tile, b, cj, len);
+            const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
+            if (UP) {
+                // lane l gathers chunk rows 8l .. 8l+7 (two groups of 4)
+                int idx[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int r = 8 * lane + i;
+                    idx[i] = r < len ? __ldg(ul + 256 * cj + r) : 0;
+                }
+                for (int kb = 0; kb < nk_up; ++kb) {
+                    if (lane == 0) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES + len * 128);
+                        tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
+                                    policy_evict_last());
+                    }
+                    __syncwarp();
+                    if (8 * lane < len) {
+                        uint8_t* dst = stB + stage * GEMM_B_BYTES + 8 * lane * 128;
+                        tma_gather4(dst, &tmB, &full[stage], kb * GEMM_BK, idx[0], idx[1], idx[2], idx[3]);
+                        tma_gather4(dst + 512, &tmB, &full[stage], kb * GEMM_BK, idx[4], idx[5], idx[6], idx[7]);
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            } else {
+                // lane l: row group g = l % 16 (rows 4g..4g+3 of the k-block), MN atoms 2*(l/16) and +1
+                const int g = lane & 15, mn0 = (lane >> 4) * 2;
+                const int nk = len / GEMM_BK;
+                int idx[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) idx[i] = __ldg(ul + 4 * g + i);
+                for (int kb = 0; kb < nk; ++kb) {
+                    int nxt[4];
+                    const int kn = kb + 1 < nk ? kb + 1 : kb;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + 4 * g + i);
+                    if (lane == 0) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES + GEMM_B_BYTES);
+                        tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
+                                    policy_evict_last());
+                    }
+                    __syncwarp();
+                    uint8_t* dst = stB + stage * GEMM_B_BYTES + g * 512;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        tma_gather4(dst + (mn0 + q) * 8192, &tmB, &full[stage], cj * 256 + (mn0 + q) * 64, idx[0],
+                                    idx[1], idx[2], idx[3]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) idx[i] = nxt[i];
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int b, cj, len;
+                tile_info(tile, b, cj, len);
+                const int nk = UP ? nk_up : len / GEMM_BK;
+                const uint32_t idesc = UP ? umma_idesc_bf16(GEMM_BM, len) : (umma_idesc_bf16(GEMM_BM, 256) | (1u << 16));
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
+                    const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < GEMM_BK / 16; ++k) {
+                        const uint64_t bd = UP ? umma_desc_sw128(b0 + k * 32) : umma_desc_sw128_mn(b0 + k * 2048, 8192, 1024);
+                        umma_f16(d, umma_desc_sw128(a0 + k * 32), bd, idesc, (kb | k) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
+        const int ew = warp - 4;
+        uint8_t* stg = epi + ew * UG_EWB;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const int NW = N >> 5;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int b, cj, len;
+            tile_info(tile, b, cj, len);
+            const int row0 = b * GEMM_BM + ew * 32;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
+            if constexpr (UP) {
+                // union positions [p0, p0 + len) of block b; this thread's row m
+                const int m = row0 + lane;
+                const int p0 = 256 * cj;
+                const int nreal = min(len, __ldg(args.um.utot + b) - p0);
+                const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
+                const uint32_t* msk = args.um.umask + static_cast<int64_t>(b) * NW;
+                const int32_t* wof = args.um.uwoff + static_cast<int64_t>(b) * NW;
+                int t_lo = 1, t_hi = 0, n_lo = 0, n_hi = -1;
+                if (nreal > 0) {
+                    n_lo = __ldg(ul + p0);
+                    n_hi = __ldg(ul + p0 + nreal - 1);
+                    t_lo = n_lo / args.T;
+                    t_hi = n_hi / args.T;
+                }
+                const int WPT = args.T / args.C, cap = WPT - 1;
+                const uint32_t* trow = args.tw + static_cast<int64_t>(m) * (N / args.C);
+                const bool row_ok = m < args.M;
+#pragma unroll 1
+                for (int h = 0; h < 2 && 128 * h < len; ++h) {
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+                    // zero this row in both 64-column boxes
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+#pragma unroll
+                        for (int c16 = 0; c16 < 8; ++c16)
+                            *reinterpret_cast<uint4*>(stg + q * 4096 + lane * 128 + c16 * 16) = make_uint4(0, 0, 0, 0);
+                    // scatter the stored gate values whose union position falls in this half
+                    if (row_ok) {
+                        for (int t = t_lo; t <= t_hi; ++t) {
+                            const uint32_t* blk = trow + static_cast<int64_t>(t) * WPT;
+                            const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+                            for (int e = 0; e < cnt; ++e) {
+                                const uint32_t w = __ldg(blk + 1 + e);
+                                const int n = static_cast<int>(w & 0xFFFFu);
+                                if (n < n_lo || n > n_hi) continue;
+                                const int wi = n >> 5;
+                                const int j = __ldg(wof + wi) + __popc(__ldg(msk + wi) & ((1u << (n & 31)) - 1u)) - p0;
+                                if ((j >> 7) != h) continue;
+                                const int c = j & 127;
+                                *reinterpret_cast<uint16_t*>(stg + (c >> 6) * 4096 + sw128_off(lane, c & 63)) =
+                                    static_cast<uint16_t>(w >> 16);
+                            }
+                        }
+                    }
+                    // h = g * u  (only where g != 0: columns past `len` hold stale TMEM)
+#pragma unroll 1
+                    for (int q32 = 0; q32 < 4; ++q32) {
+                        uint32_t v[32];
+                        tmem_ld32(tb + 128 * h + 32 * q32, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int p = 0; p < 16; ++p) {
+                            const int c = 32 * q32 + 2 * p;  // column within the half
+                            uint32_t* sp = reinterpret_cast<uint32_t*>(stg + (c >> 6) * 4096 + sw128_off(lane, c & 63));
+                            const uint32_t gg = *sp;
+                            if (gg) {
+                                const float g0 = __uint_as_float(gg << 16), g1 = __uint_as_float(gg & 0xFFFF0000u);
+                                const float h0 = (gg & 0xFFFFu) ? g0 * __uint_as_float(v[2 * p]) : 0.0f;
+                                const float h1 = (gg >> 16) ? g1 * __uint_as_float(v[2 * p + 1]) : 0.0f;
+                                *sp = pack_bf16x2(h0, h1);
+                            }
+                        }
+                    }
+                    if (h == 1 || 128 * (h + 1) >= len) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    }
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int q = 0; q < 2; ++q)
+                            if (128 * h + 64 * q < len) tma_store_2d(&tmOut, stg + q * 4096, p0 + 128 * h + 64 * q, row0);
+                        bulk_commit();
+                    }
+                }
+            } else {
+                // DOWN: plain bf16 store of the 128 x 256 tile (two halves of 128 columns)
+                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+#pragma unroll 1
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[32];
+                        tmem_ld32(tb + half * 128 + ch * 32, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            srow[ch * 16 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                    }
+                    if (half == 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    }
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmOut, stg, cj * 256 + half * 128, row0);
+                        bulk_commit();
+                    }
+                }
+            }
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (lane == 0) bulk_wait0();
+    }
+
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+}  // namespace sffn

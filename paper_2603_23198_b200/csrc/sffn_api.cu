@@ -9,6 +9,7 @@
 
 #include "../../include/sffn.h"
 #include "gemm_tc.cuh"
+#include "gemm_union.cuh"
 #include "updown.cuh"
 
 using namespace sffn;
@@ -162,6 +163,110 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
     return SFFN_OK;
 }
 
+
+// ---------------------------------------------------------------- block-union tensor-core up/down
+inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
+
+struct UnionWs {
+    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, total;
+};
+UnionWs union_ws_layout(int64_t M, int64_t N) {
+    const int64_t NB = (M + 127) / 128;
+    UnionWs w{};
+    int64_t o = 0;
+    w.hc = o;    o = align1k(o + NB * 128 * N * 2);
+    w.ulist = o; o = align1k(o + NB * N * 4);
+    w.ulen = o;  o = align1k(o + NB * 4);
+    w.utot = o;  o = align1k(o + NB * 4);
+    w.umask = o; o = align1k(o + NB * (N / 32) * 4);
+    w.uwoff = o; o = align1k(o + NB * (N / 32) * 4);
+    w.chunk = o; o = align1k(o + (NB + 1) * 4);
+    w.total = o;
+    return w;
+}
+
+bool union_applicable(int64_t N) { return N % 64 == 0 && N >= 64; }
+
+int resolve_algo(int algo, int64_t N) {
+    if (algo == SFFN_ALGO_AUTO) return union_applicable(N) ? SFFN_ALGO_UNION : SFFN_ALGO_GATHER;
+    return algo;
+}
+
+size_t updown_ws_bytes(int64_t M, int64_t N, int algo) {
+    if (resolve_algo(algo, N) != SFFN_ALGO_UNION || M <= 0) return 0;
+    return static_cast<size_t>(union_ws_layout(M, N).total);
+}
+
+int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
+                      int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st) {
+    const int64_t NB = (M + 127) / 128;
+    UnionWs L = union_ws_layout(M, N);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    UnionMeta um;
+    um.ulist = reinterpret_cast<int32_t*>(base + L.ulist);
+    um.ulen = reinterpret_cast<int32_t*>(base + L.ulen);
+    um.utot = reinterpret_cast<int32_t*>(base + L.utot);
+    um.umask = reinterpret_cast<uint32_t*>(base + L.umask);
+    um.uwoff = reinterpret_cast<int32_t*>(base + L.uwoff);
+    um.chunk_off = reinterpret_cast<int32_t*>(base + L.chunk);
+    void* hc = base + L.hc;
+
+    const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
+    union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um);
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    union_scan_kernel<<<1, 1024, 0, st>>>(um, (int)NB);
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+
+    CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
+    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&thc_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, GEMM_BK, GEMM_BM,
+                 CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wd, K, N, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, K, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return SFFN_ERR_CUDA;
+    UnionArgs ua{};
+    ua.M = (int)M;
+    ua.K = (int)K;
+    ua.N = (int)N;
+    ua.T = T;
+    ua.C = C;
+    ua.NB = (int)NB;
+    ua.NJ = (int)((K + 255) / 256);
+    ua.tw = tw;
+    ua.um = um;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+        attr = cudaFuncSetAttribute(union_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UG_SMEM);
+        if (attr == cudaSuccess)
+            attr = cudaFuncSetAttribute(union_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UG_SMEM);
+    });
+    if (attr != cudaSuccess) return SFFN_ERR_CUDA;
+    const int sms = dev_info().sms;
+    // UP: the number of (block, chunk) tiles is only known on the device; persistent grid
+    union_gemm_kernel<true><<<sms, GEMM_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua);
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    const int64_t dtiles = NB * ua.NJ;
+    const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
+    union_gemm_kernel<false><<<g2, GEMM_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ua);
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int updown_dispatch(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                    int T, int C, void* Y, void* ws, size_t ws_bytes, int algo, cudaStream_t st) {
+    if (M == 0) return SFFN_OK;
+    const int a = resolve_algo(algo, N);
+    if (a == SFFN_ALGO_UNION) {
+        if (!union_applicable(N)) return SFFN_ERR_SHAPE;
+        if (!ws || ws_bytes < updown_ws_bytes(M, N, a)) return SFFN_ERR_SHAPE;
+        return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, ws, st);
+    }
+    if (a != SFFN_ALGO_GATHER) return SFFN_ERR_INVALID_ARG;
+    return updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -187,9 +292,17 @@ int64_t sffn_twell_words(int64_t M, int64_t N, int T, int C) {
     return M * (N / C);
 }
 
-size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C) {
+size_t sffn_up_down_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo) {
+    (void)T;
+    (void)C;
+    if (M < 0 || N <= 0) return 0;
+    return updown_ws_bytes(M, N, algo);
+}
+
+size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo) {
     int64_t w = sffn_twell_words(M, N, T, C);
-    return w < 0 ? 0 : static_cast<size_t>(w) * 4;
+    if (w < 0) return 0;
+    return static_cast<size_t>(align1k(w * 4)) + updown_ws_bytes(M, N, algo);
 }
 
 int sffn_pack(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
@@ -219,24 +332,33 @@ int sffn_unpack(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int64
 }
 
 int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
-                 int T, int C, void* Y, void* stream) {
+                 int T, int C, void* Y, void* workspace, size_t ws_bytes, int algo, void* stream) {
     int r = updown_checks(X, twell, Wu, Wd, M, K, N, T, C, Y);
     if (r != SFFN_OK) return r;
+    if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
+    if (resolve_algo(algo, N) == SFFN_ALGO_UNION && M > 0) {
+        if (!union_applicable(N)) return SFFN_ERR_SHAPE;
+        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, algo)) return SFFN_ERR_SHAPE;
+    }
     if ((r = check_device()) != SFFN_OK) return r;
-    return updown_impl(X, twell, Wu, Wd, M, K, N, T, C, Y, S(stream));
+    return updown_dispatch(X, twell, Wu, Wd, M, K, N, T, C, Y, workspace, ws_bytes, algo, S(stream));
 }
 
 int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N, int T,
-                 int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, void* stream) {
+                 int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream) {
     int r = pack_checks(X, Wg, M, K, N, T, C, workspace);
     if (r != SFFN_OK) return r;
     if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
-    if (ws_bytes < sffn_forward_workspace_bytes(M, N, T, C)) return SFFN_ERR_SHAPE;
+    if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
+    if (resolve_algo(algo, N) == SFFN_ALGO_UNION && !union_applicable(N)) return SFFN_ERR_SHAPE;
+    if (ws_bytes < sffn_forward_workspace_bytes(M, N, T, C, algo)) return SFFN_ERR_SHAPE;
     if ((r = check_device()) != SFFN_OK) return r;
     if (M == 0) return SFFN_OK;
     uint32_t* tw = static_cast<uint32_t*>(workspace);
+    const int64_t tw_bytes = align1k(sffn_twell_words(M, N, T, C) * 4);
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
-    return updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, S(stream));
+    return updown_dispatch(X, tw, Wu, Wd, M, K, N, T, C, Y, static_cast<uint8_t*>(workspace) + tw_bytes,
+                           ws_bytes - static_cast<size_t>(tw_bytes), algo, S(stream));
 }
 
 int sffn_dense_forward(const void* X, const void* Wg, const void* Wu, const void* WdT, int64_t M, int64_t K, int64_t N,

@@ -83,14 +83,15 @@ int sffn_allreduce_bf16(sffn_comm* c, void* buf, int64_t count, void* stream) {
 
 int sffn_sharded_forward(sffn_comm* c, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s, int64_t M,
                          int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace, size_t ws_bytes,
-                         uint32_t* d_overflow, int n_chunks, void* stream) {
+                         uint32_t* d_overflow, int algo, int n_chunks, void* stream) {
     if (!c) return SFFN_ERR_INVALID_ARG;
     if (n_chunks < 1) n_chunks = 1;
     if (M < 0) return SFFN_ERR_SHAPE;
-    if (ws_bytes < sffn_forward_workspace_bytes(M, N_local, T, C)) return SFFN_ERR_SHAPE;
+    if (ws_bytes < sffn_forward_workspace_bytes(M, N_local, T, C, algo)) return SFFN_ERR_SHAPE;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (n_chunks == 1 || M < 2 * 128) {
-        int r = sffn_forward(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, Y, workspace, ws_bytes, d_overflow, stream);
+        int r = sffn_forward(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, Y, workspace, ws_bytes, d_overflow, algo,
+                             stream);
         if (r != SFFN_OK) return r;
         return sffn_allreduce_bf16(c, Y, M * K, stream);
     }
@@ -100,7 +101,6 @@ int sffn_sharded_forward(sffn_comm* c, const void* X, const void* Wg_s, const vo
     rows = (rows + 127) / 128 * 128;
     const char* x = static_cast<const char*>(X);
     char* y = static_cast<char*>(Y);
-    uint32_t* tw = static_cast<uint32_t*>(workspace);
     // the comm stream must not start before earlier work on `stream` that touched Y
     if (cudaEventRecord(c->events[n_chunks], st) != cudaSuccess) return SFFN_ERR_CUDA;
     if (cudaStreamWaitEvent(c->comm_stream, c->events[n_chunks], 0) != cudaSuccess) return SFFN_ERR_CUDA;
@@ -108,9 +108,9 @@ int sffn_sharded_forward(sffn_comm* c, const void* X, const void* Wg_s, const vo
     for (int64_t r0 = 0; r0 < M; r0 += rows, ++i) {
         const int64_t mr = (M - r0) < rows ? (M - r0) : rows;
         const size_t xoff = static_cast<size_t>(r0 * K) * 2;
-        uint32_t* twc = tw + r0 * (N_local / C);
-        int r = sffn_forward(x + xoff, Wg_s, Wu_s, Wd_s, mr, K, N_local, T, C, y + xoff, twc,
-                             sffn_forward_workspace_bytes(mr, N_local, T, C), d_overflow, stream);
+        // the workspace is reused by every chunk: chunk i+1's compute follows chunk i's on `stream`
+        int r = sffn_forward(x + xoff, Wg_s, Wu_s, Wd_s, mr, K, N_local, T, C, y + xoff, workspace, ws_bytes,
+                             d_overflow, algo, stream);
         if (r != SFFN_OK) return r;
         if (cudaEventRecord(c->events[i], st) != cudaSuccess) return SFFN_ERR_CUDA;
         if (cudaStreamWaitEvent(c->comm_stream, c->events[i], 0) != cudaSuccess) return SFFN_ERR_CUDA;

@@ -15,6 +15,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsffn.so")
 
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_TILE_OVERFLOW, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(7)
+ALGO_AUTO, ALGO_GATHER, ALGO_UNION = 0, 1, 2
+_ALGOS = {"auto": ALGO_AUTO, "gather": ALGO_GATHER, "union": ALGO_UNION}
+
+
+def _algo(a) -> int:
+    return _ALGOS[a] if isinstance(a, str) else int(a)
 
 _lib = None
 
@@ -24,11 +30,12 @@ _SIGS = {
     "sffn_status_string": (ctypes.c_char_p, [_int]),
     "sffn_version": (ctypes.c_char_p, []),
     "sffn_twell_words": (_i64, [_i64, _i64, _int, _int]),
-    "sffn_forward_workspace_bytes": (_sz, [_i64, _i64, _int, _int]),
+    "sffn_up_down_workspace_bytes": (_sz, [_i64, _i64, _int, _int, _int]),
+    "sffn_forward_workspace_bytes": (_sz, [_i64, _i64, _int, _int, _int]),
     "sffn_pack": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp]),
     "sffn_unpack": (_int, [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp, _vp]),
-    "sffn_up_down": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp]),
-    "sffn_forward": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _vp]),
+    "sffn_up_down": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _int, _vp]),
+    "sffn_forward": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _int, _vp]),
     "sffn_dense_forward": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "sffn_transpose_bf16": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "sffn_gate_gemm_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
@@ -38,7 +45,7 @@ _SIGS = {
     "sffn_comm_destroy": (_int, [_vp]),
     "sffn_comm_size": (_int, [_vp]),
     "sffn_sharded_forward": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
-                                    _int, _vp]),
+                                    _int, _int, _vp]),
     "sffn_allreduce_bf16": (_int, [_vp, _vp, _i64, _vp]),
 }
 
@@ -101,8 +108,19 @@ def twell_words(M: int, N: int, T: int, C: int) -> int:
     return int(lib().sffn_twell_words(M, N, T, C))
 
 
-def workspace_bytes(M: int, N: int, T: int, C: int) -> int:
-    return int(lib().sffn_forward_workspace_bytes(M, N, T, C))
+def workspace_bytes(M: int, N: int, T: int, C: int, algo="auto") -> int:
+    """Bytes of workspace sffn_forward needs (TwELL + up/down workspace)."""
+    return int(lib().sffn_forward_workspace_bytes(M, N, T, C, _algo(algo)))
+
+
+def up_down_workspace_bytes(M: int, N: int, T: int, C: int, algo="auto") -> int:
+    return int(lib().sffn_up_down_workspace_bytes(M, N, T, C, _algo(algo)))
+
+
+def _ws(nbytes: int, device, ws=None):
+    if ws is not None:
+        return ws
+    return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
 
 
 def pack(x: torch.Tensor, wg: torch.Tensor, T: int = 256, C: int = 8, out: torch.Tensor | None = None,
@@ -127,28 +145,37 @@ def unpack(tw: torch.Tensor, N: int, T: int = 256, C: int = 8, out: torch.Tensor
     return out
 
 
-def up_down(x, tw, wu, wd, T: int = 256, C: int = 8, out=None, stream=None) -> torch.Tensor:
+def up_down(x, tw, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, algo="auto",
+            stream=None) -> torch.Tensor:
     M, K = x.shape
     N = wu.shape[0]
+    a = _algo(algo)
     if out is None:
         out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+    workspace = _ws(up_down_workspace_bytes(M, N, T, C, a), x.device, workspace)
     _chk(lib().sffn_up_down(_bf16(x, "x"), _p(tw), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
-                            _bf16(out, "out"), _stream(stream)), "sffn_up_down")
+                            _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(), a,
+                            _stream(stream)), "sffn_up_down")
     return out
 
 
-def forward(x, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, overflow=None,
+def twell_view(workspace: torch.Tensor, M: int, N: int, C: int) -> torch.Tensor:
+    """The packed TwELL (int32 [M, N/C]) that sffn_forward leaves at the start of its workspace."""
+    return workspace[: M * (N // C) * 4].view(torch.int32).view(M, N // C)
+
+
+def forward(x, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, overflow=None, algo="auto",
             stream=None) -> torch.Tensor:
-    """Sparse FFN forward (pack + fused up/down).  workspace: uint8/int32 device buffer >= workspace_bytes."""
+    """Sparse FFN forward (pack + fused up/down).  workspace: uint8 device buffer >= workspace_bytes."""
     M, K = x.shape
     N = wg.shape[0]
+    a = _algo(algo)
     if out is None:
         out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
-    if workspace is None:
-        workspace = torch.empty((M, N // C), dtype=torch.int32, device=x.device)
+    workspace = _ws(workspace_bytes(M, N, T, C, a), x.device, workspace)
     _chk(lib().sffn_forward(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
                             _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(),
-                            _p(overflow), _stream(stream)), "sffn_forward")
+                            _p(overflow), a, _stream(stream)), "sffn_forward")
     return out
 
 
@@ -213,16 +240,16 @@ class Comm:
         self.h, self.rank, self.world = h, rank, world
 
     def sharded_forward(self, x, wg_s, wu_s, wd_s, T=256, C=8, out=None, workspace=None, overflow=None,
-                        n_chunks=1, stream=None):
+                        algo="auto", n_chunks=1, stream=None):
         M, K = x.shape
         N_local = wg_s.shape[0]
+        a = _algo(algo)
         if out is None:
             out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
-        if workspace is None:
-            workspace = torch.empty((M, N_local // C), dtype=torch.int32, device=x.device)
+        workspace = _ws(workspace_bytes(M, N_local, T, C, a), x.device, workspace)
         _chk(lib().sffn_sharded_forward(self.h, _bf16(x, "x"), _bf16(wg_s, "wg"), _bf16(wu_s, "wu"),
                                         _bf16(wd_s, "wd"), M, K, N_local, T, C, _bf16(out, "out"), _p(workspace),
-                                        workspace.numel() * workspace.element_size(), _p(overflow), n_chunks,
+                                        workspace.numel() * workspace.element_size(), _p(overflow), a, n_chunks,
                                         _stream(stream)), "sffn_sharded_forward")
         return out
 

@@ -42,7 +42,11 @@ def test_host_only_calls(lib):
     assert sffn.status_string(0) == "SFFN_OK"
     assert sffn.status_string(3) == "SFFN_ERR_TILE_OVERFLOW"
     assert sffn.twell_words(32768, 14336, 256, 8) == 32768 * 1792
-    assert sffn.workspace_bytes(16, 512, 256, 8) == 16 * 64 * 4
+    assert sffn.workspace_bytes(16, 512, 256, 8, "gather") == 16 * 64 * 4 + (1024 - 16 * 64 * 4 % 1024) % 1024
+    assert sffn.up_down_workspace_bytes(16, 512, 256, 8, "gather") == 0
+    # union workspace: H_c (128 rows per block x N bf16) dominates
+    assert sffn.up_down_workspace_bytes(32768, 14336, 256, 8, "union") >= 256 * 128 * 14336 * 2
+    assert sffn.workspace_bytes(32768, 14336, 256, 8) == sffn.workspace_bytes(32768, 14336, 256, 8, "union")
     assert "sm_100a" in sffn.version()
 
 
@@ -57,11 +61,15 @@ def test_argument_errors_before_launch(lib):
     # N not a multiple of T -> SHAPE
     assert lib.sffn_pack(p, p, 16, 128, 500, 256, 8, p, None, None) == 2
     # NULL -> INVALID_ARG
-    assert lib.sffn_up_down(None, p, p, p, 16, 128, 512, 256, 8, p, None) == 1
+    assert lib.sffn_up_down(None, p, p, p, 16, 128, 512, 256, 8, p, None, 0, 1, None) == 1
+    # union algo without workspace -> SHAPE
+    assert lib.sffn_up_down(p, p, p, p, 16, 128, 512, 256, 8, p, None, 0, 2, None) == 2
+    # bad algo -> INVALID_ARG
+    assert lib.sffn_up_down(p, p, p, p, 16, 128, 512, 256, 8, p, None, 0, 7, None) == 1
     # misaligned -> INVALID_ARG
     assert lib.sffn_pack(vp(4098), p, 16, 128, 512, 256, 8, p, None, None) == 1
     # workspace too small -> SHAPE
-    assert lib.sffn_forward(p, p, p, p, 16, 128, 512, 256, 8, p, p, 10, None, None) == 2
+    assert lib.sffn_forward(p, p, p, p, 16, 128, 512, 256, 8, p, p, 10, None, 0, None) == 2
 
 
 def test_product_path_does_not_import_oracle():

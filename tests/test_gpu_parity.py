@@ -132,26 +132,62 @@ def test_unpack_roundtrip(sffn):
 
 
 # ----------------------------------------------------------------- fused up/down and forward
+ALGOS = ["gather", "union"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("K", [64, 512, 2048, 4096, 8192])
-def test_up_down_vs_oracle(sffn, K):
+def test_up_down_vs_oracle(sffn, K, algo):
     """sffn_up_down fed the ORACLE's TwELL (isolates the kernel): Y vs Eq.3 with the stored bf16 gate."""
     cfg = synth.CONFIGS["1B"].replace(M=200, K=K, N=1024, Kb=min(64, K // 4), sparsity=0.97)
     X, Wg, Wu, Wd = inputs(cfg)
     wo, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
     tw = torch.from_numpy(wo.view(np.int32)).cuda()
-    Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), cfg.T, cfg.C)
+    Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo)
     Yref = oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)
     assert rel_fro(bf16_np(Y), Yref) < Y_TOL
 
 
+@pytest.mark.parametrize("T,C", [(32, 2), (64, 4), (128, 2), (256, 4), (256, 16)])
+def test_up_down_union_tiles(sffn, T, C):
+    """Union path across TwELL tile sizes and a union spanning many 256-wide chunks (N = 4096)."""
+    cfg = synth.CONFIGS["1B"].replace(M=384, K=256, N=4096, Kb=16, sparsity=0.95, T=T, C=C)
+    X, Wg, Wu, Wd = inputs(cfg)
+    wo, counts, ov, A = oracle.pack_from_inputs(X, Wg, T, C)
+    tw = torch.from_numpy(wo.view(np.int32)).cuda()
+    Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), T, C, algo="union")
+    assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, T, C)) < Y_TOL
+
+
+def test_up_down_union_dense_rows(sffn):
+    """Every neuron active for some row (union = N) and a fully empty block: both edge cases of U_b."""
+    cfg = synth.CONFIGS["1B"].replace(M=256, K=128, N=512, Kb=8, sparsity=0.9)
+    X, Wg, Wu, Wd = inputs(cfg)
+    # row 0: 255 of the 256 neurons of each tile active (C=1: capacity 255); rows 1..255 empty, so the
+    # first block's union is 510 of 512 neurons and the second block's union is empty
+    tw1 = np.zeros((cfg.M, cfg.N), dtype=np.uint32)
+    for t in range(2):
+        tw1[0, t * 256] = 255
+        for e in range(255):
+            tw1[0, t * 256 + 1 + e] = (t * 256 + e) | (0x3F80 << 16)
+    # rows 128..255 (second block) stay empty
+    tw = torch.from_numpy(tw1.view(np.int32)).cuda()
+    for algo in ALGOS:
+        Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), 256, 1, algo=algo)
+        Yref = oracle.ffn_twell(X, tw1, Wu, Wd, cfg.N, 256, 1)
+        assert rel_fro(bf16_np(Y[:1]), Yref[:1]) < Y_TOL
+        assert not torch.any(Y[1:].float() != 0)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("name,M", [("tiny", None), ("1B", 512), ("7B", 160)])
-def test_forward_vs_oracle(sffn, name, M):
+def test_forward_vs_oracle(sffn, name, M, algo):
     cfg = synth.CONFIGS[name]
     if M is not None:
         cfg = cfg.replace(M=M)
     X, Wg, Wu, Wd = inputs(cfg)
     ov = torch.zeros(1, dtype=torch.int32, device="cuda")
-    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, overflow=ov)
+    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, overflow=ov, algo=algo)
     assert sffn.overflow_check(ov) == 0
     wo, counts, n_ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
     Y3 = oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)      # Eq.3 with stored h_v
@@ -165,8 +201,9 @@ def test_forward_empty_pattern_is_zero(sffn):
     X = torch.ones((300, 128), dtype=torch.bfloat16, device="cuda")
     Wg = -torch.ones((256, 128), dtype=torch.bfloat16, device="cuda")
     Wu = torch.ones((256, 128), dtype=torch.bfloat16, device="cuda")
-    Y = sffn.forward(X, Wg, Wu, Wu, 256, 8)
-    assert torch.equal(Y.view(torch.int16), torch.zeros_like(Y).view(torch.int16))
+    for algo in ALGOS:
+        Y = sffn.forward(X, Wg, Wu, Wu, 256, 8, algo=algo)
+        assert torch.equal(Y.view(torch.int16), torch.zeros_like(Y).view(torch.int16))
 
 
 def test_forward_single_active_neuron(sffn):
@@ -189,18 +226,21 @@ def test_forward_single_active_neuron(sffn):
         tw[m, t * 32] = 1
         tw[m, t * 32 + 1] = n | (0x3E80 << 16)  # bf16 0.25
     Xn = Xb.view(torch.int16).numpy().view(np.uint16)
-    Y = sffn.up_down(to_dev(Xn), torch.from_numpy(tw.view(np.int32)).cuda(), to_dev(Wu), to_dev(Wd), 256, 8)
     Yref = oracle.ffn_twell(Xn, tw, Wu, Wd, N, 256, 8)
-    assert rel_fro(bf16_np(Y), Yref) < 4e-3
+    for algo in ALGOS:
+        Y = sffn.up_down(to_dev(Xn), torch.from_numpy(tw.view(np.int32)).cuda(), to_dev(Wu), to_dev(Wd), 256, 8,
+                         algo=algo)
+        assert rel_fro(bf16_np(Y), Yref) < 4e-3
 
 
 def test_forward_ragged_and_tiny_M(sffn):
     for M in (1, 127, 129, 383):
         cfg = synth.CONFIGS["1B"].replace(M=M, K=256, N=512, Kb=16, sparsity=0.95)
         X, Wg, Wu, Wd = inputs(cfg)
-        Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8)
         wo, _, _, _ = oracle.pack_from_inputs(X, Wg, 256, 8)
-        assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8)) < Y_TOL
+        for algo in ALGOS:
+            Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo)
+            assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8)) < Y_TOL
 
 
 # ----------------------------------------------------------------- dense baseline
