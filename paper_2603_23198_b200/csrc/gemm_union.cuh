@@ -6,15 +6,19 @@
 //   Y_b = H_b · W_d[U_b, :]               (DOWN kernel)
 // Every term skipped relative to Eq.1 has h_g = 0, exactly as in Alg.2; the terms computed
 // with G = 0 add exact zeros.  Both kernels are persistent warp-specialized tcgen05 GEMMs like
-// gemm_tc.cuh; the weight rows of U_b are gathered by TMA tile::gather4 (4 rows of 128 B per
-// instruction, 128-byte swizzle applied by address, so 4-row groups land directly in UMMA layout):
-//   UP   B operand: W_u[U_b[256c + r], k0:k0+64]       K-major   (gather4 over rows)
-//   DOWN B operand: W_d[U_b[k0 + r], 256j:256j+256]     MN-major  (gather4 over rows, 4 x 64-col atoms)
+// gemm_tc.cuh; the dense A operand comes by TMA, the weight rows of U_b are gathered by four producer
+// warps with 16-byte cp.async.cg into the 128-byte-swizzled UMMA layout (TMA tile::gather4 measured
+// ~70 SM cycles per instruction on B200 — 8x too slow to feed the tensor cores, profiles/r01):
+//   UP   B operand: W_u[U_b[256c + r], k0:k0+64]       K-major
+//   DOWN B operand: W_d[U_b[k0 + r], 256j:256j+256]     MN-major (4 x 64-column atoms)
+// cp.async completion is signalled with cp.async.mbarrier.arrive.noinc on the stage's full barrier.
 #pragma once
 #include "gemm_tc.cuh"
 #include "union.cuh"
 
 namespace sffn {
+
+typedef unsigned short bf16_t;
 
 struct UnionArgs {
     int M, K, N, T, C;
@@ -22,6 +26,7 @@ struct UnionArgs {
     int NJ;             // DOWN: output column tiles of 256
     const uint32_t* tw;  // UP: packed TwELL [M, N/C]
     UnionMeta um;
+    const bf16_t* wsrc;  // UP: W_u, DOWN: W_d, both [N, K]
 };
 
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t col, int32_t r0,
@@ -31,6 +36,13 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uin
         " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
         : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // MN-major operand, 128-byte swizzle: 64-element MN atoms LBO apart, 8-row K groups SBO apart.
@@ -59,11 +71,13 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
 }
 
 constexpr int UG_STAGES = 4;
+constexpr int UG_THREADS = 384;   // warps 0-7 as gemm_tc + warps 8-11: gather producers
+constexpr int UG_GATHER = 128;
 constexpr int UG_EWB = 8192;  // epilogue staging per warp
 constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 256;
 
 template <bool UP>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(UG_THREADS, 1)
     union_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmOut, const UnionArgs args) {
     constexpr int S = UG_STAGES;
@@ -90,7 +104,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tma_prefetch(&tmB);
         tma_prefetch(&tmOut);
         for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 1);
+            mbar_init(&full[i], 1 + UG_GATHER);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -119,7 +133,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     };
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer (whole warp issues gathers)
+        // ------------------------------------------------------------ A operand by TMA (one thread)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int b, cj, len;
+                tile_info(tile, b, cj, len);
+                const int nk = UP ? nk_up : len / GEMM_BK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES);
+                    tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
+                                policy_evict_last());
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp >= 8) {
+        // ------------------------------------------------------------ B operand: gathered weight rows
+        // 8 consecutive lanes copy one 128-B row segment (16 B each), so every warp instruction moves whole
+        // 128-B lines: UP 4 rows x 128 B, DOWN one neuron row's 4 adjacent 64-column atoms (512 B).
+        const int gw = warp - 8;          // 0..3
+        const int c8 = lane & 7, sub = lane >> 3;
         int stage = 0;
         uint32_t phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -127,57 +166,53 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tile_info(tile, b, cj, len);
             const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
             if (UP) {
-                // lane l gathers chunk rows 8l .. 8l+7 (two groups of 4)
-                int idx[8];
+                // pass i covers chunk rows 16 i + 4 gw + sub
+                int nidx[16];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int r = 8 * lane + i;
-                    idx[i] = r < len ? __ldg(ul + 256 * cj + r) : 0;
+                for (int i = 0; i < 16; ++i) {
+                    const int r = 16 * i + 4 * gw + sub;
+                    nidx[i] = r < len ? __ldg(ul + 256 * cj + r) : -1;
                 }
                 for (int kb = 0; kb < nk_up; ++kb) {
-                    if (lane == 0) {
-                        mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES + len * 128);
-                        tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
-                                    policy_evict_last());
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = 16 * i + 4 * gw + sub;
+                        if (nidx[i] >= 0)
+                            cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
+                                       args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * GEMM_BK + 8 * c8, 16);
                     }
-                    __syncwarp();
-                    if (8 * lane < len) {
-                        uint8_t* dst = stB + stage * GEMM_B_BYTES + 8 * lane * 128;
-                        tma_gather4(dst, &tmB, &full[stage], kb * GEMM_BK, idx[0], idx[1], idx[2], idx[3]);
-                        tma_gather4(dst + 512, &tmB, &full[stage], kb * GEMM_BK, idx[4], idx[5], idx[6], idx[7]);
-                    }
+                    cp_async_arrive_noinc(&full[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
             } else {
-                // lane l: row group g = l % 16 (rows 4g..4g+3 of the k-block), MN atoms 2*(l/16) and +1
-                const int g = lane & 15, mn0 = (lane >> 4) * 2;
+                // pass i covers k-block row r = 4 i + gw, MN atom a = sub (columns 256 cj + 64 a + 8 c8)
                 const int nk = len / GEMM_BK;
-                int idx[4];
+                const int col = cj * 256 + sub * 64 + 8 * c8;
+                const bool in = col < args.K;
+                int nidx[16];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) idx[i] = __ldg(ul + 4 * g + i);
+                for (int i = 0; i < 16; ++i) nidx[i] = __ldg(ul + 4 * i + gw);
                 for (int kb = 0; kb < nk; ++kb) {
-                    int nxt[4];
+                    int nxt[16];
                     const int kn = kb + 1 < nk ? kb + 1 : kb;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + 4 * g + i);
-                    if (lane == 0) {
-                        mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES + GEMM_B_BYTES);
-                        tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
-                                    policy_evict_last());
+                    for (int i = 0; i < 16; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + 4 * i + gw);
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES) + sub * 8192;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = 4 * i + gw;
+                        cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
+                                   args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + (in ? col : 0), in ? 16 : 0);
                     }
-                    __syncwarp();
-                    uint8_t* dst = stB + stage * GEMM_B_BYTES + g * 512;
+                    cp_async_arrive_noinc(&full[stage]);
 #pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        tma_gather4(dst + (mn0 + q) * 8192, &tmB, &full[stage], cj * 256 + (mn0 + q) * 64, idx[0],
-                                    idx[1], idx[2], idx[3]);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) idx[i] = nxt[i];
+                    for (int i = 0; i < 16; ++i) nidx[i] = nxt[i];
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -202,6 +237,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core (async proxy) reads
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
                     const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);

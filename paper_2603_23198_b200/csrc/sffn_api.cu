@@ -236,6 +236,9 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     ua.NJ = (int)((K + 255) / 256);
     ua.tw = tw;
     ua.um = um;
+    UnionArgs ud = ua;
+    ua.wsrc = static_cast<const bf16_t*>(Wu);
+    ud.wsrc = static_cast<const bf16_t*>(Wd);
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [] {
@@ -246,11 +249,11 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     if (attr != cudaSuccess) return SFFN_ERR_CUDA;
     const int sms = dev_info().sms;
     // UP: the number of (block, chunk) tiles is only known on the device; persistent grid
-    union_gemm_kernel<true><<<sms, GEMM_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua);
+    union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua);
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     const int64_t dtiles = NB * ua.NJ;
     const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
-    union_gemm_kernel<false><<<g2, GEMM_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ua);
+    union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud);
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
