@@ -24,6 +24,7 @@ struct UnionArgs {
     int M, K, N, T, C;
     int NB;             // token blocks of 128
     int NJ;             // DOWN: output column tiles of 256
+    int group;          // DOWN: token blocks per raster group
     const uint32_t* tw;  // UP: packed TwELL [M, N/C]
     UnionMeta um;
     const bf16_t* wsrc;  // UP: W_u, DOWN: W_d, both [N, K]
@@ -74,7 +75,7 @@ constexpr int UG_STAGES = 4;
 constexpr int UG_THREADS = 384;   // warps 0-7 as gemm_tc + warps 8-11: gather producers
 constexpr int UG_GATHER = 128;
 constexpr int UG_EWB = 8192;  // epilogue staging per warp
-constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 256;
+constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 512;
 
 template <bool UP>
 __global__ void __launch_bounds__(UG_THREADS, 1)
@@ -90,13 +91,14 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* gbar = tempty + 2;  // [4] epilogue: G tile loaded
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 4);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int N = args.N;
     const int NB = args.NB;
-    const int num_tiles = UP ? __ldg(args.um.chunk_off + NB) : NB * args.NJ;
+    const int num_tiles = UP ? __ldg(args.um.chunk_off) : NB * args.NJ;
     const int nk_up = (args.K + GEMM_BK - 1) / GEMM_BK;
 
     if (threadIdx.x == 0) {
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
+        for (int i = 0; i < 4; ++i) mbar_init(&gbar[i], 1);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -122,12 +125,19 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     // tile -> (b, c | j, rows/len)
     auto tile_info = [&](int tile, int& b, int& cj, int& len) {
         if (UP) {
-            b = upper_bound_i32(args.um.chunk_off, NB + 1, tile) - 1;
-            cj = tile - __ldg(args.um.chunk_off + b);
+            const int v = __ldg(args.um.tiles + tile);
+            b = v >> 8;
+            cj = v & 255;
             len = min(256, __ldg(args.um.ulen + b) - 256 * cj);  // rows of this chunk (multiple of 64)
         } else {
-            b = tile / args.NJ;
-            cj = tile - b * args.NJ;
+            // grouped raster: args.group blocks sweep all output column tiles together (L2 working set)
+            const int G = args.group;
+            const int per = G * args.NJ;
+            const int grp = tile / per;
+            const int gb = min(G, NB - grp * G);
+            const int in = tile - grp * per;
+            b = grp * G + in % gb;
+            cj = in / gb;
             len = __ldg(args.um.ulen + b);  // reduction length (multiple of 64)
         }
     };
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         uint8_t* stg = epi + ew * UG_EWB;
         int acc = 0;
         uint32_t acc_phase = 0;
-        const int NW = N >> 5;
+        uint32_t gphase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             int b, cj, len;
             tile_info(tile, b, cj, len);
@@ -274,54 +284,22 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             tc_fence_after();
             const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
             if constexpr (UP) {
-                // union positions [p0, p0 + len) of block b; this thread's row m
-                const int m = row0 + lane;
+                // staging <- G tile (gate values in union coordinates, pre-scattered into H_c by union_build),
+                // then H = G * (X W_u^T) in place, then TMA store back to the same H_c tile.
                 const int p0 = 256 * cj;
-                const int nreal = min(len, __ldg(args.um.utot + b) - p0);
-                const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
-                const uint32_t* msk = args.um.umask + static_cast<int64_t>(b) * NW;
-                const int32_t* wof = args.um.uwoff + static_cast<int64_t>(b) * NW;
-                int t_lo = 1, t_hi = 0, n_lo = 0, n_hi = -1;
-                if (nreal > 0) {
-                    n_lo = __ldg(ul + p0);
-                    n_hi = __ldg(ul + p0 + nreal - 1);
-                    t_lo = n_lo / args.T;
-                    t_hi = n_hi / args.T;
-                }
-                const int WPT = args.T / args.C, cap = WPT - 1;
-                const uint32_t* trow = args.tw + static_cast<int64_t>(m) * (N / args.C);
-                const bool row_ok = m < args.M;
 #pragma unroll 1
                 for (int h = 0; h < 2 && 128 * h < len; ++h) {
-                    if (lane == 0) bulk_wait_read0();
-                    __syncwarp();
-                    // zero this row in both 64-column boxes
-#pragma unroll
-                    for (int q = 0; q < 2; ++q)
-#pragma unroll
-                        for (int c16 = 0; c16 < 8; ++c16)
-                            *reinterpret_cast<uint4*>(stg + q * 4096 + lane * 128 + c16 * 16) = make_uint4(0, 0, 0, 0);
-                    // scatter the stored gate values whose union position falls in this half
-                    if (row_ok) {
-                        for (int t = t_lo; t <= t_hi; ++t) {
-                            const uint32_t* blk = trow + static_cast<int64_t>(t) * WPT;
-                            const int cnt = min(static_cast<int>(__ldg(blk)), cap);
-                            for (int e = 0; e < cnt; ++e) {
-                                const uint32_t w = __ldg(blk + 1 + e);
-                                const int n = static_cast<int>(w & 0xFFFFu);
-                                if (n < n_lo || n > n_hi) continue;
-                                const int wi = n >> 5;
-                                const int j = __ldg(wof + wi) + __popc(__ldg(msk + wi) & ((1u << (n & 31)) - 1u)) - p0;
-                                if ((j >> 7) != h) continue;
-                                const int c = j & 127;
-                                *reinterpret_cast<uint16_t*>(stg + (c >> 6) * 4096 + sw128_off(lane, c & 63)) =
-                                    static_cast<uint16_t>(w >> 16);
-                            }
-                        }
+                    const int nbox = min(2, (len - 128 * h) / 64);
+                    if (lane == 0) {
+                        bulk_wait_read0();  // previous TMA store has finished reading the staging buffer
+                        mbar_arrive_expect_tx(&gbar[ew], nbox * 4096);
+                        for (int q = 0; q < nbox; ++q)
+                            tma_load_2d(stg + q * 4096, &tmOut, &gbar[ew], p0 + 128 * h + 64 * q, row0, policy_evict_first());
                     }
-                    // h = g * u  (only where g != 0: columns past `len` hold stale TMEM)
+                    mbar_wait(&gbar[ew], gphase);
+                    gphase ^= 1;
 #pragma unroll 1
-                    for (int q32 = 0; q32 < 4; ++q32) {
+                    for (int q32 = 0; q32 < 2 * nbox; ++q32) {
                         uint32_t v[32];
                         tmem_ld32(tb + 128 * h + 32 * q32, v);
                         tmem_wait_ld();
@@ -346,9 +324,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-#pragma unroll
-                        for (int q = 0; q < 2; ++q)
-                            if (128 * h + 64 * q < len) tma_store_2d(&tmOut, stg + q * 4096, p0 + 128 * h + 64 * q, row0);
+                        for (int q = 0; q < nbox; ++q) tma_store_2d(&tmOut, stg + q * 4096, p0 + 128 * h + 64 * q, row0);
                         bulk_commit();
                     }
                 }

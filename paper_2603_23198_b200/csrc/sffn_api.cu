@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -57,6 +58,14 @@ DevInfo dev_info() {
     cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
     return d;
+}
+
+// tuning override for raster group sizes (unset in production: the compiled defaults apply)
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    const int x = std::atoi(v);
+    return x > 0 ? x : dflt;
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -168,7 +177,7 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, total;
+    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, total;
 };
 UnionWs union_ws_layout(int64_t M, int64_t N) {
     const int64_t NB = (M + 127) / 128;
@@ -181,6 +190,7 @@ UnionWs union_ws_layout(int64_t M, int64_t N) {
     w.umask = o; o = align1k(o + NB * (N / 32) * 4);
     w.uwoff = o; o = align1k(o + NB * (N / 32) * 4);
     w.chunk = o; o = align1k(o + (NB + 1) * 4);
+    w.tiles = o; o = align1k(o + NB * ((N + 255) / 256) * 4);
     w.total = o;
     return w;
 }
@@ -209,12 +219,14 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     um.umask = reinterpret_cast<uint32_t*>(base + L.umask);
     um.uwoff = reinterpret_cast<int32_t*>(base + L.uwoff);
     um.chunk_off = reinterpret_cast<int32_t*>(base + L.chunk);
+    um.tiles = reinterpret_cast<int32_t*>(base + L.tiles);
     void* hc = base + L.hc;
 
     const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
-    union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um);
+    union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um,
+                                                                               static_cast<uint16_t*>(hc));
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    union_scan_kernel<<<1, 1024, 0, st>>>(um, (int)NB);
+    union_scan_kernel<<<1, 1024, 0, st>>>(um, (int)NB, env_int("SFFN_UP_GROUP", UNION_GROUP_UP));
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
 
     CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
@@ -234,6 +246,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     ua.C = C;
     ua.NB = (int)NB;
     ua.NJ = (int)((K + 255) / 256);
+    ua.group = env_int("SFFN_DOWN_GROUP", UNION_GROUP_DOWN);
     ua.tw = tw;
     ua.um = um;
     UnionArgs ud = ua;

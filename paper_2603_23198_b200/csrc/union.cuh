@@ -7,7 +7,8 @@
 //   umask [NB, N/32]   uint32 bit n%32 of word n/32 set iff n in U_b
 //   uwoff [NB, N/32]   int32  number of union members in words < w  (position of n in U_b =
 //                             uwoff[n/32] + popc(umask[n/32] & ((1 << n%32) - 1)))
-//   chunk_off [NB + 1] int32  exclusive prefix of ceil(ulen / 256): the up-GEMM work list
+//   tiles     [..]     int32  up-GEMM work list (b << 8 | chunk c), ordered group of 16 blocks -> c -> b
+//                             so concurrently running tiles share X rows and neighbouring W_u rows
 // Deterministic: bit sets are order-independent and the positions come from prefix sums.
 #pragma once
 #include "ptx.cuh"
@@ -19,15 +20,19 @@ struct UnionMeta {
     int32_t* ulen;
     uint32_t* umask;
     int32_t* uwoff;
-    int32_t* chunk_off;
-    int32_t* utot;  // [NB] un-padded union sizes
+    int32_t* chunk_off;  // [1]: number of UP tiles
+    int32_t* utot;       // [NB] un-padded union sizes
+    int32_t* tiles;      // [NB * ceil(N/256)]: UP work list, (b << 8) | chunk, grouped raster
 };
+
+constexpr int UNION_GROUP_UP = 8;    // token blocks whose up-GEMM tiles run together (L2 working set)
+constexpr int UNION_GROUP_DOWN = 16;  // token blocks whose down-GEMM tiles run together
 
 constexpr int UB_THREADS = 512;
 
 // One CTA per block of 128 rows.  Dynamic smem: N/32 uint32 masks + N/32 int32 offsets + scan scratch.
 __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
-                                                                  int C, UnionMeta um) {
+                                                                  int C, UnionMeta um, uint16_t* __restrict__ hc) {
     extern __shared__ uint32_t ub_smem[];
     const int NW = N >> 5;
     uint32_t* mask = ub_smem;                                  // [NW]
@@ -39,17 +44,36 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
     for (int w = threadIdx.x; w < NW; w += UB_THREADS) mask[w] = 0u;
     __syncthreads();
 
-    // OR the stored indices of the block's rows (warp per (row, tile), coalesced reads of the tile's words)
-    const int NT = N / T, WPT = T / C, cap = WPT - 1;
+    // OR the stored indices of the block's rows.  Warp per row, lanes over consecutive words (coalesced);
+    // when a tile's words fit a 32-word group (T/C <= 32) the count is taken from the owning lane by shuffle.
+    const int NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
     const int rows = min(128, M - b * 128);
-    const int pairs = rows * NT;
-    for (int pidx = warp; pidx < pairs; pidx += nwarps) {
-        const int r = pidx / NT, t = pidx - r * NT;
-        const uint32_t* blk = tw + static_cast<int64_t>(b * 128 + r) * (N / C) + static_cast<int64_t>(t) * WPT;
-        const int cnt = min(static_cast<int>(__ldg(blk)), cap);
-        for (int e = lane; e < cnt; e += 32) {
-            const uint32_t n = __ldg(blk + 1 + e) & 0xFFFFu;
-            atomicOr(&mask[n >> 5], 1u << (n & 31));
+    for (int r = warp; r < rows; r += nwarps) {
+        const uint32_t* row = tw + static_cast<int64_t>(b * 128 + r) * RW;
+        if (WPT <= 32) {
+            for (int w0 = 0; w0 < RW; w0 += 128) {
+                uint32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = (w0 + 32 * u + lane < RW) ? __ldg(row + w0 + 32 * u + lane) : 0u;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int slot = (w0 + 32 * u + lane) % WPT;
+                    const int cnt = min(static_cast<int>(__shfl_sync(0xffffffffu, v[u], lane - slot)), cap);
+                    if (slot >= 1 && slot <= cnt && w0 + 32 * u + lane < RW) {
+                        const uint32_t n = v[u] & 0xFFFFu;
+                        atomicOr(&mask[n >> 5], 1u << (n & 31));
+                    }
+                }
+            }
+        } else {
+            for (int t = 0; t < NT; ++t) {
+                const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
+                const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+                for (int e = lane; e < cnt; e += 32) {
+                    const uint32_t n = __ldg(blk + 1 + e) & 0xFFFFu;
+                    atomicOr(&mask[n >> 5], 1u << (n & 31));
+                }
+            }
         }
     }
     __syncthreads();
@@ -105,19 +129,71 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
         um.ulen[b] = padded;
         um.utot[b] = total;
     }
+
+    // G_b: the stored gate values in union coordinates, H_c[b*128 + r, j] (bf16), zero elsewhere.
+    // The up-GEMM epilogue multiplies this tile in place by X_b W_u[U_b]^T.
+    uint16_t* hb = hc + static_cast<int64_t>(b) * 128 * N;
+    const int v16 = padded / 8;  // 16-byte vectors per row
+    for (int i = threadIdx.x; i < 128 * v16; i += UB_THREADS) {
+        const int r = i / v16, c = i - r * v16;
+        *reinterpret_cast<uint4*>(hb + static_cast<int64_t>(r) * N + 8 * c) = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    // scatter: warp per row, coalesced word reads (same scheme as the OR pass above)
+    for (int r = warp; r < rows; r += nwarps) {
+        const uint32_t* row = tw + static_cast<int64_t>(b * 128 + r) * RW;
+        uint16_t* hrow = hb + static_cast<int64_t>(r) * N;
+        if (WPT <= 32) {
+            for (int w0 = 0; w0 < RW; w0 += 128) {
+                uint32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = (w0 + 32 * u + lane < RW) ? __ldg(row + w0 + 32 * u + lane) : 0u;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int slot = (w0 + 32 * u + lane) % WPT;
+                    const int cnt = min(static_cast<int>(__shfl_sync(0xffffffffu, v[u], lane - slot)), cap);
+                    if (slot >= 1 && slot <= cnt && w0 + 32 * u + lane < RW) {
+                        const int n = static_cast<int>(v[u] & 0xFFFFu);
+                        const int j = woff[n >> 5] + __popc(mask[n >> 5] & ((1u << (n & 31)) - 1u));
+                        hrow[j] = static_cast<uint16_t>(v[u] >> 16);
+                    }
+                }
+            }
+        } else {
+            for (int t = 0; t < NT; ++t) {
+                const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
+                const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+                for (int e = lane; e < cnt; e += 32) {
+                    const uint32_t w = __ldg(blk + 1 + e);
+                    const int n = static_cast<int>(w & 0xFFFFu);
+                    const int j = woff[n >> 5] + __popc(mask[n >> 5] & ((1u << (n & 31)) - 1u));
+                    hrow[j] = static_cast<uint16_t>(w >> 16);
+                }
+            }
+        }
+    }
 }
 
-// chunk_off[b] = sum_{b' < b} ceil(ulen[b'] / 256);  chunk_off[NB] = total.  One CTA.
-__global__ void __launch_bounds__(1024) union_scan_kernel(UnionMeta um, int NB) {
+// UP work list: for each group of UNION_GROUP blocks, chunk-major then block: tiles[] = (b << 8) | c.
+// One CTA; thread per group; chunk_off[0] = total tiles.
+__global__ void __launch_bounds__(1024) union_scan_kernel(UnionMeta um, int NB, int UNION_GROUP) {
     __shared__ int wsum[33];
     __shared__ int carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int NG = (NB + UNION_GROUP - 1) / UNION_GROUP;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int base = 0; base < NB; base += 1024) {
-        const int i = base + threadIdx.x;
-        const int v = i < NB ? (um.ulen[i] + 255) / 256 : 0;
-        int s = v;
+    for (int base = 0; base < NG; base += 1024) {
+        const int g = base + threadIdx.x;
+        int tot = 0, maxc = 0;
+        if (g < NG) {
+            for (int b = g * UNION_GROUP; b < min(NB, (g + 1) * UNION_GROUP); ++b) {
+                const int c = (um.ulen[b] + 255) / 256;
+                tot += c;
+                maxc = max(maxc, c);
+            }
+        }
+        int s = tot;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const int u = __shfl_up_sync(0xffffffffu, s, off);
@@ -137,12 +213,18 @@ __global__ void __launch_bounds__(1024) union_scan_kernel(UnionMeta um, int NB) 
             if (lane == 31) wsum[32] = y;
         }
         __syncthreads();
-        if (i < NB) um.chunk_off[i] = carry + wsum[warp] + s - v;
+        if (g < NG) {
+            int pos = carry + wsum[warp] + s - tot;
+            const int b0 = g * UNION_GROUP, b1 = min(NB, (g + 1) * UNION_GROUP);
+            for (int c = 0; c < maxc; ++c)
+                for (int b = b0; b < b1; ++b)
+                    if (c < (um.ulen[b] + 255) / 256) um.tiles[pos++] = (b << 8) | c;
+        }
         __syncthreads();
         if (threadIdx.x == 0) carry += wsum[32];
         __syncthreads();
     }
-    if (threadIdx.x == 0) um.chunk_off[NB] = carry;
+    if (threadIdx.x == 0) um.chunk_off[0] = carry;
 }
 
 }  // namespace sffn
