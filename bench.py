@@ -188,10 +188,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     M, K, N, T, C = cfg.M, cfg.K, cfg.N, cfg.T, cfg.C
-    if N % (world * T):
-        raise SystemExit(f"N={N} not divisible by world*T")
-    Nl = N // world
-    n0 = rank * Nl
+    from paper_2603_23198_b200.sharding import shard_range
+    n0, Nl = shard_range(N, world, rank, T)
 
     def to_dev(a):
         return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).to(dev)

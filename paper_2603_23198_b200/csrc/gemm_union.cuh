@@ -72,6 +72,9 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
 }
 
 constexpr int UG_STAGES = 4;
+#ifndef FENCE_CPASYNC
+#define FENCE_CPASYNC 1
+#endif
 constexpr int UG_THREADS = 384;   // warps 0-7 as gemm_tc + warps 8-11: gather producers
 constexpr int UG_GATHER = 128;
 constexpr int UG_EWB = 8192;  // epilogue staging per warp
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
-                    fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core (async proxy) reads
+                    if (FENCE_CPASYNC) fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
                     const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);

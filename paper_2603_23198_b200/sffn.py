@@ -223,17 +223,14 @@ class Comm:
     """The library's own NCCL communicator for hidden-dim sharding; torch.distributed only broadcasts the id."""
 
     def __init__(self, rank: int, world: int, device: int, group=None):
-        import torch.distributed as dist
-        idt = torch.zeros(128, dtype=torch.uint8)
+        from .sharding import broadcast_id
+        raw_id = None
         if rank == 0:
             buf = (ctypes.c_uint8 * 128)()
             _chk(lib().sffn_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)), "sffn_comm_unique_id")
-            idt = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
-        if world > 1:
-            obj = [idt.tolist()]
-            dist.broadcast_object_list(obj, src=0, group=group)
-            idt = torch.tensor(obj[0], dtype=torch.uint8)
-        raw = (ctypes.c_uint8 * 128)(*idt.tolist())
+            raw_id = bytes(buf)
+        raw_id = broadcast_id(raw_id, rank, world, group)
+        raw = (ctypes.c_uint8 * 128)(*raw_id)
         h = ctypes.c_void_p()
         _chk(lib().sffn_comm_init(ctypes.byref(h), world, rank, ctypes.cast(raw, ctypes.c_void_p), device),
              "sffn_comm_init")

@@ -1,0 +1,28 @@
+"""Host-side logic of hidden-dim sharding (north_star (5)): which hidden units a rank owns, and the
+broadcast of the NCCL unique id.  No compute here."""
+from __future__ import annotations
+
+
+def shard_range(N: int, world: int, rank: int, T: int) -> tuple[int, int]:
+    """Contiguous block of hidden units [n0, n0 + Nl) owned by `rank`; every shard a multiple of the
+    TwELL tile T so each rank packs whole tiles with local indices."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    if N % (world * T):
+        raise ValueError(f"N={N} must be a multiple of world*T={world * T}")
+    Nl = N // world
+    return rank * Nl, Nl
+
+
+def broadcast_id(id_bytes: bytes | None, rank: int, world: int, group=None) -> bytes:
+    """Rank 0's 128-byte id to every rank through torch.distributed (any backend)."""
+    if world == 1:
+        assert id_bytes is not None
+        return id_bytes
+    import torch.distributed as dist
+    obj = [list(id_bytes) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    out = bytes(obj[0])
+    if len(out) != 128:
+        raise ValueError("unique id must be 128 bytes")
+    return out

@@ -268,3 +268,28 @@ def test_errors_do_not_launch(sffn):
     with pytest.raises(sffn.SffnError) as e:
         sffn.pack(x, w, 256, 3)
     assert e.value.status == 1
+
+
+# ----------------------------------------------------------------- sharded forward (1-rank NCCL communicator)
+@pytest.mark.parametrize("algo", ALGOS)
+def test_sharded_forward_single_rank(sffn, algo):
+    """sffn_sharded_forward on a 1-rank communicator: chunked (compute/all-reduce overlap on the comm
+    stream) and unchunked results are bit-identical to sffn_forward; hidden shards summed on the host
+    reproduce the unsharded output within tolerance (linearity, north_star (5))."""
+    cfg = synth.CONFIGS["1B"].replace(M=700, K=512, N=2048, Kb=32, sparsity=0.97)
+    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    ref = sffn.forward(X, Wg, Wu, Wd, 256, 8, algo=algo)
+    comm = sffn.Comm(0, 1, torch.cuda.current_device())
+    try:
+        for chunks in (1, 3):
+            Y = comm.sharded_forward(X, Wg, Wu, Wd, 256, 8, algo=algo, n_chunks=chunks)
+            torch.cuda.synchronize()
+            assert torch.equal(Y.view(torch.int16), ref.view(torch.int16))
+    finally:
+        comm.close()
+    from paper_2603_23198_b200.sharding import shard_range
+    parts = torch.zeros(ref.shape, dtype=torch.float32, device="cuda")
+    for r in range(4):
+        n0, Nl = shard_range(cfg.N, 4, r, 256)
+        parts += sffn.forward(X, Wg[n0:n0 + Nl], Wu[n0:n0 + Nl], Wd[n0:n0 + Nl], 256, 8, algo=algo).float()
+    assert rel_fro(parts.cpu().numpy().astype(np.float64), bf16_np(ref)) < Y_TOL
