@@ -145,6 +145,24 @@ int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int6
  */
 int sffn_overflow_check(const uint32_t* d_overflow, void* stream, uint32_t* host_count);
 
+/* ---------------------------------------------------------------- fp32 mode (reading R19)
+ * fp32 inputs and weights, fp32 accumulation everywhere (north_star: Y within 1e-5 relative Frobenius
+ * "in an fp32 mode").  The TwELL is the logical (SoA) form of Alg.1's outputs:
+ *   h_v float [M, N/C], h_I uint16 [M, N/C] (shard-local column), h_nz uint32 [M, N/T] (true count);
+ *   tile t of row m owns slots [t*T/C, (t+1)*T/C) of h_v / h_I (capacity T/C: no count word).
+ * The gate GEMM is a SIMT fp32 GEMM (tensor-core tf32 would round the inputs to 10-bit mantissas);
+ * its epilogue compacts each row-tile with warp ballot / popc, ascending columns.  Not a perf path.
+ * Constraints: K % 4 == 0 (and K <= 8192 for the up/down), N % T == 0, N <= 65536; X/W/Y 16-B aligned. */
+size_t sffn_f32_twell_bytes(int64_t M, int64_t N, int T, int C);
+int sffn_pack_f32(const float* X, const float* Wg, int64_t M, int64_t K, int64_t N, int T, int C, float* h_v,
+                  uint16_t* h_I, uint32_t* h_nz, uint32_t* d_overflow, void* stream);
+int sffn_up_down_f32(const float* X, const float* h_v, const uint16_t* h_I, const uint32_t* h_nz, const float* Wu,
+                     const float* Wd, int64_t M, int64_t K, int64_t N, int T, int C, float* Y, void* stream);
+/* workspace >= sffn_f32_twell_bytes(M, N, T, C): h_v, then h_I, then h_nz (each 1 KiB aligned). */
+int sffn_forward_f32(const float* X, const float* Wg, const float* Wu, const float* Wd, int64_t M, int64_t K,
+                     int64_t N, int T, int C, float* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
+                     void* stream);
+
 /* ---------------------------------------------------------------- multi-GPU (hidden-dim shards)
  * One process per GPU.  Rank r owns hidden units [n_offset, n_offset + N_local) — contiguous row
  * blocks of all three [N, K] weights — packs its own TwELL (local indices), computes the partial

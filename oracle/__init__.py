@@ -46,6 +46,10 @@ def _load():
         lib.oracle_unpack.argtypes = [vp, i64, i64, ci, ci, vp]
         lib.oracle_ffn_dense.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp]
         lib.oracle_ffn_twell.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, ci, ci, vp, vp]
+        lib.oracle_pack_soa.argtypes = [vp, i64, i64, ci, ci, vp, vp, vp]
+        lib.oracle_pack_soa.restype = i64
+        lib.oracle_ffn_dense_f32.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp]
+        lib.oracle_ffn_soa_f32.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, ci, ci, vp]
         _lib = lib
     return _lib
 
@@ -141,3 +145,66 @@ def valid_prefix_equal(w_a: np.ndarray, w_b: np.ndarray, T: int, C: int) -> np.n
     valid = slot <= z[:, :, None]
     slots_eq = np.all((a[:, :, 1:] == b[:, :, 1:]) | ~valid, axis=2)
     return cnt_eq & slots_eq
+
+
+# ---------------------------------------------------------------- fp32 mode (reading R19)
+def _f32(a):
+    a = np.ascontiguousarray(a)
+    assert a.dtype == np.float32, a.dtype
+    return a
+
+
+def gate_preact_f32(X, Wg) -> np.ndarray:
+    X, Wg = _f32(X), _f32(Wg)
+    M, K = X.shape
+    N = Wg.shape[0]
+    A = np.empty((M, N), dtype=np.float64)
+    _load().oracle_gate_preact_f32(X.ctypes.data, Wg.ctypes.data, M, K, N, A.ctypes.data)
+    return A
+
+
+def pack_soa(S, T: int, C: int):
+    """Alg.1 SoA outputs (h_v, h_I, h_nz) with capacity T/C; slots past the count are zero here."""
+    S = np.ascontiguousarray(S, dtype=np.float32)
+    M, N = S.shape
+    hv = np.zeros((M, N // C), dtype=np.float32)
+    hi = np.zeros((M, N // C), dtype=np.uint16)
+    hnz = np.zeros((M, N // T), dtype=np.uint32)
+    ov = _load().oracle_pack_soa(S.ctypes.data, M, N, T, C, hv.ctypes.data, hi.ctypes.data, hnz.ctypes.data)
+    return hv, hi, hnz, int(ov)
+
+
+def ffn_dense_f32(X, Wg, Wu, Wd) -> np.ndarray:
+    X, Wg, Wu, Wd = map(_f32, (X, Wg, Wu, Wd))
+    M, K = X.shape
+    N = Wg.shape[0]
+    Y = np.empty((M, K), dtype=np.float64)
+    _load().oracle_ffn_dense_f32(X.ctypes.data, Wg.ctypes.data, Wu.ctypes.data, Wd.ctypes.data, M, K, N, Y.ctypes.data)
+    return Y
+
+
+def ffn_soa_f32(X, hv, hi, hnz, Wu, Wd, N: int, T: int, C: int) -> np.ndarray:
+    X, Wu, Wd = map(_f32, (X, Wu, Wd))
+    hv = np.ascontiguousarray(hv, dtype=np.float32)
+    hi = np.ascontiguousarray(hi, dtype=np.uint16)
+    hnz = np.ascontiguousarray(hnz, dtype=np.uint32)
+    M, K = X.shape
+    Y = np.empty((M, K), dtype=np.float64)
+    _load().oracle_ffn_soa_f32(X.ctypes.data, hv.ctypes.data, hi.ctypes.data, hnz.ctypes.data, Wu.ctypes.data,
+                               Wd.ctypes.data, M, K, N, T, C, Y.ctypes.data)
+    return Y
+
+
+def soa_prefix_equal(a, b, T: int, C: int) -> np.ndarray:
+    """(hv, hi, hnz) triples: counts equal and the stored prefix (capacity T/C) equal, per (row, tile)."""
+    hva, hia, nza = a
+    hvb, hib, nzb = b
+    M = nza.shape[0]
+    W = T // C
+    cnt_eq = nza == nzb
+    z = np.minimum(nza, W)
+    valid = np.arange(W)[None, None, :] < z[:, :, None]
+    va, vb = hva.reshape(M, -1, W), hvb.reshape(M, -1, W)
+    ia, ib = hia.reshape(M, -1, W), hib.reshape(M, -1, W)
+    eq = ((va.view(np.uint32) == vb.view(np.uint32)) & (ia == ib)) | ~valid
+    return cnt_eq & np.all(eq, axis=2)

@@ -185,3 +185,74 @@ void oracle_gate_preact_f32(const float* X, const float* Wg, int64_t M, int64_t 
             A[m * N + n] = acc;
         }
 }
+
+/*
+ * fp32 mode (reading R19): Alg.1 lines 7-17 producing the logical SoA outputs of Alg.1
+ * (P:88-89): h_v [M, N/C] float, h_I [M, N/C] uint16, h_nz [M, N/T]; capacity T/C (no count word);
+ * true count kept (R5).  Returns the number of overflowed (row, tile) blocks.
+ */
+int64_t oracle_pack_soa(const float* S, int64_t M, int64_t N, int T, int C, float* hv, uint16_t* hi, uint32_t* hnz) {
+    const int64_t NT = N / T, W = T / C, cap = W;
+    int64_t overflow = 0;
+#pragma omp parallel for schedule(static) reduction(+ : overflow)
+    for (int64_t r = 0; r < M; ++r) {
+        for (int64_t t = 0; t < NT; ++t) {
+            const int64_t n0 = t * T;
+            int64_t z = 0;
+            for (int64_t c = 0; c < T; ++c) {
+                float s = S[r * N + n0 + c];
+                if (s > 0.0f) {
+                    if (z < cap) {
+                        hv[r * (N / C) + t * W + z] = s;
+                        hi[r * (N / C) + t * W + z] = (uint16_t)(n0 + c);
+                    }
+                    z += 1;
+                }
+            }
+            hnz[r * NT + t] = (uint32_t)z;
+            if (z > cap) overflow += 1;
+        }
+    }
+    return overflow;
+}
+
+/* Eq.1 with fp32 inputs, fp64 arithmetic.  Y double [M, K]. */
+void oracle_ffn_dense_f32(const float* X, const float* Wg, const float* Wu, const float* Wd, int64_t M, int64_t K,
+                          int64_t N, double* Y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t j = 0; j < K; ++j) Y[m * K + j] = 0.0;
+        for (int64_t n = 0; n < N; ++n) {
+            double g = 0.0, u = 0.0;
+            for (int64_t k = 0; k < K; ++k) {
+                g += (double)X[m * K + k] * (double)Wg[n * K + k];
+                u += (double)X[m * K + k] * (double)Wu[n * K + k];
+            }
+            double h = (g > 0.0 ? g : 0.0) * u;
+            if (h != 0.0)
+                for (int64_t j = 0; j < K; ++j) Y[m * K + j] += h * (double)Wd[n * K + j];
+        }
+    }
+}
+
+/* Eq.3 over the SoA TwELL, fp32 inputs, fp64 arithmetic, gate = stored h_v. */
+void oracle_ffn_soa_f32(const float* X, const float* hv, const uint16_t* hi, const uint32_t* hnz, const float* Wu,
+                        const float* Wd, int64_t M, int64_t K, int64_t N, int T, int C, double* Y) {
+    const int64_t NT = N / T, W = T / C;
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t j = 0; j < K; ++j) Y[m * K + j] = 0.0;
+        for (int64_t t = 0; t < NT; ++t) {
+            int64_t z = hnz[m * NT + t];
+            if (z > W) z = W;
+            for (int64_t c = 0; c < z; ++c) {
+                const int64_t o = m * (N / C) + t * W + c;
+                const int64_t n = hi[o];
+                double u = 0.0;
+                for (int64_t k = 0; k < K; ++k) u += (double)X[m * K + k] * (double)Wu[n * K + k];
+                const double h = (double)hv[o] * u;
+                for (int64_t j = 0; j < K; ++j) Y[m * K + j] += h * (double)Wd[n * K + j];
+            }
+        }
+    }
+}

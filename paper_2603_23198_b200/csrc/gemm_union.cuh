@@ -39,8 +39,20 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
+#ifndef UG_WPOL
+#define UG_WPOL 0
+#endif
+// gathered weight rows: optional L2 evict_last hint (UG_WPOL=1)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+#if UG_WPOL
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -158,7 +170,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES);
                     tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
-                                policy_evict_last());
+                                UG_WPOL ? policy_evict_first() : policy_evict_last());
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;

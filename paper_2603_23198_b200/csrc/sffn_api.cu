@@ -10,6 +10,7 @@
 
 #include "../../include/sffn.h"
 #include "gemm_tc.cuh"
+#include "fp32_path.cuh"
 #include "gemm_union.cuh"
 #include "updown.cuh"
 
@@ -439,6 +440,86 @@ int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int6
     args.out_f32 = Sout;
     args.ld_out = N;
     return launch_gemm<EPI_F32, 1>(ta, tb, tb, tb, args, GEMM_BN, S(stream));
+}
+
+// ---------------------------------------------------------------- fp32 mode (R19)
+struct F32Ws {
+    int64_t hv, hi, hnz, total;
+};
+static F32Ws f32_layout(int64_t M, int64_t N, int T, int C) {
+    F32Ws w{};
+    w.hv = 0;
+    w.hi = align1k(M * (N / C) * 4);
+    w.hnz = w.hi + align1k(M * (N / C) * 2);
+    w.total = w.hnz + align1k(M * (N / T) * 4);
+    return w;
+}
+
+size_t sffn_f32_twell_bytes(int64_t M, int64_t N, int T, int C) {
+    if (M < 0 || N <= 0 || !valid_TC(T, C)) return 0;
+    return static_cast<size_t>(f32_layout(M, N, T, C).total);
+}
+
+int sffn_pack_f32(const float* X, const float* Wg, int64_t M, int64_t K, int64_t N, int T, int C, float* hv,
+                  uint16_t* hi, uint32_t* hnz, uint32_t* d_overflow, void* stream) {
+    if (M == 0 && valid_TC(T, C)) return SFFN_OK;
+    if (!X || !Wg || !hv || !hi || !hnz) return SFFN_ERR_INVALID_ARG;
+    if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || K < 4 || K % 4 != 0 || N <= 0 || N % T != 0 || N > 65536 || M > 2147483647) return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    const int smem = F32_BM * (F32_BN + 1) * 4;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [&] { attr = cudaFuncSetAttribute(pack_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+    if (attr != cudaSuccess) return SFFN_ERR_CUDA;
+    dim3 grid(static_cast<unsigned>((N + F32_BN - 1) / F32_BN), static_cast<unsigned>((M + F32_BM - 1) / F32_BM));
+    if (grid.y > 65535) return SFFN_ERR_SHAPE;
+    pack_f32_kernel<<<grid, 256, smem, S(stream)>>>(X, Wg, (int)M, (int)K, (int)N, T, C, hv, hi, hnz, d_overflow);
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_up_down_f32(const float* X, const float* hv, const uint16_t* hi, const uint32_t* hnz, const float* Wu,
+                     const float* Wd, int64_t M, int64_t K, int64_t N, int T, int C, float* Y, void* stream) {
+    if (M == 0 && valid_TC(T, C)) return SFFN_OK;
+    if (!X || !hv || !hi || !hnz || !Wu || !Wd || !Y) return SFFN_ERR_INVALID_ARG;
+    if (!aligned16(X) || !aligned16(Wu) || !aligned16(Wd) || !aligned16(Y)) return SFFN_ERR_INVALID_ARG;
+    if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || K < 4 || K % 4 != 0 || K > 8192 || N <= 0 || N % T != 0 || N > 65536 || M > 2147483647)
+        return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    const int64_t per_warp = (K / 4 + 3) / 4;
+    const int nch = static_cast<int>((per_warp + 31) / 32);
+    const float4* x = reinterpret_cast<const float4*>(X);
+    const float4* wu = reinterpret_cast<const float4*>(Wu);
+    const float4* wd = reinterpret_cast<const float4*>(Wd);
+    float4* y = reinterpret_cast<float4*>(Y);
+    dim3 g(static_cast<unsigned>(M));
+    cudaStream_t st = S(stream);
+    if (nch <= 1) updown_f32_kernel<1><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch <= 2) updown_f32_kernel<2><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch <= 4) updown_f32_kernel<4><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch <= 8) updown_f32_kernel<8><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    else updown_f32_kernel<16><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_forward_f32(const float* X, const float* Wg, const float* Wu, const float* Wd, int64_t M, int64_t K, int64_t N,
+                     int T, int C, float* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, void* stream) {
+    if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || N <= 0) return SFFN_ERR_SHAPE;
+    if (M == 0) return SFFN_OK;
+    if (!workspace || !aligned16(workspace)) return SFFN_ERR_INVALID_ARG;
+    if (ws_bytes < sffn_f32_twell_bytes(M, N, T, C)) return SFFN_ERR_SHAPE;
+    F32Ws L = f32_layout(M, N, T, C);
+    uint8_t* b = static_cast<uint8_t*>(workspace);
+    float* hv = reinterpret_cast<float*>(b + L.hv);
+    uint16_t* hi = reinterpret_cast<uint16_t*>(b + L.hi);
+    uint32_t* hnz = reinterpret_cast<uint32_t*>(b + L.hnz);
+    int r = sffn_pack_f32(X, Wg, M, K, N, T, C, hv, hi, hnz, d_overflow, stream);
+    if (r != SFFN_OK) return r;
+    return sffn_up_down_f32(X, hv, hi, hnz, Wu, Wd, M, K, N, T, C, Y, stream);
 }
 
 int sffn_overflow_check(const uint32_t* d_overflow, void* stream, uint32_t* host_count) {

@@ -12,7 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsffn.so")
+LIB_PATH = os.environ.get("SFFN_LIB") or os.path.join(_HERE, "libsffn.so")
 
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_TILE_OVERFLOW, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(7)
 ALGO_AUTO, ALGO_GATHER, ALGO_UNION = 0, 1, 2
@@ -47,6 +47,10 @@ _SIGS = {
     "sffn_sharded_forward": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
                                     _int, _int, _vp]),
     "sffn_allreduce_bf16": (_int, [_vp, _vp, _i64, _vp]),
+    "sffn_f32_twell_bytes": (_sz, [_i64, _i64, _int, _int]),
+    "sffn_pack_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "sffn_up_down_f32": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp]),
+    "sffn_forward_f32": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _vp]),
 }
 
 
@@ -217,6 +221,47 @@ def overflow_check(overflow: torch.Tensor, stream=None) -> int:
     if s not in (OK, ERR_TILE_OVERFLOW):
         _chk(s, "sffn_overflow_check")
     return int(h.value)
+
+
+def _f32(t: torch.Tensor, name: str):
+    if t.dtype != torch.float32:
+        raise TypeError(f"sffn: {name} must be float32, got {t.dtype}")
+    return _p(t)
+
+
+def pack_f32(x, wg, T: int = 256, C: int = 8, overflow=None, stream=None):
+    """fp32 mode: SoA TwELL (h_v float32 [M, N/C], h_I int16-stored uint16 [M, N/C], h_nz int32 [M, N/T])."""
+    M, K = x.shape
+    N = wg.shape[0]
+    hv = torch.empty((M, N // C), dtype=torch.float32, device=x.device)
+    hi = torch.empty((M, N // C), dtype=torch.int16, device=x.device)
+    hnz = torch.empty((M, N // T), dtype=torch.int32, device=x.device)
+    _chk(lib().sffn_pack_f32(_f32(x, "x"), _f32(wg, "wg"), M, K, N, T, C, _p(hv), _p(hi), _p(hnz), _p(overflow),
+                             _stream(stream)), "sffn_pack_f32")
+    return hv, hi, hnz
+
+
+def up_down_f32(x, hv, hi, hnz, wu, wd, T: int = 256, C: int = 8, out=None, stream=None):
+    M, K = x.shape
+    N = wu.shape[0]
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.float32, device=x.device)
+    _chk(lib().sffn_up_down_f32(_f32(x, "x"), _p(hv), _p(hi), _p(hnz), _f32(wu, "wu"), _f32(wd, "wd"), M, K, N, T, C,
+                                _f32(out, "out"), _stream(stream)), "sffn_up_down_f32")
+    return out
+
+
+def forward_f32(x, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, overflow=None, stream=None):
+    M, K = x.shape
+    N = wg.shape[0]
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.float32, device=x.device)
+    nb = int(lib().sffn_f32_twell_bytes(M, N, T, C))
+    workspace = _ws(nb, x.device, workspace)
+    _chk(lib().sffn_forward_f32(_f32(x, "x"), _f32(wg, "wg"), _f32(wu, "wu"), _f32(wd, "wd"), M, K, N, T, C,
+                                _f32(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(),
+                                _p(overflow), _stream(stream)), "sffn_forward_f32")
+    return out
 
 
 class Comm:

@@ -293,3 +293,50 @@ def test_sharded_forward_single_rank(sffn, algo):
         n0, Nl = shard_range(cfg.N, 4, r, 256)
         parts += sffn.forward(X, Wg[n0:n0 + Nl], Wu[n0:n0 + Nl], Wd[n0:n0 + Nl], 256, 8, algo=algo).float()
     assert rel_fro(parts.cpu().numpy().astype(np.float64), bf16_np(ref)) < Y_TOL
+
+
+# ----------------------------------------------------------------- fp32 mode (R19): Y within 1e-5
+F32_TOL = 1e-5
+
+
+@pytest.mark.parametrize("T,C", [(32, 2), (256, 8), (256, 4), (64, 1)])
+def test_fp32_pack_bitexact(sffn, T, C):
+    cfg = synth.CONFIGS["1B"].replace(M=300, K=512, N=1024, Kb=32, sparsity=0.97, T=T, C=C)
+    X = synth.gen_x(cfg, dtype="f32")
+    Wg = synth.gen_w(cfg, "g", dtype="f32")
+    ov = torch.zeros(1, dtype=torch.int32, device="cuda")
+    hv, hi, hnz = sffn.pack_f32(torch.from_numpy(X).cuda(), torch.from_numpy(Wg).cuda(), T, C, overflow=ov)
+    n_ov = sffn.overflow_check(ov)
+    A = oracle.gate_preact_f32(X, Wg)
+    ref = oracle.pack_soa(A.astype(np.float32), T, C)
+    got = (hv.cpu().numpy(), hi.cpu().numpy().view(np.uint16), hnz.cpu().numpy().view(np.uint32))
+    assert oracle.soa_prefix_equal(got, ref[:3], T, C).all()
+    assert n_ov == ref[3]
+
+
+@pytest.mark.parametrize("name,M", [("tiny", None), ("1B", 256), ("7B", 64)])
+def test_fp32_forward_grid(sffn, name, M):
+    cfg = synth.CONFIGS[name]
+    if M is not None:
+        cfg = cfg.replace(M=M)
+    X = synth.gen_x(cfg, dtype="f32")
+    Wg, Wu, Wd = (synth.gen_w(cfg, w, dtype="f32") for w in "gud")
+    t = lambda a: torch.from_numpy(a).cuda()
+    Y = sffn.forward_f32(t(X), t(Wg), t(Wu), t(Wd), cfg.T, cfg.C)
+    Y1 = oracle.ffn_dense_f32(X, Wg, Wu, Wd)
+    assert rel_fro(Y.cpu().numpy().astype(np.float64), Y1) < F32_TOL
+
+
+def test_fp32_forward_gaussian(sffn):
+    """Off-grid Gaussian fp32 inputs (gate signs near 0 may differ from the fp64 oracle; their
+    contribution is tiny): Y still within 1e-5 of Eq.1 with C=1 capacity (no overflow)."""
+    rng = np.random.default_rng(3)
+    M, K, N, T, C = 200, 512, 1024, 256, 1
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    Wg = (rng.standard_normal((N, K)) * 0.05 - 0.004).astype(np.float32)
+    Wu = (rng.standard_normal((N, K)) * 0.05).astype(np.float32)
+    Wd = (rng.standard_normal((N, K)) * 0.05).astype(np.float32)
+    t = lambda a: torch.from_numpy(a).cuda()
+    Y = sffn.forward_f32(t(X), t(Wg), t(Wu), t(Wd), T, C)
+    Y1 = oracle.ffn_dense_f32(X, Wg, Wu, Wd)
+    assert rel_fro(Y.cpu().numpy().astype(np.float64), Y1) < F32_TOL

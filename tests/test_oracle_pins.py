@@ -371,3 +371,49 @@ def test_single_active_neuron():
     u = (qx @ qu) * 2.0 ** -11
     exp = 0.5 * u[:, None] * synth.bf16_to_f32(Wd[n]).astype(np.float64)[None, :]
     assert np.array_equal(Y, exp)
+
+
+# ---------------------------------------------------------------- fp32 mode oracle (reading R19)
+def test_pack_soa_bruteforce():
+    """SoA form of Alg.1: capacity T/C, values kept in fp32, true count."""
+    rng = np.random.default_rng(7)
+    M, N, T, C = 5, 512, 64, 4
+    S = rng.standard_normal((M, N)).astype(np.float32)
+    S[rng.random((M, N)) < 0.8] = 0.0
+    S[0, :T] = 2.0  # overflow (64 > 16)
+    hv, hi, hnz, ov = oracle.pack_soa(S, T, C)
+    W = T // C
+    n_ov = 0
+    for m in range(M):
+        for t in range(N // T):
+            nz = np.flatnonzero(S[m, t * T:(t + 1) * T] > 0)
+            assert hnz[m, t] == len(nz)
+            k = min(len(nz), W)
+            assert hi[m, t * W:t * W + k].tolist() == (nz[:k] + t * T).tolist()
+            assert np.array_equal(hv[m, t * W:t * W + k], S[m, t * T + nz[:k]])
+            n_ov += len(nz) > W
+    assert ov == n_ov == 1
+
+
+def test_fp32_eq3_equals_eq1_and_perm():
+    """fp32-input Eq.3 over the SoA TwELL == Eq.1 when nothing overflows (gate stored exactly in fp32);
+    permutation-matrix closed form for the fp32 dense oracle."""
+    cfg = synth.CONFIGS["tiny"]
+    X = synth.gen_x(cfg, dtype="f32")
+    Wg, Wu, Wd = (synth.gen_w(cfg, w, dtype="f32") for w in "gud")
+    A = oracle.gate_preact_f32(X, Wg)
+    hv, hi, hnz, ov = oracle.pack_soa(A.astype(np.float32), cfg.T, cfg.C)
+    assert ov == 0
+    Y1 = oracle.ffn_dense_f32(X, Wg, Wu, Wd)
+    Y3 = oracle.ffn_soa_f32(X, hv, hi, hnz, Wu, Wd, cfg.N, cfg.T, cfg.C)
+    assert np.max(np.abs(Y1 - Y3)) <= 1e-12 * np.max(np.abs(Y1))
+    # the bf16 and fp32 oracles agree on grid inputs (same values, exactly representable in both)
+    Yb = oracle.ffn_dense(synth.gen_x(cfg), *(synth.gen_w(cfg, w) for w in "gud"))
+    assert np.array_equal(Y1, Yb)
+    Xf, p1, p2, p3, Wgb, Wub, Wdb = _perm_ffn_case(seed=9)
+    f = lambda b: synth.bf16_to_f32(b)
+    Y = oracle.ffn_dense_f32(Xf, f(Wgb), f(Wub), f(Wdb))
+    exp = np.zeros_like(Y)
+    for n in range(Xf.shape[1]):
+        exp[:, p3[n]] = np.maximum(Xf[:, p1[n]], 0) * Xf[:, p2[n]]
+    assert np.array_equal(Y, exp)
