@@ -199,9 +199,9 @@ def main():
     X = to_dev(X_host)
     Wg, Wu, Wd = (to_dev(synth.gen_w(cfg, w, n0, Nl)) for w in "gud")
     Y = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
-    ws = torch.empty(sffn.workspace_bytes(M, Nl, T, C, args.algo), dtype=torch.uint8, device=dev)
+    ws = torch.empty(sffn.workspace_bytes(M, K, Nl, T, C, args.algo), dtype=torch.uint8, device=dev)
     tw_view = sffn.twell_view(ws, M, Nl, C)
-    ud_ws = torch.empty(max(16, sffn.up_down_workspace_bytes(M, Nl, T, C, args.algo)), dtype=torch.uint8, device=dev)
+    ud_ws = torch.empty(max(16, sffn.up_down_workspace_bytes(M, K, Nl, T, C, args.algo)), dtype=torch.uint8, device=dev)
     ov = torch.zeros(1, dtype=torch.int32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()

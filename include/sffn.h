@@ -55,7 +55,9 @@ typedef enum {
 /* Algorithm of the fused sparse up/down (Alg.2 / Eq.3).  Both compute the same Eq.3 sum:
  *   SFFN_ALGO_GATHER: one CTA per token row, fp32 FMA over coalesced 16-byte gathers of the active
  *                     W_u / W_d rows (the paper's Listing 2 design); needs no workspace.
- *   SFFN_ALGO_UNION : per block of 128 rows, the union U_b of their active neurons; the up projection
+ *   SFFN_ALGO_UNION : rows reordered by pi (Alg.2 iterates m in pi(0..M-1): descending stored
+ *                     non-zeros within each 2048-row sequence window), then
+ *                     per block of 128 rows, the union U_b of their active neurons; the up projection
  *                     X_b W_u[U_b]^T and the down projection H_b W_d[U_b] run on tcgen05 tensor cores
  *                     with the gate applied in the epilogue (zero off-pattern, so skipped terms are
  *                     exactly the h_g = 0 terms of Alg.2); W_u / W_d rows gathered by TMA gather4.
@@ -71,10 +73,10 @@ const char* sffn_version(void);
 /* Number of uint32 words of a packed TwELL for [M, N] with tile T and compression C: M * N / C. */
 int64_t sffn_twell_words(int64_t M, int64_t N, int T, int C);
 /* Bytes of device workspace sffn_up_down needs for `algo` (0 for GATHER). */
-size_t sffn_up_down_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo);
+size_t sffn_up_down_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo);
 /* Bytes of device workspace sffn_forward needs: the TwELL of the gate (4 * sffn_twell_words, rounded
  * to 1 KiB) followed by the up/down workspace of `algo`. */
-size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo);
+size_t sffn_forward_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo);
 
 /*
  * sffn_pack — Alg.1: TwELL of relu(X W_g^T), computed by a tcgen05/TMEM tensor-core GEMM
@@ -183,7 +185,7 @@ int sffn_comm_size(const sffn_comm* comm);
  * of Y [M, K] bf16 on `stream`.  With n_chunks > 1 the M dimension is processed in chunks (multiples
  * of 128 rows) and the all-reduce of chunk i overlaps the compute of chunk i+1 (the library orders
  * them with events on an internal communication stream; still no host synchronization).  The
- * workspace (>= sffn_forward_workspace_bytes(M, N_local, T, C, algo)) is reused chunk after chunk.
+ * workspace (>= sffn_forward_workspace_bytes(M, K, N_local, T, C, algo)) is reused chunk after chunk.
  */
 int sffn_sharded_forward(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
                          int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,

@@ -28,6 +28,8 @@ struct UnionArgs {
     const uint32_t* tw;  // UP: packed TwELL [M, N/C]
     UnionMeta um;
     const bf16_t* wsrc;  // UP: W_u, DOWN: W_d, both [N, K]
+    const int32_t* perm;  // DOWN: output row of permuted row i
+    bf16_t* Y;            // DOWN: output [M, K]
 };
 
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t col, int32_t r0,
@@ -344,33 +346,34 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     }
                 }
             } else {
-                // DOWN: plain bf16 store of the 128 x 256 tile (two halves of 128 columns)
-                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
+                // DOWN: this thread's row goes to Y[perm[row]] (rows were processed in pi order); direct
+                // 16-byte stores of its 256-column slice (K tail clipped)
+                const int prow = row0 + lane;
+                const bool ok = prow < args.M;
+                bf16_t* yrow = args.Y + (ok ? static_cast<int64_t>(__ldg(args.perm + prow)) * args.K : 0);
 #pragma unroll 1
-                for (int half = 0; half < 2; ++half) {
-                    if (lane == 0) bulk_wait_read0();
-                    __syncwarp();
-#pragma unroll 1
-                    for (int ch = 0; ch < 4; ++ch) {
-                        uint32_t v[32];
-                        tmem_ld32(tb + half * 128 + ch * 32, v);
-                        tmem_wait_ld();
+                for (int ch = 0; ch < 8; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tb + ch * 32, v);
+                    tmem_wait_ld();
+                    const int col = cj * 256 + ch * 32;
+                    if (ok) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            srow[ch * 16 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-                    }
-                    if (half == 1) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[acc]);
-                    }
-                    fence_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_2d(&tmOut, stg, cj * 256 + half * 128, row0);
-                        bulk_commit();
+                        for (int q = 0; q < 4; ++q) {
+                            if (col + 8 * q < args.K) {
+                                uint4 o;
+                                o.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+                                o.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+                                o.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+                                o.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+                                *reinterpret_cast<uint4*>(yrow + col + 8 * q) = o;
+                            }
+                        }
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
             }
             if (++acc == 2) {
                 acc = 0;

@@ -178,9 +178,9 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, total;
+    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, total;
 };
-UnionWs union_ws_layout(int64_t M, int64_t N) {
+UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K) {
     const int64_t NB = (M + 127) / 128;
     UnionWs w{};
     int64_t o = 0;
@@ -192,6 +192,8 @@ UnionWs union_ws_layout(int64_t M, int64_t N) {
     w.uwoff = o; o = align1k(o + NB * (N / 32) * 4);
     w.chunk = o; o = align1k(o + (NB + 1) * 4);
     w.tiles = o; o = align1k(o + NB * ((N + 255) / 256) * 4);
+    w.perm = o;  o = align1k(o + M * 4);
+    w.xp = o;    o = align1k(o + M * K * 2);
     w.total = o;
     return w;
 }
@@ -203,15 +205,15 @@ int resolve_algo(int algo, int64_t N) {
     return algo;
 }
 
-size_t updown_ws_bytes(int64_t M, int64_t N, int algo) {
+size_t updown_ws_bytes(int64_t M, int64_t N, int64_t K, int algo) {
     if (resolve_algo(algo, N) != SFFN_ALGO_UNION || M <= 0) return 0;
-    return static_cast<size_t>(union_ws_layout(M, N).total);
+    return static_cast<size_t>(union_ws_layout(M, N, K).total);
 }
 
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st) {
     const int64_t NB = (M + 127) / 128;
-    UnionWs L = union_ws_layout(M, N);
+    UnionWs L = union_ws_layout(M, N, K);
     uint8_t* base = static_cast<uint8_t*>(ws);
     UnionMeta um;
     um.ulist = reinterpret_cast<int32_t*>(base + L.ulist);
@@ -222,16 +224,24 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     um.chunk_off = reinterpret_cast<int32_t*>(base + L.chunk);
     um.tiles = reinterpret_cast<int32_t*>(base + L.tiles);
     void* hc = base + L.hc;
+    int32_t* perm = reinterpret_cast<int32_t*>(base + L.perm);
+    void* xp = base + L.xp;
+    // row permutation pi (per 2048-row window, descending stored nnz) and the permuted copy of X
+    union_perm_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), 1024, 0, st>>>(tw, (int)M, (int)N, T, C, perm);
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp));
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
 
     const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
     union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um,
-                                                                               static_cast<uint16_t*>(hc));
+                                                                               static_cast<uint16_t*>(hc), perm);
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     union_scan_kernel<<<1, 1024, 0, st>>>(um, (int)NB, env_int("SFFN_UP_GROUP", UNION_GROUP_UP));
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
 
     CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
-    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&thc_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, GEMM_BK, GEMM_BM,
@@ -250,6 +260,8 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     ua.group = env_int("SFFN_DOWN_GROUP", UNION_GROUP_DOWN);
     ua.tw = tw;
     ua.um = um;
+    ua.perm = perm;
+    ua.Y = static_cast<bf16_t*>(Y);
     UnionArgs ud = ua;
     ua.wsrc = static_cast<const bf16_t*>(Wu);
     ud.wsrc = static_cast<const bf16_t*>(Wd);
@@ -277,7 +289,7 @@ int updown_dispatch(const void* X, const uint32_t* tw, const void* Wu, const voi
     const int a = resolve_algo(algo, N);
     if (a == SFFN_ALGO_UNION) {
         if (!union_applicable(N)) return SFFN_ERR_SHAPE;
-        if (!ws || ws_bytes < updown_ws_bytes(M, N, a)) return SFFN_ERR_SHAPE;
+        if (!ws || ws_bytes < updown_ws_bytes(M, N, K, a)) return SFFN_ERR_SHAPE;
         return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, ws, st);
     }
     if (a != SFFN_ALGO_GATHER) return SFFN_ERR_INVALID_ARG;
@@ -309,17 +321,17 @@ int64_t sffn_twell_words(int64_t M, int64_t N, int T, int C) {
     return M * (N / C);
 }
 
-size_t sffn_up_down_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo) {
+size_t sffn_up_down_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo) {
     (void)T;
     (void)C;
-    if (M < 0 || N <= 0) return 0;
-    return updown_ws_bytes(M, N, algo);
+    if (M < 0 || N <= 0 || K <= 0) return 0;
+    return updown_ws_bytes(M, N, K, algo);
 }
 
-size_t sffn_forward_workspace_bytes(int64_t M, int64_t N, int T, int C, int algo) {
+size_t sffn_forward_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo) {
     int64_t w = sffn_twell_words(M, N, T, C);
-    if (w < 0) return 0;
-    return static_cast<size_t>(align1k(w * 4)) + updown_ws_bytes(M, N, algo);
+    if (w < 0 || K <= 0) return 0;
+    return static_cast<size_t>(align1k(w * 4)) + updown_ws_bytes(M, N, K, algo);
 }
 
 int sffn_pack(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
@@ -355,7 +367,7 @@ int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const voi
     if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
     if (resolve_algo(algo, N) == SFFN_ALGO_UNION && M > 0) {
         if (!union_applicable(N)) return SFFN_ERR_SHAPE;
-        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, algo)) return SFFN_ERR_SHAPE;
+        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, K, algo)) return SFFN_ERR_SHAPE;
     }
     if ((r = check_device()) != SFFN_OK) return r;
     return updown_dispatch(X, twell, Wu, Wd, M, K, N, T, C, Y, workspace, ws_bytes, algo, S(stream));
@@ -368,7 +380,7 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
     if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
     if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
     if (resolve_algo(algo, N) == SFFN_ALGO_UNION && !union_applicable(N)) return SFFN_ERR_SHAPE;
-    if (ws_bytes < sffn_forward_workspace_bytes(M, N, T, C, algo)) return SFFN_ERR_SHAPE;
+    if (ws_bytes < sffn_forward_workspace_bytes(M, K, N, T, C, algo)) return SFFN_ERR_SHAPE;
     if ((r = check_device()) != SFFN_OK) return r;
     if (M == 0) return SFFN_OK;
     uint32_t* tw = static_cast<uint32_t*>(workspace);

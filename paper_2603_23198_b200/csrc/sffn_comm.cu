@@ -87,7 +87,7 @@ int sffn_sharded_forward(sffn_comm* c, const void* X, const void* Wg_s, const vo
     if (!c) return SFFN_ERR_INVALID_ARG;
     if (n_chunks < 1) n_chunks = 1;
     if (M < 0) return SFFN_ERR_SHAPE;
-    if (ws_bytes < sffn_forward_workspace_bytes(M, N_local, T, C, algo)) return SFFN_ERR_SHAPE;
+    if (ws_bytes < sffn_forward_workspace_bytes(M, K, N_local, T, C, algo)) return SFFN_ERR_SHAPE;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (n_chunks == 1 || M < 2 * 128) {
         int r = sffn_forward(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, Y, workspace, ws_bytes, d_overflow, algo,

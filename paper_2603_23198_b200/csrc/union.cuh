@@ -32,7 +32,8 @@ constexpr int UB_THREADS = 512;
 
 // One CTA per block of 128 rows.  Dynamic smem: N/32 uint32 masks + N/32 int32 offsets + scan scratch.
 __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
-                                                                  int C, UnionMeta um, uint16_t* __restrict__ hc) {
+                                                                  int C, UnionMeta um, uint16_t* __restrict__ hc,
+                                                                  const int32_t* __restrict__ perm) {
     extern __shared__ uint32_t ub_smem[];
     const int NW = N >> 5;
     uint32_t* mask = ub_smem;                                  // [NW]
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
     const int NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
     const int rows = min(128, M - b * 128);
     for (int r = warp; r < rows; r += nwarps) {
-        const uint32_t* row = tw + static_cast<int64_t>(b * 128 + r) * RW;
+        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
         if (WPT <= 32) {
             for (int w0 = 0; w0 < RW; w0 += 128) {
                 uint32_t v[4];
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
     __syncthreads();
     // scatter: warp per row, coalesced word reads (same scheme as the OR pass above)
     for (int r = warp; r < rows; r += nwarps) {
-        const uint32_t* row = tw + static_cast<int64_t>(b * 128 + r) * RW;
+        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
         uint16_t* hrow = hb + static_cast<int64_t>(r) * N;
         if (WPT <= 32) {
             for (int w0 = 0; w0 < RW; w0 += 128) {
@@ -172,6 +173,58 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
             }
         }
     }
+}
+
+// Row permutation pi (Alg.2 iterates m in pi(0..M-1); descending-nnz order): within each
+// window of PERM_W consecutive rows (one 2048-token sequence), rows sorted by stored non-zeros
+// descending, ties by row index -> unique keys, deterministic.  Blocks of 128 never straddle windows.
+constexpr int PERM_W = 2048;
+__global__ void __launch_bounds__(1024) union_perm_kernel(const uint32_t* __restrict__ tw, int M, int N, int T, int C,
+                                                          int32_t* __restrict__ perm) {
+    __shared__ unsigned long long keys[PERM_W];
+    const int w0 = blockIdx.x * PERM_W;
+    const int rows = min(PERM_W, M - w0);
+    const int NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
+    for (int i = threadIdx.x; i < PERM_W; i += 1024) {
+        unsigned long long key = ~0ull;  // padding sorts last
+        if (i < rows) {
+            const int m = w0 + i;
+            const uint32_t* row = tw + static_cast<int64_t>(m) * RW;
+            int nnz = 0;
+            for (int t = 0; t < NT; ++t) nnz += min(static_cast<int>(__ldg(row + static_cast<int64_t>(t) * WPT)), cap);
+            key = (static_cast<unsigned long long>(0x7FFFFFFF - nnz) << 32) | static_cast<unsigned>(m);
+        }
+        keys[i] = key;
+    }
+    __syncthreads();
+    for (int k = 2; k <= PERM_W; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < PERM_W; i += 1024) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned long long a = keys[i], c = keys[l];
+                    const bool up = (i & k) == 0;
+                    if ((a > c) == up) {
+                        keys[i] = c;
+                        keys[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < rows; i += 1024) perm[w0 + i] = static_cast<int32_t>(keys[i] & 0xFFFFFFFFu);
+}
+
+// Xp[i, :] = X[perm[i], :]  (warp per row, 16-byte vectors)
+__global__ void permute_rows_kernel(const uint4* __restrict__ X, const int32_t* __restrict__ perm, int M, int K8,
+                                    uint4* __restrict__ Xp) {
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= M) return;
+    const uint4* src = X + static_cast<int64_t>(__ldg(perm + gw)) * K8;
+    uint4* dst = Xp + gw * K8;
+    for (int c = lane; c < K8; c += 32) dst[c] = __ldg(src + c);
 }
 
 // UP work list: for each group of UNION_GROUP blocks, chunk-major then block: tiles[] = (b << 8) | c.

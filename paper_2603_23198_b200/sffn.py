@@ -30,8 +30,8 @@ _SIGS = {
     "sffn_status_string": (ctypes.c_char_p, [_int]),
     "sffn_version": (ctypes.c_char_p, []),
     "sffn_twell_words": (_i64, [_i64, _i64, _int, _int]),
-    "sffn_up_down_workspace_bytes": (_sz, [_i64, _i64, _int, _int, _int]),
-    "sffn_forward_workspace_bytes": (_sz, [_i64, _i64, _int, _int, _int]),
+    "sffn_up_down_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int, _int]),
+    "sffn_forward_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int, _int]),
     "sffn_pack": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp]),
     "sffn_unpack": (_int, [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp, _vp]),
     "sffn_up_down": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _int, _vp]),
@@ -112,13 +112,13 @@ def twell_words(M: int, N: int, T: int, C: int) -> int:
     return int(lib().sffn_twell_words(M, N, T, C))
 
 
-def workspace_bytes(M: int, N: int, T: int, C: int, algo="auto") -> int:
+def workspace_bytes(M: int, K: int, N: int, T: int, C: int, algo="auto") -> int:
     """Bytes of workspace sffn_forward needs (TwELL + up/down workspace)."""
-    return int(lib().sffn_forward_workspace_bytes(M, N, T, C, _algo(algo)))
+    return int(lib().sffn_forward_workspace_bytes(M, K, N, T, C, _algo(algo)))
 
 
-def up_down_workspace_bytes(M: int, N: int, T: int, C: int, algo="auto") -> int:
-    return int(lib().sffn_up_down_workspace_bytes(M, N, T, C, _algo(algo)))
+def up_down_workspace_bytes(M: int, K: int, N: int, T: int, C: int, algo="auto") -> int:
+    return int(lib().sffn_up_down_workspace_bytes(M, K, N, T, C, _algo(algo)))
 
 
 def _ws(nbytes: int, device, ws=None):
@@ -156,7 +156,7 @@ def up_down(x, tw, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, a
     a = _algo(algo)
     if out is None:
         out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
-    workspace = _ws(up_down_workspace_bytes(M, N, T, C, a), x.device, workspace)
+    workspace = _ws(up_down_workspace_bytes(M, K, N, T, C, a), x.device, workspace)
     _chk(lib().sffn_up_down(_bf16(x, "x"), _p(tw), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
                             _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(), a,
                             _stream(stream)), "sffn_up_down")
@@ -176,7 +176,7 @@ def forward(x, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, o
     a = _algo(algo)
     if out is None:
         out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
-    workspace = _ws(workspace_bytes(M, N, T, C, a), x.device, workspace)
+    workspace = _ws(workspace_bytes(M, K, N, T, C, a), x.device, workspace)
     _chk(lib().sffn_forward(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
                             _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(),
                             _p(overflow), a, _stream(stream)), "sffn_forward")
@@ -288,7 +288,7 @@ class Comm:
         a = _algo(algo)
         if out is None:
             out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
-        workspace = _ws(workspace_bytes(M, N_local, T, C, a), x.device, workspace)
+        workspace = _ws(workspace_bytes(M, K, N_local, T, C, a), x.device, workspace)
         _chk(lib().sffn_sharded_forward(self.h, _bf16(x, "x"), _bf16(wg_s, "wg"), _bf16(wu_s, "wu"),
                                         _bf16(wd_s, "wd"), M, K, N_local, T, C, _bf16(out, "out"), _p(workspace),
                                         workspace.numel() * workspace.element_size(), _p(overflow), a, n_chunks,

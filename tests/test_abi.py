@@ -42,11 +42,11 @@ def test_host_only_calls(lib):
     assert sffn.status_string(0) == "SFFN_OK"
     assert sffn.status_string(3) == "SFFN_ERR_TILE_OVERFLOW"
     assert sffn.twell_words(32768, 14336, 256, 8) == 32768 * 1792
-    assert sffn.workspace_bytes(16, 512, 256, 8, "gather") == 16 * 64 * 4 + (1024 - 16 * 64 * 4 % 1024) % 1024
-    assert sffn.up_down_workspace_bytes(16, 512, 256, 8, "gather") == 0
-    # union workspace: H_c (128 rows per block x N bf16) dominates
-    assert sffn.up_down_workspace_bytes(32768, 14336, 256, 8, "union") >= 256 * 128 * 14336 * 2
-    assert sffn.workspace_bytes(32768, 14336, 256, 8) == sffn.workspace_bytes(32768, 14336, 256, 8, "union")
+    assert sffn.workspace_bytes(16, 128, 512, 256, 8, "gather") == 16 * 64 * 4 + (1024 - 16 * 64 * 4 % 1024) % 1024
+    assert sffn.up_down_workspace_bytes(16, 128, 512, 256, 8, "gather") == 0
+    # union workspace: H_c (128 rows per block x N bf16) + the permuted copy of X dominate
+    assert sffn.up_down_workspace_bytes(32768, 4096, 14336, 256, 8, "union") >= 256 * 128 * 14336 * 2 + 32768 * 4096 * 2
+    assert sffn.workspace_bytes(32768, 4096, 14336, 256, 8) == sffn.workspace_bytes(32768, 4096, 14336, 256, 8, "union")
     assert "sm_100a" in sffn.version()
 
 

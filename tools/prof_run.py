@@ -18,7 +18,7 @@ dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
 X = dev(synth.gen_x(cfg)); Wg, Wu, Wd = (dev(synth.gen_w(cfg, w)) for w in "gud")
 ws = torch.empty((cfg.M, cfg.N // cfg.C), dtype=torch.int32, device="cuda")
 Y = torch.empty((cfg.M, cfg.K), dtype=torch.bfloat16, device="cuda")
-udws = torch.empty(max(16, sffn.up_down_workspace_bytes(cfg.M, cfg.N, cfg.T, cfg.C, a.algo)), dtype=torch.uint8, device="cuda")
+udws = torch.empty(max(16, sffn.up_down_workspace_bytes(cfg.M, cfg.K, cfg.N, cfg.T, cfg.C, a.algo)), dtype=torch.uint8, device="cuda")
 for _ in range(a.iters):
     sffn.pack(X, Wg, cfg.T, cfg.C, out=ws)
     sffn.up_down(X, ws, Wu, Wd, cfg.T, cfg.C, out=Y, workspace=udws, algo=a.algo)

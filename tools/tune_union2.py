@@ -9,7 +9,7 @@ cfg = synth.CONFIGS["7B"]
 dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
 X = dev(synth.gen_x(cfg)); Wg, Wu, Wd = (dev(synth.gen_w(cfg, w)) for w in "gud")
 tw = sffn.pack(X, Wg, cfg.T, cfg.C)
-ws = torch.empty(sffn.up_down_workspace_bytes(cfg.M, cfg.N, cfg.T, cfg.C, "union"), dtype=torch.uint8, device="cuda")
+ws = torch.empty(sffn.up_down_workspace_bytes(cfg.M, cfg.K, cfg.N, cfg.T, cfg.C, "union"), dtype=torch.uint8, device="cuda")
 Y = torch.empty((cfg.M, cfg.K), dtype=torch.bfloat16, device="cuda")
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device="cuda")
 def t(fn, n=10):
