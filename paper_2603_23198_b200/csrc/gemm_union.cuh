@@ -60,6 +60,13 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// 1-D bulk copy shared -> global (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+
 // MN-major operand, 128-byte swizzle: 64-element MN atoms LBO apart, 8-row K groups SBO apart.
 __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = 0;
@@ -346,34 +353,42 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     }
                 }
             } else {
-                // DOWN: this thread's row goes to Y[perm[row]] (rows were processed in pi order); direct
-                // 16-byte stores of its 256-column slice (K tail clipped)
-                const int prow = row0 + lane;
-                const bool ok = prow < args.M;
-                bf16_t* yrow = args.Y + (ok ? static_cast<int64_t>(__ldg(args.perm + prow)) * args.K : 0);
+                // DOWN: rows were processed in pi order; row i of the tile goes to Y[perm[row0 + i]].
+                // Stage 32 rows x 128 columns (bf16) per half in SMEM, then one 256-byte bulk copy per row.
+                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
+                const int ncols = min(128, args.K - cj * 256);  // per half, K tail
 #pragma unroll 1
-                for (int ch = 0; ch < 8; ++ch) {
-                    uint32_t v[32];
-                    tmem_ld32(tb + ch * 32, v);
-                    tmem_wait_ld();
-                    const int col = cj * 256 + ch * 32;
-                    if (ok) {
+                for (int half = 0; half < 2; ++half) {
+                    const int c0 = cj * 256 + half * 128;
+                    const int nc = min(128, args.K - c0);
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+#pragma unroll 1
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[32];
+                        tmem_ld32(tb + half * 128 + ch * 32, v);
+                        tmem_wait_ld();
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            if (col + 8 * q < args.K) {
-                                uint4 o;
-                                o.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
-                                o.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
-                                o.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
-                                o.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
-                                *reinterpret_cast<uint4*>(yrow + col + 8 * q) = o;
-                            }
+                        for (int j = 0; j < 16; ++j)
+                            srow[ch * 16 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                    }
+                    if (half == 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    }
+                    fence_async_smem();
+                    __syncwarp();
+                    if (nc > 0) {
+                        const int prow = row0 + lane;
+                        if (prow < args.M) {
+                            bf16_t* dst = args.Y + static_cast<int64_t>(__ldg(args.perm + prow)) * args.K + c0;
+                            bulk_s2g(dst, stg + lane * 256, static_cast<uint32_t>(nc) * 2);
                         }
+                        bulk_commit();
                     }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                (void)ncols;
             }
             if (++acc == 2) {
                 acc = 0;
