@@ -29,6 +29,7 @@ struct UnionArgs {
     UnionMeta um;
     const bf16_t* wsrc;  // UP: W_u, DOWN: W_d, both [N, K]
     const int32_t* perm;  // DOWN: output row of permuted row i
+    int* counter;         // dynamic tile scheduler (zeroed by union_scan_kernel)
     bf16_t* Y;            // DOWN: output [M, K]
 };
 
@@ -99,7 +100,9 @@ constexpr int UG_STAGES = 4;
 constexpr int UG_THREADS = 384;   // warps 0-7 as gemm_tc + warps 8-11: gather producers
 constexpr int UG_GATHER = 128;
 constexpr int UG_EWB = 8192;  // epilogue staging per warp
-constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 512;
+constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 1024;
+constexpr int UG_RING = 8;       // tile-scheduler ring depth
+constexpr int UG_READERS = 9;    // 4 gather warps + MMA thread + 4 epilogue warps
 
 template <bool UP>
 __global__ void __launch_bounds__(UG_THREADS, 1)
@@ -116,7 +119,10 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint64_t* gbar = tempty + 2;  // [4] epilogue: G tile loaded
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 4);
+    uint64_t* sfull = gbar + 4;   // [UG_RING] tile ring
+    uint64_t* sempty = sfull + UG_RING;
+    int* sched = reinterpret_cast<int*>(sempty + UG_RING);  // [UG_RING]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched + UG_RING);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -138,6 +144,10 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             mbar_init(&tempty[i], 4);
         }
         for (int i = 0; i < 4; ++i) mbar_init(&gbar[i], 1);
+        for (int i = 0; i < UG_RING; ++i) {
+            mbar_init(&sfull[i], 1);
+            mbar_init(&sempty[i], UG_READERS);
+        }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -145,6 +155,19 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+
+    // dynamic scheduler ring: warp 0 lane 0 claims tiles (atomicAdd) in the raster order and publishes them;
+    // every role reads the same sequence.  next_tile() returns -1 when the work is exhausted.
+    auto next_tile = [&](int& ridx, uint32_t& rphase, bool arrive_lane) -> int {
+        mbar_wait(&sfull[ridx], rphase);
+        const int t = *reinterpret_cast<volatile int*>(&sched[ridx]);
+        if (arrive_lane) mbar_arrive(&sempty[ridx]);
+        if (++ridx == UG_RING) {
+            ridx = 0;
+            rphase ^= 1;
+        }
+        return t;
+    };
 
     // tile -> (b, c | j, rows/len)
     auto tile_info = [&](int tile, int& b, int& cj, int& len) {
@@ -171,7 +194,19 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int widx = 0;
+            uint32_t wphase = 0;
+            for (;;) {
+                mbar_wait(&sempty[widx], wphase ^ 1);
+                int tile = atomicAdd(args.counter, 1);
+                if (tile >= num_tiles) tile = -1;
+                sched[widx] = tile;
+                mbar_arrive(&sfull[widx]);
+                if (++widx == UG_RING) {
+                    widx = 0;
+                    wphase ^= 1;
+                }
+                if (tile < 0) break;
                 int b, cj, len;
                 tile_info(tile, b, cj, len);
                 const int nk = UP ? nk_up : len / GEMM_BK;
@@ -195,7 +230,11 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         const int c8 = lane & 7, sub = lane >> 3;
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int ridx = 0;
+        uint32_t rphase = 0;
+        for (;;) {
+            const int tile = next_tile(ridx, rphase, lane == 0);
+            if (tile < 0) break;
             int b, cj, len;
             tile_info(tile, b, cj, len);
             const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
@@ -261,7 +300,11 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int ridx = 0;
+            uint32_t rphase = 0;
+            for (;;) {
+                const int tile = next_tile(ridx, rphase, true);
+                if (tile < 0) break;
                 int b, cj, len;
                 tile_info(tile, b, cj, len);
                 const int nk = UP ? nk_up : len / GEMM_BK;
@@ -300,7 +343,11 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t gphase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int ridx = 0;
+        uint32_t rphase = 0;
+        for (;;) {
+            const int tile = next_tile(ridx, rphase, lane == 0);
+            if (tile < 0) break;
             int b, cj, len;
             tile_info(tile, b, cj, len);
             const int row0 = b * GEMM_BM + ew * 32;

@@ -178,7 +178,7 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, total;
+    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, total;
 };
 UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K) {
     const int64_t NB = (M + 127) / 128;
@@ -194,6 +194,7 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K) {
     w.tiles = o; o = align1k(o + NB * ((N + 255) / 256) * 4);
     w.perm = o;  o = align1k(o + M * 4);
     w.xp = o;    o = align1k(o + M * K * 2);
+    w.ctr = o;   o = align1k(o + 64);
     w.total = o;
     return w;
 }
@@ -223,6 +224,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     um.uwoff = reinterpret_cast<int32_t*>(base + L.uwoff);
     um.chunk_off = reinterpret_cast<int32_t*>(base + L.chunk);
     um.tiles = reinterpret_cast<int32_t*>(base + L.tiles);
+    um.counters = reinterpret_cast<int*>(base + L.ctr);
     void* hc = base + L.hc;
     int32_t* perm = reinterpret_cast<int32_t*>(base + L.perm);
     void* xp = base + L.xp;
@@ -262,7 +264,9 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     ua.um = um;
     ua.perm = perm;
     ua.Y = static_cast<bf16_t*>(Y);
+    ua.counter = um.counters;
     UnionArgs ud = ua;
+    ud.counter = um.counters + 1;
     ua.wsrc = static_cast<const bf16_t*>(Wu);
     ud.wsrc = static_cast<const bf16_t*>(Wd);
     static std::once_flag once;

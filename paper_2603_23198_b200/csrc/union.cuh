@@ -23,6 +23,7 @@ struct UnionMeta {
     int32_t* chunk_off;  // [1]: number of UP tiles
     int32_t* utot;       // [NB] un-padded union sizes
     int32_t* tiles;      // [NB * ceil(N/256)]: UP work list, (b << 8) | chunk, grouped raster
+    int* counters;       // [2] dynamic tile-scheduler counters of the UP and DOWN GEMMs
 };
 
 constexpr int UNION_GROUP_UP = 8;    // token blocks whose up-GEMM tiles run together (L2 working set)
@@ -277,7 +278,11 @@ __global__ void __launch_bounds__(1024) union_scan_kernel(UnionMeta um, int NB, 
         if (threadIdx.x == 0) carry += wsum[32];
         __syncthreads();
     }
-    if (threadIdx.x == 0) um.chunk_off[0] = carry;
+    if (threadIdx.x == 0) {
+        um.chunk_off[0] = carry;
+        um.counters[0] = 0;
+        um.counters[1] = 0;
+    }
 }
 
 }  // namespace sffn
