@@ -236,8 +236,10 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
 
     const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
-    union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um,
-                                                                               static_cast<uint16_t*>(hc), perm);
+    union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um, perm);
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (128 / GS_ROWS)), 256, 0, st>>>(
+        tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm);
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     union_scan_kernel<<<1, 1024, 0, st>>>(um, (int)NB, env_int("SFFN_UP_GROUP", UNION_GROUP_UP));
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;

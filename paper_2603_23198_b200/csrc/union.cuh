@@ -33,8 +33,7 @@ constexpr int UB_THREADS = 512;
 
 // One CTA per block of 128 rows.  Dynamic smem: N/32 uint32 masks + N/32 int32 offsets + scan scratch.
 __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
-                                                                  int C, UnionMeta um, uint16_t* __restrict__ hc,
-                                                                  const int32_t* __restrict__ perm) {
+                                                                  int C, UnionMeta um, const int32_t* __restrict__ perm) {
     extern __shared__ uint32_t ub_smem[];
     const int NW = N >> 5;
     uint32_t* mask = ub_smem;                                  // [NW]
@@ -132,45 +131,52 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
         um.utot[b] = total;
     }
 
-    // G_b: the stored gate values in union coordinates, H_c[b*128 + r, j] (bf16), zero elsewhere.
-    // The up-GEMM epilogue multiplies this tile in place by X_b W_u[U_b]^T.
-    uint16_t* hb = hc + static_cast<int64_t>(b) * 128 * N;
-    const int v16 = padded / 8;  // 16-byte vectors per row
-    for (int i = threadIdx.x; i < 128 * v16; i += UB_THREADS) {
-        const int r = i / v16, c = i - r * v16;
-        *reinterpret_cast<uint4*>(hb + static_cast<int64_t>(r) * N + 8 * c) = make_uint4(0, 0, 0, 0);
-    }
-    __syncthreads();
-    // scatter: warp per row, coalesced word reads (same scheme as the OR pass above)
-    for (int r = warp; r < rows; r += nwarps) {
-        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
-        uint16_t* hrow = hb + static_cast<int64_t>(r) * N;
-        if (WPT <= 32) {
-            for (int w0 = 0; w0 < RW; w0 += 128) {
-                uint32_t v[4];
+}
+
+// G_b: the stored gate values in union coordinates, H_c[b*128 + r, j] (bf16), zero elsewhere; the up-GEMM
+// epilogue multiplies this tile in place by X_b W_u[U_b]^T.  One CTA (256 threads) per 8 rows of a block.
+constexpr int GS_ROWS = 8;
+__global__ void __launch_bounds__(256) union_gate_scatter_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
+                                                                 int C, UnionMeta um, uint16_t* __restrict__ hc,
+                                                                 const int32_t* __restrict__ perm) {
+    const int b = blockIdx.x / (128 / GS_ROWS);
+    const int r0 = (blockIdx.x % (128 / GS_ROWS)) * GS_ROWS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp w handles row r0 + w
+    const int NW = N >> 5, NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
+    const int padded = __ldg(um.ulen + b);
+    const uint32_t* msk = um.umask + static_cast<int64_t>(b) * NW;
+    const int32_t* wof = um.uwoff + static_cast<int64_t>(b) * NW;
+    const int r = r0 + warp;
+    uint16_t* hrow = hc + (static_cast<int64_t>(b) * 128 + r) * N;
+    for (int c = lane; c < padded / 8; c += 32) *reinterpret_cast<uint4*>(hrow + 8 * c) = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    if (b * 128 + r >= M) return;
+    const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
+    if (WPT <= 32) {
+        for (int w0 = 0; w0 < RW; w0 += 128) {
+            uint32_t v[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = (w0 + 32 * u + lane < RW) ? __ldg(row + w0 + 32 * u + lane) : 0u;
+            for (int u = 0; u < 4; ++u) v[u] = (w0 + 32 * u + lane < RW) ? __ldg(row + w0 + 32 * u + lane) : 0u;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int slot = (w0 + 32 * u + lane) % WPT;
-                    const int cnt = min(static_cast<int>(__shfl_sync(0xffffffffu, v[u], lane - slot)), cap);
-                    if (slot >= 1 && slot <= cnt && w0 + 32 * u + lane < RW) {
-                        const int n = static_cast<int>(v[u] & 0xFFFFu);
-                        const int j = woff[n >> 5] + __popc(mask[n >> 5] & ((1u << (n & 31)) - 1u));
-                        hrow[j] = static_cast<uint16_t>(v[u] >> 16);
-                    }
+            for (int u = 0; u < 4; ++u) {
+                const int slot = (w0 + 32 * u + lane) % WPT;
+                const int cnt = min(static_cast<int>(__shfl_sync(0xffffffffu, v[u], lane - slot)), cap);
+                if (slot >= 1 && slot <= cnt && w0 + 32 * u + lane < RW) {
+                    const int n = static_cast<int>(v[u] & 0xFFFFu);
+                    const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
+                    hrow[j] = static_cast<uint16_t>(v[u] >> 16);
                 }
             }
-        } else {
-            for (int t = 0; t < NT; ++t) {
-                const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
-                const int cnt = min(static_cast<int>(__ldg(blk)), cap);
-                for (int e = lane; e < cnt; e += 32) {
-                    const uint32_t w = __ldg(blk + 1 + e);
-                    const int n = static_cast<int>(w & 0xFFFFu);
-                    const int j = woff[n >> 5] + __popc(mask[n >> 5] & ((1u << (n & 31)) - 1u));
-                    hrow[j] = static_cast<uint16_t>(w >> 16);
-                }
+        }
+    } else {
+        for (int t = 0; t < NT; ++t) {
+            const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
+            const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+            for (int e = lane; e < cnt; e += 32) {
+                const uint32_t w = __ldg(blk + 1 + e);
+                const int n = static_cast<int>(w & 0xFFFFu);
+                const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
+                hrow[j] = static_cast<uint16_t>(w >> 16);
             }
         }
     }
@@ -192,6 +198,7 @@ __global__ void __launch_bounds__(1024) union_perm_kernel(const uint32_t* __rest
             const int m = w0 + i;
             const uint32_t* row = tw + static_cast<int64_t>(m) * RW;
             int nnz = 0;
+#pragma unroll 8
             for (int t = 0; t < NT; ++t) nnz += min(static_cast<int>(__ldg(row + static_cast<int64_t>(t) * WPT)), cap);
             key = (static_cast<unsigned long long>(0x7FFFFFFF - nnz) << 32) | static_cast<unsigned>(m);
         }
