@@ -142,6 +142,15 @@ int sffn_transpose_bf16(const void* in, int64_t rows, int64_t cols, void* out, v
 int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, float* S, void* stream);
 
 /*
+ * sffn_union_stats — measurement helper for SFFN_ALGO_UNION: after sffn_up_down (workspace = its
+ * workspace) synchronizes `stream` and returns the sum over 128-row blocks of the padded union sizes
+ * (the tensor-core work is 4 * 128 * padded_sum * K FLOP), of the exact union sizes, and the number of
+ * up-GEMM tiles.  Any output pointer may be NULL.
+ */
+int sffn_union_stats(const void* workspace, int64_t M, int64_t K, int64_t N, int64_t* padded_sum, int64_t* real_sum,
+                     int64_t* up_tiles, void* stream);
+
+/*
  * sffn_overflow_check — synchronizes `stream`, copies *d_overflow to *host_count (if non-NULL) and
  * returns SFFN_ERR_TILE_OVERFLOW if it is non-zero, else SFFN_OK.
  */

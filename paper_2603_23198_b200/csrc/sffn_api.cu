@@ -540,6 +540,35 @@ int sffn_forward_f32(const float* X, const float* Wg, const float* Wu, const flo
     return sffn_up_down_f32(X, hv, hi, hnz, Wu, Wd, M, K, N, T, C, Y, stream);
 }
 
+int sffn_union_stats(const void* workspace, int64_t M, int64_t K, int64_t N, int64_t* padded_sum, int64_t* real_sum,
+                     int64_t* up_tiles, void* stream) {
+    if (!workspace || M <= 0 || N <= 0 || K <= 0) return SFFN_ERR_INVALID_ARG;
+    const int64_t NB = (M + 127) / 128;
+    UnionWs L = union_ws_layout(M, N, K);
+    const uint8_t* base = static_cast<const uint8_t*>(workspace);
+    int32_t* h = static_cast<int32_t*>(std::malloc(static_cast<size_t>(2 * NB + 1) * 4));
+    if (!h) return SFFN_ERR_INVALID_ARG;
+    cudaStream_t st = S(stream);
+    int r = SFFN_OK;
+    if (cudaMemcpyAsync(h, base + L.ulen, NB * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(h + NB, base + L.utot, NB * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(h + 2 * NB, base + L.chunk, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        r = SFFN_ERR_CUDA;
+    if (r == SFFN_OK) {
+        int64_t a = 0, b = 0;
+        for (int64_t i = 0; i < NB; ++i) {
+            a += h[i];
+            b += h[NB + i];
+        }
+        if (padded_sum) *padded_sum = a;
+        if (real_sum) *real_sum = b;
+        if (up_tiles) *up_tiles = h[2 * NB];
+    }
+    std::free(h);
+    return r;
+}
+
 int sffn_overflow_check(const uint32_t* d_overflow, void* stream, uint32_t* host_count) {
     if (!d_overflow) return SFFN_ERR_INVALID_ARG;
     uint32_t h = 0;

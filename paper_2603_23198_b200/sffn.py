@@ -48,6 +48,7 @@ _SIGS = {
                                     _int, _int, _vp]),
     "sffn_allreduce_bf16": (_int, [_vp, _vp, _i64, _vp]),
     "sffn_f32_twell_bytes": (_sz, [_i64, _i64, _int, _int]),
+    "sffn_union_stats": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "sffn_pack_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "sffn_up_down_f32": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp]),
     "sffn_forward_f32": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _vp]),
@@ -212,6 +213,14 @@ def gate_gemm_f32(x, wg, out=None, stream=None) -> torch.Tensor:
     _chk(lib().sffn_gate_gemm_f32(_bf16(x, "x"), _bf16(wg, "wg"), M, K, N, _p(out), _stream(stream)),
          "sffn_gate_gemm_f32")
     return out
+
+
+def union_stats(up_down_workspace: torch.Tensor, M: int, K: int, N: int, stream=None) -> dict:
+    """Union sizes left in an sffn_up_down(algo="union") workspace (synchronizes the stream)."""
+    a, b, t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _chk(lib().sffn_union_stats(_p(up_down_workspace), M, K, N, ctypes.byref(a), ctypes.byref(b), ctypes.byref(t),
+                                _stream(stream)), "sffn_union_stats")
+    return {"padded_sum": a.value, "union_sum": b.value, "up_tiles": t.value}
 
 
 def overflow_check(overflow: torch.Tensor, stream=None) -> int:
