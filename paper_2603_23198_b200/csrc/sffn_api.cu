@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/sffn.h"
 #include "gemm_tc.cuh"
@@ -538,6 +539,87 @@ int sffn_forward_f32(const float* X, const float* Wg, const float* Wu, const flo
     int r = sffn_pack_f32(X, Wg, M, K, N, T, C, hv, hi, hnz, d_overflow, stream);
     if (r != SFFN_OK) return r;
     return sffn_up_down_f32(X, hv, hi, hnz, Wu, Wd, M, K, N, T, C, Y, stream);
+}
+
+// ---------------------------------------------------------------- host-buffer forward (copy/compute overlap)
+namespace {
+struct CopyStreams {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+};
+std::mutex g_cs_mu;
+CopyStreams g_cs[64];
+int copy_streams(int dev, CopyStreams* out) {
+    if (dev < 0 || dev >= 64) return SFFN_ERR_UNSUPPORTED;
+    std::lock_guard<std::mutex> lk(g_cs_mu);
+    CopyStreams& c = g_cs[dev];
+    if (!c.h2d) {
+        if (cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking) != cudaSuccess) return SFFN_ERR_CUDA;
+        if (cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking) != cudaSuccess) return SFFN_ERR_CUDA;
+    }
+    *out = c;
+    return SFFN_OK;
+}
+}  // namespace
+
+size_t sffn_forward_host_stage_bytes(int64_t K, int64_t chunk_rows) {
+    if (K <= 0 || chunk_rows <= 0) return 0;
+    return static_cast<size_t>(4 * align1k(chunk_rows * K * 2));  // 2 x X slots + 2 x Y slots
+}
+
+int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
+                      int64_t N, int T, int C, void* Y_host, void* workspace, size_t ws_bytes, void* stage,
+                      size_t stage_bytes, uint32_t* d_overflow, int algo, int64_t chunk_rows, void* stream) {
+    if (!X_host || !Y_host || !stage) return M == 0 ? SFFN_OK : SFFN_ERR_INVALID_ARG;
+    if (chunk_rows <= 0 || chunk_rows % 128 != 0) return SFFN_ERR_SHAPE;
+    if (M < 0 || K <= 0) return SFFN_ERR_SHAPE;
+    if (M == 0) return SFFN_OK;
+    const int64_t rows = chunk_rows < M ? chunk_rows : ((M + 127) / 128) * 128;
+    if (stage_bytes < sffn_forward_host_stage_bytes(K, rows)) return SFFN_ERR_SHAPE;
+    if (ws_bytes < sffn_forward_workspace_bytes(rows < M ? rows : M, K, N, T, C, algo)) return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    CopyStreams cs;
+    if ((r = copy_streams(dev, &cs)) != SFFN_OK) return r;
+    cudaStream_t st = S(stream);
+    const int64_t nchunks = (M + rows - 1) / rows;
+    const int64_t slot = align1k(rows * K * 2);
+    uint8_t* xs[2] = {static_cast<uint8_t*>(stage), static_cast<uint8_t*>(stage) + slot};
+    uint8_t* ys[2] = {static_cast<uint8_t*>(stage) + 2 * slot, static_cast<uint8_t*>(stage) + 3 * slot};
+    // events: per chunk h2d done, compute done, d2h done
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(3 * nchunks + 1));
+    for (auto& e : ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SFFN_ERR_CUDA;
+    auto E = [&](int kind, int64_t i) { return ev[static_cast<size_t>(3 * i + kind)]; };
+    // the copies must not start before earlier work on `stream`
+    cudaEventRecord(ev.back(), st);
+    cudaStreamWaitEvent(cs.h2d, ev.back(), 0);
+    cudaStreamWaitEvent(cs.d2h, ev.back(), 0);
+    for (int64_t i = 0; i < nchunks && r == SFFN_OK; ++i) {
+        const int64_t r0 = i * rows, mr = (M - r0) < rows ? (M - r0) : rows;
+        const size_t bytes = static_cast<size_t>(mr * K * 2);
+        const int sl = static_cast<int>(i & 1);
+        if (i >= 2) cudaStreamWaitEvent(cs.h2d, E(1, i - 2), 0);  // X slot free once chunk i-2 computed
+        if (cudaMemcpyAsync(xs[sl], static_cast<const uint8_t*>(X_host) + r0 * K * 2, bytes, cudaMemcpyHostToDevice,
+                            cs.h2d) != cudaSuccess) { r = SFFN_ERR_CUDA; break; }
+        cudaEventRecord(E(0, i), cs.h2d);
+        cudaStreamWaitEvent(st, E(0, i), 0);
+        if (i >= 2) cudaStreamWaitEvent(st, E(2, i - 2), 0);  // Y slot free once chunk i-2 copied out
+        r = sffn_forward(xs[sl], Wg, Wu, Wd, mr, K, N, T, C, ys[sl], workspace, ws_bytes, d_overflow, algo, stream);
+        if (r != SFFN_OK) break;
+        cudaEventRecord(E(1, i), st);
+        cudaStreamWaitEvent(cs.d2h, E(1, i), 0);
+        if (cudaMemcpyAsync(static_cast<uint8_t*>(Y_host) + r0 * K * 2, ys[sl], bytes, cudaMemcpyDeviceToHost,
+                            cs.d2h) != cudaSuccess) { r = SFFN_ERR_CUDA; break; }
+        cudaEventRecord(E(2, i), cs.d2h);
+    }
+    if (r == SFFN_OK) {
+        cudaEventRecord(ev.back(), cs.d2h);
+        cudaStreamWaitEvent(st, ev.back(), 0);  // the call completes on `stream`
+    }
+    for (auto& e : ev) cudaEventDestroy(e);  // destruction is deferred until the events complete
+    return r;
 }
 
 int sffn_union_stats(const void* workspace, int64_t M, int64_t K, int64_t N, int64_t* padded_sum, int64_t* real_sum,

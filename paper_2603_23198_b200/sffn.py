@@ -49,6 +49,9 @@ _SIGS = {
     "sffn_allreduce_bf16": (_int, [_vp, _vp, _i64, _vp]),
     "sffn_f32_twell_bytes": (_sz, [_i64, _i64, _int, _int]),
     "sffn_union_stats": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "sffn_forward_host_stage_bytes": (_sz, [_i64, _i64]),
+    "sffn_forward_host": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _sz, _vp, _int,
+                                 _i64, _vp]),
     "sffn_pack_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "sffn_up_down_f32": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp]),
     "sffn_forward_f32": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _vp]),
@@ -181,6 +184,27 @@ def forward(x, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, o
     _chk(lib().sffn_forward(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
                             _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(),
                             _p(overflow), a, _stream(stream)), "sffn_forward")
+    return out
+
+
+def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, stage=None,
+                 overflow=None, algo="auto", chunk_rows: int = 4096, stream=None) -> torch.Tensor:
+    """Sparse forward with X / Y in (pinned) host memory; copies overlap compute (sffn_forward_host)."""
+    M, K = x_host.shape
+    N = wg.shape[0]
+    if x_host.is_cuda or x_host.dtype != torch.bfloat16 or not x_host.is_contiguous():
+        raise ValueError("x_host must be a contiguous bf16 CPU tensor (pinned for overlap)")
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, pin_memory=True)
+    a = _algo(algo)
+    rows = min(chunk_rows, ((M + 127) // 128) * 128)
+    workspace = _ws(workspace_bytes(min(rows, M), K, N, T, C, a), wg.device, workspace)
+    stage = _ws(int(lib().sffn_forward_host_stage_bytes(K, rows)), wg.device, stage)
+    _chk(lib().sffn_forward_host(ctypes.c_void_p(x_host.data_ptr()), _bf16(wg, "wg"), _bf16(wu, "wu"),
+                                 _bf16(wd, "wd"), M, K, N, T, C, ctypes.c_void_p(out.data_ptr()), _p(workspace),
+                                 workspace.numel() * workspace.element_size(), _p(stage),
+                                 stage.numel() * stage.element_size(), _p(overflow), a, chunk_rows,
+                                 _stream(stream)), "sffn_forward_host")
     return out
 
 

@@ -340,3 +340,16 @@ def test_fp32_forward_gaussian(sffn):
     Y = sffn.forward_f32(t(X), t(Wg), t(Wu), t(Wd), T, C)
     Y1 = oracle.ffn_dense_f32(X, Wg, Wu, Wd)
     assert rel_fro(Y.cpu().numpy().astype(np.float64), Y1) < F32_TOL
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_forward_host_pipeline(sffn, algo):
+    """Host-buffer forward (chunked copy/compute overlap) == device forward, bit-identical (chunks are
+    multiples of the 2048-row permutation window)."""
+    cfg = synth.CONFIGS["1B"].replace(M=5000, K=256, N=1024, Kb=16, sparsity=0.97)
+    X, Wg, Wu, Wd = inputs(cfg)
+    ref = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo)
+    xh = torch.from_numpy(X.view(np.int16)).view(torch.bfloat16).pin_memory()
+    yh = sffn.forward_host(xh, to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo, chunk_rows=2048)
+    torch.cuda.synchronize()
+    assert torch.equal(yh.view(torch.int16), ref.cpu().view(torch.int16))
