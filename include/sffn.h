@@ -123,6 +123,21 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
                  void* stream);
 
 /*
+ * sffn_forward_host — sffn_forward with X and Y in HOST memory (page-locked for overlap): rows are
+ * processed in chunks of `chunk_rows` (a multiple of 128; a multiple of 2048 keeps the UNION row
+ * permutation windows, hence the results, identical to one sffn_forward call); the host->device copy of
+ * chunk i+1 and the device->host copy of chunk i-1 overlap the compute of chunk i on two internal copy
+ * streams (created once per device, event-ordered; no host synchronization).  The call is
+ * stream-ordered on `stream`: Y_host is complete when `stream` reaches this point.
+ *   stage: device buffer >= sffn_forward_host_stage_bytes(K, chunk_rows) (2 X + 2 Y chunk slots)
+ *   workspace: >= sffn_forward_workspace_bytes(min(chunk_rows, M), K, N, T, C, algo)
+ */
+size_t sffn_forward_host_stage_bytes(int64_t K, int64_t chunk_rows);
+int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
+                      int64_t N, int T, int C, void* Y_host, void* workspace, size_t ws_bytes, void* stage,
+                      size_t stage_bytes, uint32_t* d_overflow, int algo, int64_t chunk_rows, void* stream);
+
+/*
  * sffn_dense_forward — the library's own dense tcgen05 FFN (Eq.1 without sparsity): the speedup
  * denominator.  Launch 1: fused gate||up GEMM with epilogue H = bf16(relu(g) * u)   (H [M, N] bf16,
  * caller-owned).  Launch 2: Y = H W_d as a GEMM against WdT = W_d^T stored [K, N] row-major (a
