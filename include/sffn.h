@@ -60,7 +60,7 @@ typedef enum {
  *                     per block of 128 rows, the union U_b of their active neurons; the up projection
  *                     X_b W_u[U_b]^T and the down projection H_b W_d[U_b] run on tcgen05 tensor cores
  *                     with the gate applied in the epilogue (zero off-pattern, so skipped terms are
- *                     exactly the h_g = 0 terms of Alg.2); W_u / W_d rows gathered by TMA gather4.
+ *                     exactly the h_g = 0 terms of Alg.2); W_u / W_d rows gathered with cp.async.
  *                     Needs workspace (sffn_up_down_workspace_bytes) and N % 64 == 0.
  *   SFFN_ALGO_AUTO  : UNION when N % 64 == 0, else GATHER. */
 typedef enum { SFFN_ALGO_AUTO = 0, SFFN_ALGO_GATHER = 1, SFFN_ALGO_UNION = 2 } sffn_algo;

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 for (int half = 0; half < 2; ++half) {
                     const int c0 = cj * 256 + half * 128;
                     const int nc = min(128, args.K - c0);
-                    if (lane == 0) bulk_wait_read0();
+                    bulk_wait_read0();  // every lane's own bulk copy (per-thread bulk group) has read its row
                     __syncwarp();
 #pragma unroll 1
                     for (int ch = 0; ch < 4; ++ch) {
@@ -442,7 +442,11 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 acc_phase ^= 1;
             }
         }
-        if (lane == 0) bulk_wait0();
+        if (UP) {
+            if (lane == 0) bulk_wait0();
+        } else {
+            bulk_wait0();  // per-thread bulk groups of the row copies
+        }
     }
 
     __syncwarp();
