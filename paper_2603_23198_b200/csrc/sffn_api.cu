@@ -179,7 +179,7 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, total;
+    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, total;
 };
 UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K) {
     const int64_t NB = (M + 127) / 128;
@@ -196,6 +196,7 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K) {
     w.perm = o;  o = align1k(o + M * 4);
     w.xp = o;    o = align1k(o + M * K * 2);
     w.ctr = o;   o = align1k(o + 64);
+    w.nnz = o;   o = align1k(o + M * 4);
     w.total = o;
     return w;
 }
@@ -230,7 +231,10 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     int32_t* perm = reinterpret_cast<int32_t*>(base + L.perm);
     void* xp = base + L.xp;
     // row permutation pi (per 2048-row window, descending stored nnz) and the permuted copy of X
-    union_perm_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), 1024, 0, st>>>(tw, (int)M, (int)N, T, C, perm);
+    int* rnnz = reinterpret_cast<int*>(base + L.nnz);
+    row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz);
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    union_perm_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), 1024, 0, st>>>(rnnz, (int)M, perm);
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
         static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp));

@@ -186,22 +186,29 @@ __global__ void __launch_bounds__(256) union_gate_scatter_kernel(const uint32_t*
 // window of PERM_W consecutive rows (one 2048-token sequence), rows sorted by stored non-zeros
 // descending, ties by row index -> unique keys, deterministic.  Blocks of 128 never straddle windows.
 constexpr int PERM_W = 2048;
-__global__ void __launch_bounds__(1024) union_perm_kernel(const uint32_t* __restrict__ tw, int M, int N, int T, int C,
-                                                          int32_t* __restrict__ perm) {
+
+// stored non-zeros per row (warp per row; lanes stride over the row's count words)
+__global__ void row_nnz_kernel(const uint32_t* __restrict__ tw, int M, int N, int T, int C, int* __restrict__ nnz) {
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= M) return;
+    const int NT = N / T, WPT = T / C, cap = WPT - 1;
+    const uint32_t* row = tw + gw * (N / C);
+    int s = 0;
+    for (int t = lane; t < NT; t += 32) s += min(static_cast<int>(__ldg(row + static_cast<int64_t>(t) * WPT)), cap);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) nnz[gw] = s;
+}
+
+__global__ void __launch_bounds__(1024) union_perm_kernel(const int* __restrict__ nnz, int M, int32_t* __restrict__ perm) {
     __shared__ unsigned long long keys[PERM_W];
     const int w0 = blockIdx.x * PERM_W;
     const int rows = min(PERM_W, M - w0);
-    const int NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
     for (int i = threadIdx.x; i < PERM_W; i += 1024) {
         unsigned long long key = ~0ull;  // padding sorts last
-        if (i < rows) {
-            const int m = w0 + i;
-            const uint32_t* row = tw + static_cast<int64_t>(m) * RW;
-            int nnz = 0;
-#pragma unroll 8
-            for (int t = 0; t < NT; ++t) nnz += min(static_cast<int>(__ldg(row + static_cast<int64_t>(t) * WPT)), cap);
-            key = (static_cast<unsigned long long>(0x7FFFFFFF - nnz) << 32) | static_cast<unsigned>(m);
-        }
+        if (i < rows)
+            key = (static_cast<unsigned long long>(0x7FFFFFFF - __ldg(nnz + w0 + i)) << 32) | static_cast<unsigned>(w0 + i);
         keys[i] = key;
     }
     __syncthreads();
