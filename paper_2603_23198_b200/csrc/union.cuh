@@ -31,6 +31,44 @@ constexpr int UNION_GROUP_DOWN = 16;  // token blocks whose down-GEMM tiles run 
 
 constexpr int UB_THREADS = 512;
 
+// Visit every stored entry (n, word) of one packed TwELL row: warp-cooperative, lane-ordered.
+// Fast path (4 <= T/C <= 32): 16-byte loads, each warp instruction covers 128 words; a lane's 4 words lie in
+// one tile whose count word sits in the lane holding the tile's first word (shuffle).  Generic path otherwise.
+template <class F>
+__device__ __forceinline__ void for_each_row_entry(const uint32_t* __restrict__ row, int RW, int NT, int WPT, int cap,
+                                                   int lane, F&& f) {
+    if (WPT >= 4 && WPT <= 32) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(row);
+        const int RW4 = RW >> 2;
+        for (int g0 = 0; g0 < RW4; g0 += 64) {
+            uint4 v[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) v[u] = (g0 + 32 * u + lane < RW4) ? __ldg(r4 + g0 + 32 * u + lane) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int w0 = 4 * (g0 + 32 * u + lane);  // first word of this lane
+                const int s0 = w0 % WPT;                 // slot of v.x
+                const int src = lane - (s0 >> 2);
+                const int cnt = min(static_cast<int>(__shfl_sync(0xffffffffu, v[u].x, src)), cap);
+                if (w0 < RW) {
+                    const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int sl = s0 + q;
+                        if (sl >= 1 && sl <= cnt) f(w[q]);
+                    }
+                }
+            }
+        }
+    } else {
+        for (int t = 0; t < NT; ++t) {
+            const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
+            const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+            for (int e = lane; e < cnt; e += 32) f(__ldg(blk + 1 + e));
+        }
+    }
+}
+
 // One CTA per block of 128 rows.  Dynamic smem: N/32 uint32 masks + N/32 int32 offsets + scan scratch.
 __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
                                                                   int C, UnionMeta um, const int32_t* __restrict__ perm) {
@@ -51,31 +89,10 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
     const int rows = min(128, M - b * 128);
     for (int r = warp; r < rows; r += nwarps) {
         const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
-        if (WPT <= 32) {
-            for (int w0 = 0; w0 < RW; w0 += 128) {
-                uint32_t v[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = (w0 + 32 * u + lane < RW) ? __ldg(row + w0 + 32 * u + lane) : 0u;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int slot = (w0 + 32 * u + lane) % WPT;
-                    const int cnt = min(static_cast<int>(__shfl_sync(0xffffffffu, v[u], lane - slot)), cap);
-                    if (slot >= 1 && slot <= cnt && w0 + 32 * u + lane < RW) {
-                        const uint32_t n = v[u] & 0xFFFFu;
-                        atomicOr(&mask[n >> 5], 1u << (n & 31));
-                    }
-                }
-            }
-        } else {
-            for (int t = 0; t < NT; ++t) {
-                const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
-                const int cnt = min(static_cast<int>(__ldg(blk)), cap);
-                for (int e = lane; e < cnt; e += 32) {
-                    const uint32_t n = __ldg(blk + 1 + e) & 0xFFFFu;
-                    atomicOr(&mask[n >> 5], 1u << (n & 31));
-                }
-            }
-        }
+        for_each_row_entry(row, RW, NT, WPT, cap, lane, [&](uint32_t w) {
+            const uint32_t n = w & 0xFFFFu;
+            atomicOr(&mask[n >> 5], 1u << (n & 31));
+        });
     }
     __syncthreads();
 
@@ -152,34 +169,11 @@ __global__ void __launch_bounds__(256) union_gate_scatter_kernel(const uint32_t*
     __syncwarp();
     if (b * 128 + r >= M) return;
     const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
-    if (WPT <= 32) {
-        for (int w0 = 0; w0 < RW; w0 += 128) {
-            uint32_t v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = (w0 + 32 * u + lane < RW) ? __ldg(row + w0 + 32 * u + lane) : 0u;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int slot = (w0 + 32 * u + lane) % WPT;
-                const int cnt = min(static_cast<int>(__shfl_sync(0xffffffffu, v[u], lane - slot)), cap);
-                if (slot >= 1 && slot <= cnt && w0 + 32 * u + lane < RW) {
-                    const int n = static_cast<int>(v[u] & 0xFFFFu);
-                    const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
-                    hrow[j] = static_cast<uint16_t>(v[u] >> 16);
-                }
-            }
-        }
-    } else {
-        for (int t = 0; t < NT; ++t) {
-            const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
-            const int cnt = min(static_cast<int>(__ldg(blk)), cap);
-            for (int e = lane; e < cnt; e += 32) {
-                const uint32_t w = __ldg(blk + 1 + e);
-                const int n = static_cast<int>(w & 0xFFFFu);
-                const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
-                hrow[j] = static_cast<uint16_t>(w >> 16);
-            }
-        }
-    }
+    for_each_row_entry(row, RW, NT, WPT, cap, lane, [&](uint32_t w) {
+        const int n = static_cast<int>(w & 0xFFFFu);
+        const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
+        hrow[j] = static_cast<uint16_t>(w >> 16);
+    });
 }
 
 // Row permutation pi (Alg.2 iterates m in pi(0..M-1); descending-nnz order): within each
