@@ -122,6 +122,20 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
                  int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo,
                  void* stream);
 
+/* ---------------------------------------------------------------- non-gated variant (App.C, NEXT-2)
+ * h = relu(x W_u), y = h W_d: the TwELL now comes from the UP projection (the same
+ * tcgen05 pack kernel applied to W_u), and only the down projection remains (Listing 3,
+ * P:1085-1215).
+ * sffn_down: Y[m,:] = sum over the stored entries (n, h_v) of h_v * Wd[n,:]  (fp32 accumulate, bf16 Y).
+ *   GATHER: one CTA per row, each warp owns a K slice (the paper's SPLIT_OUT_DIM); UNION: the union
+ *   pipeline with the scattered TwELL values as H (no up GEMM).  Workspace as sffn_up_down.
+ * sffn_forward_nongated: sffn_pack(X, Wu) into the workspace, then sffn_down (workspace as sffn_forward). */
+int sffn_down(const uint32_t* twell, const void* Wd, int64_t M, int64_t K, int64_t N, int T, int C, void* Y,
+              void* workspace, size_t ws_bytes, int algo, void* stream);
+int sffn_forward_nongated(const void* X, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N, int T,
+                          int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo,
+                          void* stream);
+
 /*
  * sffn_forward_host — sffn_forward with X and Y in HOST memory (page-locked for overlap): rows are
  * processed in chunks of `chunk_rows` (a multiple of 128; a multiple of 2048 keeps the UNION row

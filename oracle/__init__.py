@@ -46,6 +46,8 @@ def _load():
         lib.oracle_unpack.argtypes = [vp, i64, i64, ci, ci, vp]
         lib.oracle_ffn_dense.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp]
         lib.oracle_ffn_twell.argtypes = [vp, vp, vp, vp, i64, i64, i64, ci, ci, ci, vp, vp]
+        lib.oracle_ffn_nongated_dense.argtypes = [vp, vp, vp, i64, i64, i64, vp]
+        lib.oracle_down_twell.argtypes = [vp, vp, i64, i64, i64, ci, ci, ci, vp, vp]
         lib.oracle_pack_soa.argtypes = [vp, i64, i64, ci, ci, vp, vp, vp]
         lib.oracle_pack_soa.restype = i64
         lib.oracle_ffn_dense_f32.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp]
@@ -208,3 +210,28 @@ def soa_prefix_equal(a, b, T: int, C: int) -> np.ndarray:
     ia, ib = hia.reshape(M, -1, W), hib.reshape(M, -1, W)
     eq = ((va.view(np.uint32) == vb.view(np.uint32)) & (ia == ib)) | ~valid
     return cnt_eq & np.all(eq, axis=2)
+
+
+# ---------------------------------------------------------------- non-gated variant (App.C, NEXT-2)
+def ffn_nongated_dense(X, Wu, Wd) -> np.ndarray:
+    """y = relu(x W_u) W_d, fp64."""
+    X, Wu, Wd = map(_u16, (X, Wu, Wd))
+    M, K = X.shape
+    N = Wu.shape[0]
+    Y = np.empty((M, K), dtype=np.float64)
+    _load().oracle_ffn_nongated_dense(X.ctypes.data, Wu.ctypes.data, Wd.ctypes.data, M, K, N, Y.ctypes.data)
+    return Y
+
+
+def down_twell(words, Wd, K: int, N: int, T: int, C: int, A=None) -> np.ndarray:
+    """sum over stored entries of h_v * W_d[n, :] (Listing 3 semantics); exact A instead of h_v if given."""
+    Wd = _u16(Wd)
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    M = words.shape[0]
+    Y = np.empty((M, K), dtype=np.float64)
+    mode, Ap = 0, None
+    if A is not None:
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        mode, Ap = 1, A.ctypes.data
+    _load().oracle_down_twell(words.ctypes.data, Wd.ctypes.data, M, K, N, T, C, mode, Ap, Y.ctypes.data)
+    return Y

@@ -256,3 +256,42 @@ void oracle_ffn_soa_f32(const float* X, const float* hv, const uint16_t* hi, con
         }
     }
 }
+
+/* Non-gated FFN, App.C eq.: h = relu(x W_u), y = h W_d, fp64.  Y double [M, K]. */
+void oracle_ffn_nongated_dense(const uint16_t* X, const uint16_t* Wu, const uint16_t* Wd, int64_t M, int64_t K,
+                               int64_t N, double* Y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t j = 0; j < K; ++j) Y[m * K + j] = 0.0;
+        for (int64_t n = 0; n < N; ++n) {
+            double a = 0.0;
+            for (int64_t k = 0; k < K; ++k)
+                a += oracle_bf16_to_double(X[m * K + k]) * oracle_bf16_to_double(Wu[n * K + k]);
+            if (a > 0.0)
+                for (int64_t j = 0; j < K; ++j) Y[m * K + j] += a * oracle_bf16_to_double(Wd[n * K + j]);
+        }
+    }
+}
+
+/* Down projection from a packed TwELL of h (Listing 3 semantics):
+ *   y[m,:] = sum over the stored entries (n, h_v) of h_v * W_d[n,:]   (fp64, stored order).
+ * gate_mode 1: h_v replaced by the exact A[m, n] (then equals the dense non-gated FFN exactly). */
+void oracle_down_twell(const uint32_t* words, const uint16_t* Wd, int64_t M, int64_t K, int64_t N, int T, int C,
+                       int gate_mode, const double* A, double* Y) {
+    const int64_t NT = N / T, W = T / C, cap = W - 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t j = 0; j < K; ++j) Y[m * K + j] = 0.0;
+        for (int64_t t = 0; t < NT; ++t) {
+            const uint32_t* blk = words + m * (N / C) + t * W;
+            int64_t z = blk[0];
+            if (z > cap) z = cap;
+            for (int64_t c = 0; c < z; ++c) {
+                uint32_t w = blk[1 + c];
+                int64_t n = (int64_t)(w & 0xFFFFu);
+                double h = gate_mode == 1 ? A[m * N + n] : oracle_bf16_to_double((uint16_t)(w >> 16));
+                for (int64_t j = 0; j < K; ++j) Y[m * K + j] += h * oracle_bf16_to_double(Wd[n * K + j]);
+            }
+        }
+    }
+}

@@ -214,7 +214,7 @@ size_t updown_ws_bytes(int64_t M, int64_t N, int64_t K, int algo) {
 }
 
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
-                      int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st) {
+                      int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true) {
     const int64_t NB = (M + 127) / 128;
     UnionWs L = union_ws_layout(M, N, K);
     uint8_t* base = static_cast<uint8_t*>(ws);
@@ -236,9 +236,11 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     union_perm_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), 1024, 0, st>>>(rnnz, (int)M, perm);
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
-        static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp));
-    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    if (gated) {
+        permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+            static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp));
+        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    }
 
     const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
     union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um, perm);
@@ -250,7 +252,8 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
 
     CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
-    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M > 0 ? M : 1, GEMM_BK, GEMM_BM,
+                 CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&thc_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, GEMM_BK, GEMM_BM,
@@ -285,9 +288,12 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     });
     if (attr != cudaSuccess) return SFFN_ERR_CUDA;
     const int sms = dev_info().sms;
-    // UP: the number of (block, chunk) tiles is only known on the device; persistent grid
-    union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua);
-    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    if (gated) {
+        // UP: the number of (block, chunk) tiles is only known on the device; persistent grid.  For the
+        // non-gated variant H_c already holds h = relu(x W_u) (the scattered TwELL values): no UP GEMM.
+        union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua);
+        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    }
     const int64_t dtiles = NB * ua.NJ;
     const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
     union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud);
@@ -399,6 +405,47 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
     return updown_dispatch(X, tw, Wu, Wd, M, K, N, T, C, Y, static_cast<uint8_t*>(workspace) + tw_bytes,
                            ws_bytes - static_cast<size_t>(tw_bytes), algo, S(stream));
+}
+
+int sffn_down(const uint32_t* twell, const void* Wd, int64_t M, int64_t K, int64_t N, int T, int C, void* Y,
+              void* workspace, size_t ws_bytes, int algo, void* stream) {
+    int r = updown_checks(Wd, twell, Wd, Wd, M, K, N, T, C, Y);
+    if (r != SFFN_OK) return r;
+    if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
+    const int a = resolve_algo(algo, N);
+    if (a == SFFN_ALGO_UNION && M > 0) {
+        if (!union_applicable(N)) return SFFN_ERR_SHAPE;
+        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, K, a)) return SFFN_ERR_SHAPE;
+    }
+    if ((r = check_device()) != SFFN_OK) return r;
+    if (M == 0) return SFFN_OK;
+    cudaStream_t st = S(stream);
+    if (a == SFFN_ALGO_UNION) return union_updown_impl(Wd, twell, Wd, Wd, M, K, N, T, C, Y, workspace, st, false);
+    const int64_t per_warp = (K / 8 + UD_WARPS - 1) / UD_WARPS;
+    const int nch = static_cast<int>((per_warp + 31) / 32);
+    const uint4* wd = static_cast<const uint4*>(Wd);
+    uint4* y = static_cast<uint4*>(Y);
+    dim3 g(static_cast<unsigned>(M)), blk(UD_WARPS * 32);
+    if (nch <= 1) down_kernel<1><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch <= 2) down_kernel<2><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch <= 4) down_kernel<4><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
+    else if (nch <= 8) down_kernel<8><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
+    else return SFFN_ERR_SHAPE;
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_forward_nongated(const void* X, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N, int T, int C,
+                          void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream) {
+    int r = pack_checks(X, Wu, M, K, N, T, C, workspace);
+    if (r != SFFN_OK) return r;
+    if (ws_bytes < sffn_forward_workspace_bytes(M, K, N, T, C, algo)) return SFFN_ERR_SHAPE;
+    if ((r = check_device()) != SFFN_OK) return r;
+    if (M == 0) return SFFN_OK;
+    uint32_t* tw = static_cast<uint32_t*>(workspace);
+    const int64_t tw_bytes = align1k(sffn_twell_words(M, N, T, C) * 4);
+    if ((r = pack_impl(X, Wu, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
+    return sffn_down(tw, Wd, M, K, N, T, C, Y, static_cast<uint8_t*>(workspace) + tw_bytes,
+                     ws_bytes - static_cast<size_t>(tw_bytes), algo, stream);
 }
 
 int sffn_dense_forward(const void* X, const void* Wg, const void* Wu, const void* WdT, int64_t M, int64_t K, int64_t N,

@@ -193,3 +193,77 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ in, int6
 }
 
 }  // namespace sffn
+
+namespace sffn {
+
+// Non-gated down projection from TwELL (App.C eq. P:1751-1756, y = h W_d with h = relu(x W_u) stored in
+// TwELL; the paper's Listing 3).  One CTA of 4 warps per row; warp w owns a contiguous K
+// slice of the output (the paper's SPLIT_OUT_DIM idea) and walks every stored entry
+// independently — no cross-warp reduction: y[slice] += h_v * W_d[n, slice] in fp32 FMA.
+template <int NCH>
+__global__ void __launch_bounds__(UD_WARPS * 32)
+    down_kernel(const uint32_t* __restrict__ tw, const uint4* __restrict__ Wd, uint4* __restrict__ Y, int M, int K,
+                int N, int T, int C) {
+    constexpr int EB = 4;
+    const int m = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int K8 = K >> 3;
+    int cidx[NCH];
+    bool cok[NCH];
+    float y[NCH * 8];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+        cidx[j] = warp * 32 * NCH + j * 32 + lane;
+        cok[j] = cidx[j] < K8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[j * 8 + i] = 0.0f;
+    }
+    const int WPT = T / C, cap = WPT - 1, NT = N / T;
+    const uint32_t* trow = tw + static_cast<int64_t>(m) * (N / C);
+#pragma unroll 1
+    for (int t = 0; t < NT; ++t) {
+        const uint32_t* blk = trow + t * WPT;
+        const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+#pragma unroll 1
+        for (int e0 = 0; e0 < cnt; e0 += 32) {
+            const int ne = min(32, cnt - e0);
+            const uint32_t myw = lane < ne ? __ldg(blk + 1 + e0 + lane) : 0u;
+#pragma unroll 1
+            for (int e = 0; e < ne; e += EB) {
+                uint4 q[EB][NCH];
+                float h[EB];
+#pragma unroll
+                for (int i = 0; i < EB; ++i) {
+                    const int ee = min(e + i, ne - 1);
+                    const uint32_t w = __shfl_sync(0xffffffffu, myw, ee);
+                    h[i] = (e + i < ne) ? __uint_as_float(w & 0xFFFF0000u) : 0.0f;
+                    const uint4* wr = Wd + static_cast<int64_t>(w & 0xFFFFu) * K8;
+#pragma unroll
+                    for (int j = 0; j < NCH; ++j) q[i][j] = cok[j] ? ldg_nc(wr + cidx[j]) : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int i = 0; i < EB; ++i)
+#pragma unroll
+                    for (int j = 0; j < NCH; ++j) {
+                        float w[8];
+                        bf16x8_to_f32(q[i][j], w);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) y[j * 8 + k] = fmaf(h[i], w[k], y[j * 8 + k]);
+                    }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+        if (cok[j]) {
+            uint4 o;
+            o.x = pack_bf16x2(y[j * 8 + 0], y[j * 8 + 1]);
+            o.y = pack_bf16x2(y[j * 8 + 2], y[j * 8 + 3]);
+            o.z = pack_bf16x2(y[j * 8 + 4], y[j * 8 + 5]);
+            o.w = pack_bf16x2(y[j * 8 + 6], y[j * 8 + 7]);
+            Y[static_cast<int64_t>(m) * K8 + cidx[j]] = o;
+        }
+    }
+}
+
+}  // namespace sffn

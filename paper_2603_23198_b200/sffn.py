@@ -49,6 +49,8 @@ _SIGS = {
     "sffn_allreduce_bf16": (_int, [_vp, _vp, _i64, _vp]),
     "sffn_f32_twell_bytes": (_sz, [_i64, _i64, _int, _int]),
     "sffn_union_stats": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "sffn_down": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _int, _vp]),
+    "sffn_forward_nongated": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _int, _vp]),
     "sffn_forward_host_stage_bytes": (_sz, [_i64, _i64]),
     "sffn_forward_host": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _sz, _vp, _int,
                                  _i64, _vp]),
@@ -205,6 +207,34 @@ def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspa
                                  workspace.numel() * workspace.element_size(), _p(stage),
                                  stage.numel() * stage.element_size(), _p(overflow), a, chunk_rows,
                                  _stream(stream)), "sffn_forward_host")
+    return out
+
+
+def down(tw, wd, K: int, T: int = 256, C: int = 8, out=None, workspace=None, algo="auto", stream=None):
+    """Non-gated down projection from a TwELL of h = relu(x W_u) (App.C)."""
+    M = tw.shape[0]
+    N = wd.shape[0]
+    a = _algo(algo)
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=wd.device)
+    workspace = _ws(up_down_workspace_bytes(M, K, N, T, C, a), wd.device, workspace)
+    _chk(lib().sffn_down(_p(tw), _bf16(wd, "wd"), M, K, N, T, C, _bf16(out, "out"), _p(workspace),
+                         workspace.numel() * workspace.element_size(), a, _stream(stream)), "sffn_down")
+    return out
+
+
+def forward_nongated(x, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, overflow=None, algo="auto",
+                     stream=None):
+    """Non-gated sparse FFN y = relu(x W_u) W_d (App.C)."""
+    M, K = x.shape
+    N = wu.shape[0]
+    a = _algo(algo)
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+    workspace = _ws(workspace_bytes(M, K, N, T, C, a), x.device, workspace)
+    _chk(lib().sffn_forward_nongated(_bf16(x, "x"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
+                                     _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(),
+                                     _p(overflow), a, _stream(stream)), "sffn_forward_nongated")
     return out
 
 

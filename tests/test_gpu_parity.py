@@ -353,3 +353,32 @@ def test_forward_host_pipeline(sffn, algo):
     yh = sffn.forward_host(xh, to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo, chunk_rows=2048)
     torch.cuda.synchronize()
     assert torch.equal(yh.view(torch.int16), ref.cpu().view(torch.int16))
+
+
+# ----------------------------------------------------------------- non-gated variant (App.C, NEXT-2)
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("name,M", [("tiny", None), ("1B", 300), ("7B", 128)])
+def test_nongated_forward(sffn, name, M, algo):
+    """y = relu(x W_u) W_d: the TwELL comes from the up projection (same tcgen05 pack kernel), then the
+    down-only kernel; Y within 1e-2 of the dense non-gated oracle and of the stored-value TwELL sum."""
+    cfg = synth.CONFIGS[name]
+    if M is not None:
+        cfg = cfg.replace(M=M)
+    X = synth.gen_x(cfg)
+    Wu, Wd = synth.gen_w(cfg, "g"), synth.gen_w(cfg, "d")  # sparse relu(x W_u) with the gate statistics
+    Y = sffn.forward_nongated(to_dev(X), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo)
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wu, cfg.T, cfg.C)
+    y = bf16_np(Y)
+    assert rel_fro(y, oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C)) < Y_TOL
+    assert rel_fro(y, oracle.ffn_nongated_dense(X, Wu, Wd)) < Y_TOL
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_down_from_oracle_twell(sffn, algo):
+    cfg = synth.CONFIGS["1B"].replace(M=333, K=1024, N=2048, Kb=32, sparsity=0.97)
+    X = synth.gen_x(cfg)
+    Wu, Wd = synth.gen_w(cfg, "g"), synth.gen_w(cfg, "d")
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wu, cfg.T, cfg.C)
+    tw = torch.from_numpy(words.view(np.int32)).cuda()
+    Y = sffn.down(tw, to_dev(Wd), cfg.K, cfg.T, cfg.C, algo=algo)
+    assert rel_fro(bf16_np(Y), oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C)) < Y_TOL

@@ -417,3 +417,26 @@ def test_fp32_eq3_equals_eq1_and_perm():
     for n in range(Xf.shape[1]):
         exp[:, p3[n]] = np.maximum(Xf[:, p1[n]], 0) * Xf[:, p2[n]]
     assert np.array_equal(Y, exp)
+
+
+# ---------------------------------------------------------------- non-gated variant (App.C)
+def test_nongated_permutation_and_identity():
+    """y = relu(x W_u) W_d (P:1751-1756): with permutation matrices y[p3(n)] = relu(x[p1(n)]) (closed form);
+    the TwELL down projection with the exact pre-activation equals the dense form; with the stored bf16
+    value it is within the bf16 rounding of h."""
+    Xf, p1, p2, p3, Wg, Wu, Wd = _perm_ffn_case(seed=11)
+    Y = oracle.ffn_nongated_dense(synth_bits(Xf), Wg, Wd)
+    exp = np.zeros_like(Y)
+    for n in range(Xf.shape[1]):
+        exp[:, p3[n]] = np.maximum(Xf[:, p1[n]], 0)
+    assert np.array_equal(Y, exp)
+    cfg = synth.CONFIGS["tiny"]
+    X = synth.gen_x(cfg)
+    Wu, Wd = synth.gen_w(cfg, "g"), synth.gen_w(cfg, "d")  # W_g's statistics give a sparse relu(x W_u)
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wu, cfg.T, cfg.C)
+    assert ov == 0
+    Yd = oracle.ffn_nongated_dense(X, Wu, Wd)
+    Ye = oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C, A=A)
+    assert np.max(np.abs(Yd - Ye)) <= 1e-12 * np.max(np.abs(Yd))
+    Yb = oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C)
+    assert np.linalg.norm(Yb - Yd) / np.linalg.norm(Yd) < 2.0 ** -8
