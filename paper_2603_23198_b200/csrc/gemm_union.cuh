@@ -97,12 +97,16 @@ constexpr int UG_STAGES = 4;
 #ifndef FENCE_CPASYNC
 #define FENCE_CPASYNC 1
 #endif
-constexpr int UG_THREADS = 384;   // warps 0-7 as gemm_tc + warps 8-11: gather producers
-constexpr int UG_GATHER = 128;
+#ifndef UG_NGW
+#define UG_NGW 8
+#endif
+constexpr int UG_GW = UG_NGW;                  // gather producer warps (8..8+UG_GW-1)
+constexpr int UG_THREADS = 256 + 32 * UG_GW;   // warps 0-7 as gemm_tc + gather producer warps
+constexpr int UG_GATHER = 32 * UG_GW;
 constexpr int UG_EWB = 8192;  // epilogue staging per warp
 constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 1024;
 constexpr int UG_RING = 8;       // tile-scheduler ring depth
-constexpr int UG_READERS = 9;    // 4 gather warps + MMA thread + 4 epilogue warps
+constexpr int UG_READERS = UG_GW + 5;  // gather warps + MMA thread + 4 epilogue warps
 
 template <bool UP>
 __global__ void __launch_bounds__(UG_THREADS, 1)
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         // ------------------------------------------------------------ B operand: gathered weight rows
         // 8 consecutive lanes copy one 128-B row segment (16 B each), so every warp instruction moves whole
         // 128-B lines: UP 4 rows x 128 B, DOWN one neuron row's 4 adjacent 64-column atoms (512 B).
-        const int gw = warp - 8;          // 0..3
+        const int gw = warp - 8;          // 0..UG_GW-1
         const int c8 = lane & 7, sub = lane >> 3;
         int stage = 0;
         uint32_t phase = 0;
@@ -239,19 +243,20 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             tile_info(tile, b, cj, len);
             const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
             if (UP) {
-                // pass i covers chunk rows 16 i + 4 gw + sub
-                int nidx[16];
+                // pass i covers chunk rows 4 UG_GW i + 4 gw + sub
+                constexpr int NP = 64 / UG_GW;
+                int nidx[NP];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int r = 16 * i + 4 * gw + sub;
+                for (int i = 0; i < NP; ++i) {
+                    const int r = 4 * UG_GW * i + 4 * gw + sub;
                     nidx[i] = r < len ? __ldg(ul + 256 * cj + r) : -1;
                 }
                 for (int kb = 0; kb < nk_up; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = 16 * i + 4 * gw + sub;
+                    for (int i = 0; i < NP; ++i) {
+                        const int r = 4 * UG_GW * i + 4 * gw + sub;
                         if (nidx[i] >= 0)
                             cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
                                        args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * GEMM_BK + 8 * c8, 16);
@@ -263,29 +268,30 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     }
                 }
             } else {
-                // pass i covers k-block row r = 4 i + gw, MN atom a = sub (columns 256 cj + 64 a + 8 c8)
+                // pass i covers k-block row r = UG_GW i + gw, MN atom a = sub (columns 256 cj + 64 a + 8 c8)
+                constexpr int NP = 64 / UG_GW;
                 const int nk = len / GEMM_BK;
                 const int col = cj * 256 + sub * 64 + 8 * c8;
                 const bool in = col < args.K;
-                int nidx[16];
+                int nidx[NP];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) nidx[i] = __ldg(ul + 4 * i + gw);
+                for (int i = 0; i < NP; ++i) nidx[i] = __ldg(ul + UG_GW * i + gw);
                 for (int kb = 0; kb < nk; ++kb) {
-                    int nxt[16];
+                    int nxt[NP];
                     const int kn = kb + 1 < nk ? kb + 1 : kb;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + 4 * i + gw);
+                    for (int i = 0; i < NP; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + UG_GW * i + gw);
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES) + sub * 8192;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = 4 * i + gw;
+                    for (int i = 0; i < NP; ++i) {
+                        const int r = UG_GW * i + gw;
                         cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
                                    args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + (in ? col : 0), in ? 16 : 0);
                     }
                     cp_async_arrive_noinc(&full[stage]);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) nidx[i] = nxt[i];
+                    for (int i = 0; i < NP; ++i) nidx[i] = nxt[i];
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
