@@ -10,7 +10,7 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a); parity tests through the C ABI")
-    config.addinivalue_line("markers", "slow: long-running")
+    config.addinivalue_line("markers", "slow: long-running (full BASELINE sizes)")
 
 
 @pytest.fixture(scope="session", autouse=True)

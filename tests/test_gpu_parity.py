@@ -382,3 +382,58 @@ def test_down_from_oracle_twell(sffn, algo):
     tw = torch.from_numpy(words.view(np.int32)).cuda()
     Y = sffn.down(tw, to_dev(Wd), cfg.K, cfg.T, cfg.C, algo=algo)
     assert rel_fro(bf16_np(Y), oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C)) < Y_TOL
+
+
+# ----------------------------------------------------------------- full-size parity (bench launch configuration)
+def _sample_rows(M, n_random=48, seed=0):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([np.arange(16), np.arange(M - 16, M), rng.choice(M, n_random, replace=False)]))
+
+
+@pytest.mark.slow
+def test_7b_full_size_sampled(sffn):
+    """BASELINE configs[2] at full size (M=32768, K=4096, N=14336), the default (union) algorithm exactly as
+    bench.py launches it: TwELL bit-exact and Y within 1e-2 on sampled rows (first/last 16 + 48 random),
+    structural TwELL invariants on all rows, zero overflow."""
+    cfg = synth.CONFIGS["7B"]
+    p = synth.token_targets(cfg)
+    X = synth.gen_x(cfg, p=p)
+    Wg, Wu, Wd = (synth.gen_w(cfg, w) for w in "gud")
+    ws = torch.empty(sffn.workspace_bytes(cfg.M, cfg.K, cfg.N, cfg.T, cfg.C), dtype=torch.uint8, device="cuda")
+    ov = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, workspace=ws, overflow=ov)
+    assert sffn.overflow_check(ov) == 0
+    tw = words_np(sffn.twell_view(ws, cfg.M, cfg.N, cfg.C))
+    twell_invariants(tw, cfg.N, cfg.T, cfg.C)
+    rows = _sample_rows(cfg.M)
+    wo, counts, n_ov, A = oracle.pack_from_inputs(X[rows], Wg, cfg.T, cfg.C)
+    assert oracle.valid_prefix_equal(tw[rows], wo, cfg.T, cfg.C).all()
+    Yref = oracle.ffn_twell(X[rows], wo, Wu, Wd, cfg.N, cfg.T, cfg.C)
+    assert rel_fro(bf16_np(Y)[rows], Yref) < Y_TOL
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_70b_shapes(sffn, algo):
+    """BASELINE configs[4] shapes (K=8192, N=28672 = one GPU's full hidden dim; N=3584 = an 8-way shard) at
+    a reduced M."""
+    for N in (28672, 3584):
+        cfg = synth.CONFIGS["70B"].replace(M=256, N=N)
+        X, Wg, Wu, Wd = inputs(cfg)
+        Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo)
+        rows = np.arange(0, 256, 8)
+        wo, counts, n_ov, A = oracle.pack_from_inputs(X[rows], Wg, cfg.T, cfg.C)
+        assert rel_fro(bf16_np(Y)[rows], oracle.ffn_twell(X[rows], wo, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_forward_with_overflow(sffn, algo):
+    """Overflowed tiles through the whole forward: only the stored (first T/C-1) entries contribute, for both
+    algorithms (reading R5; oracle identical)."""
+    cfg = synth.CONFIGS["1B"].replace(M=256, K=256, N=1024, Kb=16, sparsity=0.80, C=16, pmax_ratio=1.2)
+    X, Wg, Wu, Wd = inputs(cfg)
+    ov = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, overflow=ov, algo=algo)
+    n_ov = sffn.overflow_check(ov)
+    wo, counts, n_ov_ref, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    assert n_ov == n_ov_ref > 0
+    assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
