@@ -287,7 +287,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
             attr = cudaFuncSetAttribute(union_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UG_SMEM);
     });
     if (attr != cudaSuccess) return SFFN_ERR_CUDA;
-    const int sms = dev_info().sms;
+    const int sms = env_int("SFFN_UNION_GRID", dev_info().sms);  // tuning override (default: all SMs)
     if (gated) {
         // UP: the number of (block, chunk) tiles is only known on the device; persistent grid.  For the
         // non-gated variant H_c already holds h = relu(x W_u) (the scattered TwELL values): no UP GEMM.
