@@ -122,6 +122,20 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
                  int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo,
                  void* stream);
 
+/* ---------------------------------------------------------------- overflow-exact (hybrid) forward
+ * the paper's hybrid idea (rows routed to the compact sparse form or to a dense backup,
+ * P:177-182; backup rows sized e.g. M/8) applied to inference.  After sffn_forward, every row
+ * whose TwELL has an overflowed tile (count > T/C-1) is recomputed with the dense tcgen05 FFN (Eq.1 over all
+ * hidden units: exact) and written over the sparse result, so Y is exact for any sparsity tail.  At most
+ * `backup_rows` rows are recomputed; *d_backup_count (device int, optional) receives the number of rows that
+ * needed it (if it exceeds backup_rows the remaining rows keep the stored-entries result, reading R5).
+ * Requires N % 128 == 0.  Weights as sffn_forward (W_d [N, K] is read MN-major by TMA: no transpose).
+ * workspace >= sffn_hybrid_workspace_bytes(...) (= forward workspace + backup buffers). */
+size_t sffn_hybrid_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo, int64_t backup_rows);
+int sffn_forward_hybrid(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
+                        int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes, int64_t backup_rows,
+                        int* d_backup_count, uint32_t* d_overflow, int algo, void* stream);
+
 /* ---------------------------------------------------------------- non-gated variant (App.C, NEXT-2)
  * h = relu(x W_u), y = h W_d: the TwELL now comes from the UP projection (the same
  * tcgen05 pack kernel applied to W_u), and only the down projection remains (Listing 3,

@@ -31,11 +31,14 @@ constexpr int GEMM_THREADS = 256;
 constexpr int GEMM_SMEM_LIMIT = 232448;  // max dynamic shared memory per block (227 KB)
 constexpr int GEMM_GROUP_M = 16;         // tile raster: 16 M-tiles sweep all N-tiles together (L2 reuse)
 
-enum { EPI_TWELL = 0, EPI_F32 = 1, EPI_GLU = 2, EPI_BF16 = 3 };
+enum { EPI_TWELL = 0, EPI_F32 = 1, EPI_GLU = 2, EPI_BF16 = 3, EPI_BF16_MN = 4 };
+// EPI_BF16_MN: as EPI_BF16, but B is given MN-major, i.e. as the [Kred, Nout] row-major matrix itself (W_d of
+// the down projection, reduction over its rows): four 64-column x 64-row TMA boxes per k-block land as the
+// 128B-swizzled MN-major UMMA layout (LBO 8 KB between 64-column atoms, SBO 1 KB between 8-row groups).
 
 template <int EPI, int C>
 __host__ __device__ constexpr int gemm_epi_warp_bytes() {
-    return EPI == EPI_TWELL ? 32 * (GEMM_BN / C) * 4 : (EPI == EPI_F32 ? 0 : 32 * 128 * 2);
+    return EPI == EPI_TWELL ? 32 * (GEMM_BN / C) * 4 : (EPI == EPI_F32 ? 0 : 32 * 128 * 2);  // GLU/BF16/BF16_MN
 }
 template <int EPI, int C>
 __host__ __device__ constexpr int gemm_stages() {
@@ -57,7 +60,19 @@ struct GemmArgs {
     uint32_t* overflow;  // EPI_TWELL, may be null
     float* out_f32;      // EPI_F32
     int64_t ld_out;      // EPI_F32 row stride (elements)
+    const int* m_dev;    // optional device row count: rows >= min(M, *m_dev) are skipped (dense backup rows)
 };
+
+// MN-major 128B-swizzled operand: 64-column atoms 8 KB apart (LBO), 8-row groups 1 KB apart (SBO)
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn_tc(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>(8192 >> 4) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
 
 __device__ __forceinline__ void gemm_tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
     const int group = tile / (GEMM_GROUP_M * num_n);
@@ -90,7 +105,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int num_tiles = args.num_m * args.num_n;
+    const int num_m = args.m_dev ? (min(args.M, __ldg(args.m_dev)) + GEMM_BM - 1) / GEMM_BM : args.num_m;
+    const int num_tiles = num_m * args.num_n;
     const int nk = (args.K + GEMM_BK - 1) / GEMM_BK;
 
     if (threadIdx.x == 0) {
@@ -122,7 +138,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 int mb, nb;
-                gemm_tile_coords(tile, args.num_m, args.num_n, mb, nb);
+                gemm_tile_coords(tile, num_m, args.num_n, mb, nb);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], GEMM_STAGE_BYTES);
@@ -131,6 +147,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         tma_load_2d(stB + stage * GEMM_B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * 128, pol);
                         tma_load_2d(stB + stage * GEMM_B_BYTES + GEMM_B_BYTES / 2, &tmB2, &full[stage], kb * GEMM_BK,
                                     nb * 128, pol);
+                    } else if (EPI == EPI_BF16_MN) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            tma_load_2d(stB + stage * GEMM_B_BYTES + q * 8192, &tmB, &full[stage], nb * GEMM_BN + 64 * q,
+                                        kb * GEMM_BK, pol);
                     } else {
                         tma_load_2d(stB + stage * GEMM_B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN, pol);
                     }
@@ -144,7 +165,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
-            constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, GEMM_BN);
+            constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, GEMM_BN) | (EPI == EPI_BF16_MN ? (1u << 16) : 0u);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -160,8 +181,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);
 #pragma unroll
                     for (int k = 0; k < GEMM_BK / 16; ++k)
-                        umma_f16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
-                                 (kb | k) != 0);
+                        umma_f16(d, umma_desc_sw128(a0 + k * 32),
+                                 EPI == EPI_BF16_MN ? umma_desc_sw128_mn_tc(b0 + k * 2048) : umma_desc_sw128(b0 + k * 32),
+                                 IDESC, (kb | k) != 0);
                     umma_commit(&empty[stage]);
                     if (++stage == S) {
                         stage = 0;
@@ -183,7 +205,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             int mb, nb;
-            gemm_tile_coords(tile, args.num_m, args.num_n, mb, nb);
+            gemm_tile_coords(tile, num_m, args.num_n, mb, nb);
             const int row0 = mb * GEMM_BM + ew * 32;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -277,7 +299,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     tma_store_2d(&tmOut, stg, nb * 128, row0);
                     bulk_commit();
                 }
-            } else {  // EPI_BF16
+            } else {  // EPI_BF16, EPI_BF16_MN
                 uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
 #pragma unroll 1
                 for (int half = 0; half < 2; ++half) {

@@ -13,6 +13,7 @@
 #include "gemm_tc.cuh"
 #include "fp32_path.cuh"
 #include "gemm_union.cuh"
+#include "hybrid.cuh"
 #include "updown.cuh"
 
 using namespace sffn;
@@ -671,6 +672,85 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     }
     for (auto& e : ev) cudaEventDestroy(e);  // destruction is deferred until the events complete
     return r;
+}
+
+// ---------------------------------------------------------------- overflow-exact (hybrid) forward
+namespace {
+struct HybWs {
+    int64_t fwd, cnt, list, xo, ho, yo, total;
+};
+HybWs hyb_layout(int64_t M, int64_t K, int64_t N, int T, int C, int algo, int64_t R) {
+    HybWs w{};
+    w.fwd = 0;
+    int64_t o = align1k(static_cast<int64_t>(sffn_forward_workspace_bytes(M, K, N, T, C, algo)));
+    w.cnt = o;  o = align1k(o + 16);
+    w.list = o; o = align1k(o + R * 4);
+    w.xo = o;   o = align1k(o + R * K * 2);
+    w.ho = o;   o = align1k(o + R * N * 2);
+    w.yo = o;   o = align1k(o + R * K * 2);
+    w.total = o;
+    return w;
+}
+}  // namespace
+
+size_t sffn_hybrid_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo, int64_t backup_rows) {
+    if (M < 0 || K <= 0 || N <= 0 || backup_rows < 0) return 0;
+    const int64_t R = ((backup_rows + 127) / 128) * 128;
+    return static_cast<size_t>(hyb_layout(M, K, N, T, C, algo, R).total);
+}
+
+int sffn_forward_hybrid(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                        int T, int C, void* Y, void* workspace, size_t ws_bytes, int64_t backup_rows,
+                        int* d_backup_count, uint32_t* d_overflow, int algo, void* stream) {
+    if (backup_rows < 0) return SFFN_ERR_INVALID_ARG;
+    if (N % 128 != 0) return SFFN_ERR_SHAPE;  // dense backup GEMM tiles
+    const int64_t R = ((backup_rows + 127) / 128) * 128;
+    if (ws_bytes < sffn_hybrid_workspace_bytes(M, K, N, T, C, algo, backup_rows)) return SFFN_ERR_SHAPE;
+    HybWs L = hyb_layout(M, K, N, T, C, algo, R);
+    uint8_t* b = static_cast<uint8_t*>(workspace);
+    int r = sffn_forward(X, Wg, Wu, Wd, M, K, N, T, C, Y, b, static_cast<size_t>(L.cnt), d_overflow, algo, stream);
+    if (r != SFFN_OK || M == 0) return r;
+    cudaStream_t st = S(stream);
+    int* cnt = reinterpret_cast<int*>(b + L.cnt);
+    int32_t* list = reinterpret_cast<int32_t*>(b + L.list);
+    if (cudaMemsetAsync(cnt, 0, 4, st) != cudaSuccess) return SFFN_ERR_CUDA;
+    ov_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint32_t*>(workspace), (int)M, (int)N, T, C, cnt, list, (int)R);
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    if (d_backup_count && cudaMemcpyAsync(d_backup_count, cnt, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return SFFN_ERR_CUDA;
+    if (R == 0) return SFFN_OK;
+    void* xo = b + L.xo;
+    void* ho = b + L.ho;
+    void* yo = b + L.yo;
+    const unsigned g = static_cast<unsigned>((R * 32 + 255) / 256);
+    move_rows_kernel<true><<<g, 256, 0, st>>>(static_cast<const uint4*>(X), static_cast<uint4*>(xo), list, cnt, (int)R,
+                                              (int)(K / 8));
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    CUtensorMap tx, tg, tu, th_out, th_in, twd, ty;
+    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xo, K, R, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&th_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ho, N, R, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !tmap_2d(&th_in, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ho, N, R, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wd, K, N, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, yo, K, R, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return SFFN_ERR_CUDA;
+    GemmArgs a1{};
+    a1.M = (int)R;
+    a1.N = (int)N;
+    a1.K = (int)K;
+    a1.m_dev = cnt;
+    if ((r = launch_gemm<EPI_GLU, 1>(tx, tg, tu, th_out, a1, 128, st)) != SFFN_OK) return r;
+    GemmArgs a2{};
+    a2.M = (int)R;
+    a2.N = (int)K;
+    a2.K = (int)N;
+    a2.m_dev = cnt;
+    if ((r = launch_gemm<EPI_BF16_MN, 1>(th_in, twd, twd, ty, a2, GEMM_BN, st)) != SFFN_OK) return r;
+    move_rows_kernel<false><<<g, 256, 0, st>>>(static_cast<const uint4*>(yo), static_cast<uint4*>(Y), list, cnt,
+                                               (int)R, (int)(K / 8));
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
 int sffn_union_stats(const void* workspace, int64_t M, int64_t K, int64_t N, int64_t* padded_sum, int64_t* real_sum,

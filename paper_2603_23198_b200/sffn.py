@@ -49,6 +49,9 @@ _SIGS = {
     "sffn_allreduce_bf16": (_int, [_vp, _vp, _i64, _vp]),
     "sffn_f32_twell_bytes": (_sz, [_i64, _i64, _int, _int]),
     "sffn_union_stats": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "sffn_hybrid_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int, _int, _i64]),
+    "sffn_forward_hybrid": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _i64, _vp, _vp,
+                                   _int, _vp]),
     "sffn_down": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _int, _vp]),
     "sffn_forward_nongated": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _int, _vp]),
     "sffn_forward_host_stage_bytes": (_sz, [_i64, _i64]),
@@ -207,6 +210,22 @@ def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspa
                                  workspace.numel() * workspace.element_size(), _p(stage),
                                  stage.numel() * stage.element_size(), _p(overflow), a, chunk_rows,
                                  _stream(stream)), "sffn_forward_host")
+    return out
+
+
+def forward_hybrid(x, wg, wu, wd, T: int = 256, C: int = 8, backup_rows: int | None = None, out=None,
+                   workspace=None, backup_count=None, overflow=None, algo="auto", stream=None):
+    """Overflow-exact sparse forward: rows with an overflowed TwELL tile are recomputed densely (NEXT-1)."""
+    M, K = x.shape
+    N = wg.shape[0]
+    a = _algo(algo)
+    R = max(128, M // 8) if backup_rows is None else backup_rows
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+    workspace = _ws(int(lib().sffn_hybrid_workspace_bytes(M, K, N, T, C, a, R)), x.device, workspace)
+    _chk(lib().sffn_forward_hybrid(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
+                                   _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(), R,
+                                   _p(backup_count), _p(overflow), a, _stream(stream)), "sffn_forward_hybrid")
     return out
 
 

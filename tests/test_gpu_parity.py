@@ -437,3 +437,38 @@ def test_forward_with_overflow(sffn, algo):
     wo, counts, n_ov_ref, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
     assert n_ov == n_ov_ref > 0
     assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
+
+
+# ----------------------------------------------------------------- overflow-exact (hybrid) forward, NEXT-1
+@pytest.mark.parametrize("algo", ALGOS)
+def test_forward_hybrid_exact_on_overflow(sffn, algo):
+    """Rows with an overflowed tile are recomputed densely: they match Eq.1 (all positives), the other rows
+    match Eq.3 over the stored entries; the backup count equals the oracle's number of overflowing rows."""
+    cfg = synth.CONFIGS["1B"].replace(M=700, K=256, N=1024, Kb=16, sparsity=0.96, C=16, pmax_ratio=3.0)
+    X, Wg, Wu, Wd = inputs(cfg)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Y = sffn.forward_hybrid(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, backup_rows=512,
+                            backup_count=cnt, algo=algo)
+    torch.cuda.synchronize()
+    wo, counts, n_ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    ov_rows = np.flatnonzero((counts > cfg.T // cfg.C - 1).any(1))
+    ok_rows = np.setdiff1d(np.arange(cfg.M), ov_rows)
+    assert 0 < len(ov_rows) <= 512 and int(cnt.item()) == len(ov_rows)
+    y = bf16_np(Y)
+    Y1 = oracle.ffn_dense(X[ov_rows], Wg, Wu, Wd)
+    assert rel_fro(y[ov_rows], Y1) < Y_TOL
+    Y3 = oracle.ffn_twell(X[ok_rows], wo[ok_rows], Wu, Wd, cfg.N, cfg.T, cfg.C)
+    assert rel_fro(y[ok_rows], Y3) < Y_TOL
+    # without the backup the overflowed rows are truncated (and measurably off Eq.1)
+    Yt = bf16_np(sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo))
+    assert rel_fro(Yt[ov_rows], Y1) > 10 * rel_fro(y[ov_rows], Y1)
+
+
+def test_forward_hybrid_no_overflow_is_plain_forward(sffn):
+    cfg = synth.CONFIGS["1B"].replace(M=300, K=256, N=1024, Kb=16, sparsity=0.99)
+    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    cnt = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    Y = sffn.forward_hybrid(X, Wg, Wu, Wd, 256, 8, backup_count=cnt)
+    ref = sffn.forward(X, Wg, Wu, Wd, 256, 8)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0 and torch.equal(Y.view(torch.int16), ref.view(torch.int16))
