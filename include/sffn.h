@@ -136,6 +136,19 @@ int sffn_forward_hybrid(const void* X, const void* Wg, const void* Wu, const voi
                         int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes, int64_t backup_rows,
                         int* d_backup_count, uint32_t* d_overflow, int algo, void* stream);
 
+/* ---------------------------------------------------------------- training entry: TwELL -> hybrid (NEXT-4)
+ * Listing 4 on the packed TwELL, hybrid format P:177-182: per row, the stored entries in
+ * ascending column order compacted into an ELL row of width ell_w (ell_val bf16 [M, ell_w], ell_col int16
+ * [M, ell_w], slots past min(nnz, ell_w) untouched); row_nnz[m] = stored count (true occupancy, may exceed
+ * ell_w).  Rows with row_nnz > ell_w go to the dense tail: slot s < dense_cap (atomic order), dense_rows[s, :]
+ * = the densified row (bf16 [dense_cap, N]), dense_map[s] = m, row_loc[m] = s; row_loc[m] = -1 for ELL rows
+ * and -2 when the tail is full (the paper's "discard the excess and set a flag").  *d_dense_count
+ * (device int, zeroed by the caller) = rows that needed the tail.  d_l0l1 (device double[2], optional,
+ * accumulated): += sum_m nnz_m / M and sum_m sum(values_m) / M (Listing 4's L0 / L1 statistics). */
+int sffn_twell_to_hybrid(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int ell_w, void* ell_val,
+                         int16_t* ell_col, int32_t* row_nnz, int32_t* row_loc, int64_t dense_cap, void* dense_rows,
+                         int32_t* dense_map, int* d_dense_count, double* d_l0l1, void* stream);
+
 /* ---------------------------------------------------------------- non-gated variant (App.C, NEXT-2)
  * h = relu(x W_u), y = h W_d: the TwELL now comes from the UP projection (the same
  * tcgen05 pack kernel applied to W_u), and only the down projection remains (Listing 3,

@@ -49,6 +49,7 @@ def _load():
         lib.oracle_ffn_nongated_dense.argtypes = [vp, vp, vp, i64, i64, i64, vp]
         lib.oracle_down_twell.argtypes = [vp, vp, i64, i64, i64, ci, ci, ci, vp, vp]
         lib.oracle_pack_soa.argtypes = [vp, i64, i64, ci, ci, vp, vp, vp]
+        lib.oracle_twell_to_ell.argtypes = [vp, i64, i64, ci, ci, i64, vp, vp, vp, vp]
         lib.oracle_pack_soa.restype = i64
         lib.oracle_ffn_dense_f32.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp]
         lib.oracle_ffn_soa_f32.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, ci, ci, vp]
@@ -235,3 +236,17 @@ def down_twell(words, Wd, K: int, N: int, T: int, C: int, A=None) -> np.ndarray:
         mode, Ap = 1, A.ctypes.data
     _load().oracle_down_twell(words.ctypes.data, Wd.ctypes.data, M, K, N, T, C, mode, Ap, Y.ctypes.data)
     return Y
+
+
+# ---------------------------------------------------------------- training entry: TwELL -> hybrid (NEXT-4)
+def twell_to_ell(words, N: int, T: int, C: int, ell_w: int):
+    """(ell_val uint16 [M, ell_w] (0 past nnz), ell_col int16 [M, ell_w] (-1 past nnz), row_nnz, (l0, l1))."""
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    M = words.shape[0]
+    val = np.zeros((M, ell_w), dtype=np.uint16)
+    col = np.full((M, ell_w), -1, dtype=np.int16)
+    nnz = np.zeros(M, dtype=np.int32)
+    l = np.zeros(2, dtype=np.float64)
+    _load().oracle_twell_to_ell(words.ctypes.data, M, N, T, C, ell_w, val.ctypes.data, col.ctypes.data,
+                                nnz.ctypes.data, l.ctypes.data)
+    return val, col, nnz, (float(l[0]), float(l[1]))

@@ -295,3 +295,36 @@ void oracle_down_twell(const uint32_t* words, const uint16_t* Wd, int64_t M, int
         }
     }
 }
+
+/*
+ * TwELL -> ELL part of the hybrid format with L0/L1 statistics (Listing 4; hybrid P:177-182):
+ * row m's stored entries in tile order (ascending columns) fill ell_col/ell_val[m, 0 .. min(nnz, ell_w));
+ * row_nnz[m] = stored count; l0l1[0] = sum_m nnz_m / M, l1l1[1] = sum_m sum(values_m) / M (fp64).
+ */
+void oracle_twell_to_ell(const uint32_t* words, int64_t M, int64_t N, int T, int C, int64_t ell_w,
+                         uint16_t* ell_val, int16_t* ell_col, int32_t* row_nnz, double* l0l1) {
+    const int64_t NT = N / T, W = T / C, cap = W - 1;
+    double l0 = 0.0, l1 = 0.0;
+    for (int64_t m = 0; m < M; ++m) {
+        int64_t k = 0;
+        double vs = 0.0;
+        for (int64_t t = 0; t < NT; ++t) {
+            const uint32_t* blk = words + m * (N / C) + t * W;
+            int64_t z = blk[0];
+            if (z > cap) z = cap;
+            for (int64_t c = 0; c < z; ++c, ++k) {
+                uint32_t w = blk[1 + c];
+                vs += oracle_bf16_to_double((uint16_t)(w >> 16));
+                if (k < ell_w) {
+                    ell_val[m * ell_w + k] = (uint16_t)(w >> 16);
+                    ell_col[m * ell_w + k] = (int16_t)(w & 0xFFFFu);
+                }
+            }
+        }
+        row_nnz[m] = (int32_t)k;
+        l0 += (double)k / (double)M;
+        l1 += vs / (double)M;
+    }
+    l0l1[0] = l0;
+    l0l1[1] = l1;
+}

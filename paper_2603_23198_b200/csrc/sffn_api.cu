@@ -753,6 +753,22 @@ int sffn_forward_hybrid(const void* X, const void* Wg, const void* Wu, const voi
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
+int sffn_twell_to_hybrid(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int ell_w, void* ell_val,
+                         int16_t* ell_col, int32_t* row_nnz, int32_t* row_loc, int64_t dense_cap, void* dense_rows,
+                         int32_t* dense_map, int* d_dense_count, double* d_l0l1, void* stream) {
+    if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
+    if (M < 0 || N <= 0 || N % T != 0 || N > 65536 || ell_w < 1 || dense_cap < 0) return SFFN_ERR_SHAPE;
+    if (M == 0) return SFFN_OK;
+    if (!twell || !ell_val || !ell_col || !row_nnz || !row_loc || !d_dense_count) return SFFN_ERR_INVALID_ARG;
+    if (dense_cap > 0 && (!dense_rows || !dense_map)) return SFFN_ERR_INVALID_ARG;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    twell_to_hybrid_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, S(stream)>>>(
+        twell, (int)M, (int)N, T, C, ell_w, static_cast<uint16_t*>(ell_val), ell_col, row_nnz, row_loc,
+        (int)dense_cap, static_cast<uint16_t*>(dense_rows), dense_map, d_dense_count, d_l0l1);
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
 int sffn_union_stats(const void* workspace, int64_t M, int64_t K, int64_t N, int64_t* padded_sum, int64_t* real_sum,
                      int64_t* up_tiles, void* stream) {
     if (!workspace || M <= 0 || N <= 0 || K <= 0) return SFFN_ERR_INVALID_ARG;

@@ -52,6 +52,8 @@ _SIGS = {
     "sffn_hybrid_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int, _int, _i64]),
     "sffn_forward_hybrid": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _i64, _vp, _vp,
                                    _int, _vp]),
+    "sffn_twell_to_hybrid": (_int, [_vp, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
+                                    _vp]),
     "sffn_down": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _int, _vp]),
     "sffn_forward_nongated": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _int, _vp]),
     "sffn_forward_host_stage_bytes": (_sz, [_i64, _i64]),
@@ -226,6 +228,27 @@ def forward_hybrid(x, wg, wu, wd, T: int = 256, C: int = 8, backup_rows: int | N
     _chk(lib().sffn_forward_hybrid(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
                                    _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(), R,
                                    _p(backup_count), _p(overflow), a, _stream(stream)), "sffn_forward_hybrid")
+    return out
+
+
+def twell_to_hybrid(tw, N: int, T: int = 256, C: int = 8, ell_w: int = 128, dense_cap: int | None = None,
+                    stream=None) -> dict:
+    """TwELL -> hybrid (ELL + dense tail + row locations) with L0/L1 statistics (NEXT-4, Listing 4)."""
+    M = tw.shape[0]
+    dev = tw.device
+    D = max(1, M // 8) if dense_cap is None else dense_cap
+    out = {"ell_val": torch.empty((M, ell_w), dtype=torch.bfloat16, device=dev),
+           "ell_col": torch.empty((M, ell_w), dtype=torch.int16, device=dev),
+           "row_nnz": torch.empty(M, dtype=torch.int32, device=dev),
+           "row_loc": torch.empty(M, dtype=torch.int32, device=dev),
+           "dense_rows": torch.empty((max(D, 1), N), dtype=torch.bfloat16, device=dev),
+           "dense_map": torch.empty(max(D, 1), dtype=torch.int32, device=dev),
+           "dense_count": torch.zeros(1, dtype=torch.int32, device=dev),
+           "l0l1": torch.zeros(2, dtype=torch.float64, device=dev)}
+    _chk(lib().sffn_twell_to_hybrid(_p(tw), M, N, T, C, ell_w, _p(out["ell_val"]), _p(out["ell_col"]),
+                                    _p(out["row_nnz"]), _p(out["row_loc"]), D, _p(out["dense_rows"]),
+                                    _p(out["dense_map"]), _p(out["dense_count"]), _p(out["l0l1"]), _stream(stream)),
+         "sffn_twell_to_hybrid")
     return out
 
 

@@ -472,3 +472,34 @@ def test_forward_hybrid_no_overflow_is_plain_forward(sffn):
     ref = sffn.forward(X, Wg, Wu, Wd, 256, 8)
     torch.cuda.synchronize()
     assert int(cnt.item()) == 0 and torch.equal(Y.view(torch.int16), ref.view(torch.int16))
+
+
+# ----------------------------------------------------------------- training entry: TwELL -> hybrid (NEXT-4)
+def test_twell_to_hybrid(sffn):
+    cfg = synth.CONFIGS["1B"].replace(M=900, K=256, N=2048, Kb=16, sparsity=0.97)
+    X, Wg = synth.gen_x(cfg), synth.gen_w(cfg, "g")
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    tw = torch.from_numpy(words.view(np.int32)).cuda()
+    ell_w = 64
+    h = sffn.twell_to_hybrid(tw, cfg.N, cfg.T, cfg.C, ell_w=ell_w, dense_cap=1024)
+    torch.cuda.synchronize()
+    val, col, nnz, (l0, l1) = oracle.twell_to_ell(words, cfg.N, cfg.T, cfg.C, ell_w)
+    g_nnz = h["row_nnz"].cpu().numpy()
+    assert np.array_equal(g_nnz, nnz)
+    g_val = h["ell_val"].cpu().view(torch.int16).numpy().view(np.uint16)
+    g_col = h["ell_col"].cpu().numpy()
+    for m in range(cfg.M):
+        k = min(nnz[m], ell_w)
+        assert np.array_equal(g_col[m, :k], col[m, :k]) and np.array_equal(g_val[m, :k], val[m, :k])
+    loc = h["row_loc"].cpu().numpy()
+    wide = np.flatnonzero(nnz > ell_w)
+    assert len(wide) > 0 and int(h["dense_count"].item()) == len(wide)
+    assert np.array_equal(np.flatnonzero(loc >= 0), wide) and (loc[nnz <= ell_w] == -1).all()
+    dmap = h["dense_map"].cpu().numpy()
+    H = oracle.unpack(words, cfg.N, cfg.T, cfg.C)
+    dense = h["dense_rows"].float().cpu().numpy()
+    for m in wide:
+        s = loc[m]
+        assert dmap[s] == m and np.array_equal(dense[s], H[m])
+    g = h["l0l1"].cpu().numpy()
+    assert abs(g[0] - l0) < 1e-9 * l0 and abs(g[1] - l1) < 1e-5 * abs(l1)

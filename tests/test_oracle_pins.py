@@ -440,3 +440,25 @@ def test_nongated_permutation_and_identity():
     assert np.max(np.abs(Yd - Ye)) <= 1e-12 * np.max(np.abs(Yd))
     Yb = oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C)
     assert np.linalg.norm(Yb - Yd) / np.linalg.norm(Yd) < 2.0 ** -8
+
+
+# ---------------------------------------------------------------- training entry: TwELL -> hybrid (NEXT-4)
+def test_twell_to_ell_pins():
+    """Listing 4 semantics on the oracle: the ELL row is the concatenation of the tiles' stored entries
+    (brute force via the dense matrix's row-wise nonzeros, ascending); row_nnz is the stored count;
+    L0 = mean stored nnz; L1 = mean row sum of the stored values."""
+    cfg = synth.CONFIGS["tiny"]
+    X, Wg = synth.gen_x(cfg), synth.gen_w(cfg, "g")
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    assert ov == 0
+    ell_w = 16
+    val, col, nnz, (l0, l1) = oracle.twell_to_ell(words, cfg.N, cfg.T, cfg.C, ell_w)
+    H = oracle.unpack(words, cfg.N, cfg.T, cfg.C)
+    for m in range(cfg.M):
+        nzc = np.flatnonzero(H[m])
+        assert nnz[m] == len(nzc) == counts[m].sum()
+        k = min(len(nzc), ell_w)
+        assert col[m, :k].tolist() == nzc[:k].tolist()
+        assert np.array_equal(synth.bf16_to_f32(val[m, :k]), H[m, nzc[:k]])
+    assert abs(l0 - counts.sum() / cfg.M) < 1e-12
+    assert abs(l1 - H.astype(np.float64).sum() / cfg.M) < 1e-9 * max(1.0, abs(l1))
