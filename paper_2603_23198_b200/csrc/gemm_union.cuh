@@ -348,7 +348,6 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         uint8_t* stg = epi + ew * UG_EWB;
         int acc = 0;
         uint32_t acc_phase = 0;
-        uint32_t gphase = 0;
         int ridx = 0;
         uint32_t rphase = 0;
         for (;;) {
@@ -361,20 +360,30 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             tc_fence_after();
             const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
             if constexpr (UP) {
-                // staging <- G tile (gate values in union coordinates, pre-scattered into H_c by union_build),
-                // then H = G * (X W_u^T) in place, then TMA store back to the same H_c tile.
+                // staging <- this row's gate values for the chunk (from the compact gate list, zero elsewhere),
+                // then H = G * (X W_u^T) in place, then TMA store of the H_c tile.
                 const int p0 = 256 * cj;
+                const int64_t prow = static_cast<int64_t>(row0) + lane;  // pi-ordered row (H_c row)
+                const uint32_t* gl = args.um.glist + prow * args.um.lmax;
+                const uint16_t* co = args.um.coff + prow * (args.um.nchunk + 1);
+                const int e0 = __ldg(co + cj), e1 = __ldg(co + cj + 1);
 #pragma unroll 1
                 for (int h = 0; h < 2 && 128 * h < len; ++h) {
                     const int nbox = min(2, (len - 128 * h) / 64);
-                    if (lane == 0) {
-                        bulk_wait_read0();  // previous TMA store has finished reading the staging buffer
-                        mbar_arrive_expect_tx(&gbar[ew], nbox * 4096);
-                        for (int q = 0; q < nbox; ++q)
-                            tma_load_2d(stg + q * 4096, &tmOut, &gbar[ew], p0 + 128 * h + 64 * q, row0, policy_evict_first());
+                    if (lane == 0) bulk_wait_read0();  // previous TMA store has finished reading the staging buffer
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+#pragma unroll
+                        for (int c16 = 0; c16 < 8; ++c16)
+                            *reinterpret_cast<uint4*>(stg + q * 4096 + lane * 128 + c16 * 16) = make_uint4(0, 0, 0, 0);
+                    for (int e = e0; e < e1; ++e) {
+                        const uint32_t w = __ldg(gl + e);
+                        const int j = static_cast<int>(w >> 16) - p0 - 128 * h;
+                        if (j >= 0 && j < 128)
+                            *reinterpret_cast<uint16_t*>(stg + (j >> 6) * 4096 + sw128_off(lane, j & 63)) =
+                                static_cast<uint16_t>(w & 0xFFFFu);
                     }
-                    mbar_wait(&gbar[ew], gphase);
-                    gphase ^= 1;
 #pragma unroll 1
                     for (int q32 = 0; q32 < 2 * nbox; ++q32) {
                         uint32_t v[32];

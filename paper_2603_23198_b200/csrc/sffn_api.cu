@@ -180,9 +180,10 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, total;
+    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, glist, coff, total;
+    int lmax, nchunk;
 };
-UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K) {
+UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8) {
     const int64_t NB = (M + 127) / 128;
     UnionWs w{};
     int64_t o = 0;
@@ -198,6 +199,10 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K) {
     w.xp = o;    o = align1k(o + M * K * 2);
     w.ctr = o;   o = align1k(o + 64);
     w.nnz = o;   o = align1k(o + M * 4);
+    w.lmax = static_cast<int>((N / T) * (T / C - 1));  // most stored entries a row can have
+    w.nchunk = static_cast<int>((N + 255) / 256);
+    w.glist = o; o = align1k(o + NB * 128 * static_cast<int64_t>(w.lmax) * 4);
+    w.coff = o;  o = align1k(o + NB * 128 * static_cast<int64_t>(w.nchunk + 1) * 2);
     w.total = o;
     return w;
 }
@@ -209,15 +214,16 @@ int resolve_algo(int algo, int64_t N) {
     return algo;
 }
 
-size_t updown_ws_bytes(int64_t M, int64_t N, int64_t K, int algo) {
+size_t updown_ws_bytes(int64_t M, int64_t N, int64_t K, int algo, int T = 32, int C = 1) {
+    // sized for the worst (T, C) unless given: the gate lists need (N/T)*(T/C-1) entries per row
     if (resolve_algo(algo, N) != SFFN_ALGO_UNION || M <= 0) return 0;
-    return static_cast<size_t>(union_ws_layout(M, N, K).total);
+    return static_cast<size_t>(union_ws_layout(M, N, K, T, C).total);
 }
 
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true) {
     const int64_t NB = (M + 127) / 128;
-    UnionWs L = union_ws_layout(M, N, K);
+    UnionWs L = union_ws_layout(M, N, K, T, C);
     uint8_t* base = static_cast<uint8_t*>(ws);
     UnionMeta um;
     um.ulist = reinterpret_cast<int32_t*>(base + L.ulist);
@@ -228,6 +234,10 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     um.chunk_off = reinterpret_cast<int32_t*>(base + L.chunk);
     um.tiles = reinterpret_cast<int32_t*>(base + L.tiles);
     um.counters = reinterpret_cast<int*>(base + L.ctr);
+    um.glist = reinterpret_cast<uint32_t*>(base + L.glist);
+    um.coff = reinterpret_cast<uint16_t*>(base + L.coff);
+    um.lmax = L.lmax;
+    um.nchunk = L.nchunk;
     void* hc = base + L.hc;
     int32_t* perm = reinterpret_cast<int32_t*>(base + L.perm);
     void* xp = base + L.xp;
@@ -246,8 +256,12 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
     union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um, perm);
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (128 / GS_ROWS)), 256, 0, st>>>(
-        tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm);
+    if (gated)  // compact gate lists consumed by the UP epilogue
+        union_gate_list_kernel<<<static_cast<unsigned>(NB * 128 * 32 / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C,
+                                                                                           um, perm);
+    else  // non-gated: H_c = the scattered TwELL values (no up GEMM)
+        union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (128 / GS_ROWS)), 256, 0, st>>>(
+            tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm);
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     union_scan_kernel<<<1, 1024, 0, st>>>(um, (int)NB, env_int("SFFN_UP_GROUP", UNION_GROUP_UP));
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
@@ -307,7 +321,7 @@ int updown_dispatch(const void* X, const uint32_t* tw, const void* Wu, const voi
     const int a = resolve_algo(algo, N);
     if (a == SFFN_ALGO_UNION) {
         if (!union_applicable(N)) return SFFN_ERR_SHAPE;
-        if (!ws || ws_bytes < updown_ws_bytes(M, N, K, a)) return SFFN_ERR_SHAPE;
+        if (!ws || ws_bytes < updown_ws_bytes(M, N, K, a, T, C)) return SFFN_ERR_SHAPE;
         return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, ws, st);
     }
     if (a != SFFN_ALGO_GATHER) return SFFN_ERR_INVALID_ARG;
@@ -340,16 +354,14 @@ int64_t sffn_twell_words(int64_t M, int64_t N, int T, int C) {
 }
 
 size_t sffn_up_down_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo) {
-    (void)T;
-    (void)C;
-    if (M < 0 || N <= 0 || K <= 0) return 0;
-    return updown_ws_bytes(M, N, K, algo);
+    if (M < 0 || N <= 0 || K <= 0 || !valid_TC(T, C)) return 0;
+    return updown_ws_bytes(M, N, K, algo, T, C);
 }
 
 size_t sffn_forward_workspace_bytes(int64_t M, int64_t K, int64_t N, int T, int C, int algo) {
     int64_t w = sffn_twell_words(M, N, T, C);
     if (w < 0 || K <= 0) return 0;
-    return static_cast<size_t>(align1k(w * 4)) + updown_ws_bytes(M, N, K, algo);
+    return static_cast<size_t>(align1k(w * 4)) + updown_ws_bytes(M, N, K, algo, T, C);
 }
 
 int sffn_pack(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
@@ -385,7 +397,7 @@ int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const voi
     if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
     if (resolve_algo(algo, N) == SFFN_ALGO_UNION && M > 0) {
         if (!union_applicable(N)) return SFFN_ERR_SHAPE;
-        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, K, algo)) return SFFN_ERR_SHAPE;
+        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, K, algo, T, C)) return SFFN_ERR_SHAPE;
     }
     if ((r = check_device()) != SFFN_OK) return r;
     return updown_dispatch(X, twell, Wu, Wd, M, K, N, T, C, Y, workspace, ws_bytes, algo, S(stream));
@@ -416,7 +428,7 @@ int sffn_down(const uint32_t* twell, const void* Wd, int64_t M, int64_t K, int64
     const int a = resolve_algo(algo, N);
     if (a == SFFN_ALGO_UNION && M > 0) {
         if (!union_applicable(N)) return SFFN_ERR_SHAPE;
-        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, K, a)) return SFFN_ERR_SHAPE;
+        if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, K, a, T, C)) return SFFN_ERR_SHAPE;
     }
     if ((r = check_device()) != SFFN_OK) return r;
     if (M == 0) return SFFN_OK;

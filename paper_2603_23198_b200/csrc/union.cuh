@@ -24,6 +24,9 @@ struct UnionMeta {
     int32_t* utot;       // [NB] un-padded union sizes
     int32_t* tiles;      // [NB * ceil(N/256)]: UP work list, (b << 8) | chunk, grouped raster
     int* counters;       // [2] dynamic tile-scheduler counters of the UP and DOWN GEMMs
+    uint32_t* glist;     // [NB*128, lmax] per (pi-ordered) row: (union position << 16) | bf16 gate, ascending
+    uint16_t* coff;      // [NB*128, nchunk + 1] per row: entries before union chunk c (256 positions per chunk)
+    int lmax, nchunk;
 };
 
 constexpr int UNION_GROUP_UP = 8;    // token blocks whose up-GEMM tiles run together (L2 working set)
@@ -174,6 +177,57 @@ __global__ void __launch_bounds__(256) union_gate_scatter_kernel(const uint32_t*
         const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
         hrow[j] = static_cast<uint16_t>(w >> 16);
     });
+}
+
+// Compact gate lists for the UP epilogue (instead of materialising G in H_c): warp per pi-ordered row i;
+// the row's stored entries in ascending neuron order = ascending union position; warp ballot/popc
+// compaction; then coff[i][c] = #entries with position < 256 c (lower bounds, lanes over chunks).
+__global__ void union_gate_list_kernel(const uint32_t* __restrict__ tw, int M, int N, int T, int C, UnionMeta um,
+                                       const int32_t* __restrict__ perm) {
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int NB = (M + 127) / 128;
+    if (i >= static_cast<int64_t>(NB) * 128) return;
+    const int b = static_cast<int>(i >> 7);
+    const int NW = N >> 5, NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
+    const uint32_t* msk = um.umask + static_cast<int64_t>(b) * NW;
+    const int32_t* wof = um.uwoff + static_cast<int64_t>(b) * NW;
+    uint32_t* gl = um.glist + i * um.lmax;
+    int base = 0;
+    if (i < M) {
+        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + i)) * RW;
+        // visit the row in word order; compact with ballot/popc in lane order (ascending)
+        for (int t0 = 0; t0 < NT; t0 += 32) {
+            const int t = t0 + lane;
+            const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
+            const int cnt = t < NT ? min(static_cast<int>(__ldg(blk)), cap) : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const int start = base + incl - cnt;
+            for (int e = 0; e < cnt; ++e) {
+                const uint32_t w = __ldg(blk + 1 + e);
+                const int n = static_cast<int>(w & 0xFFFFu);
+                const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
+                gl[start + e] = (static_cast<uint32_t>(j) << 16) | (w >> 16);
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncwarp();
+    uint16_t* co = um.coff + i * (um.nchunk + 1);
+    for (int c = lane; c <= um.nchunk; c += 32) {
+        int lo = 0, hi = base;  // first entry with position >= 256 c
+        const uint32_t key = static_cast<uint32_t>(256 * c) << 16;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (gl[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        co[c] = static_cast<uint16_t>(lo);
+    }
 }
 
 // Row permutation pi (Alg.2 iterates m in pi(0..M-1); descending-nnz order): within each
