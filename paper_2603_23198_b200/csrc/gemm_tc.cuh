@@ -40,15 +40,22 @@ template <int EPI, int C>
 __host__ __device__ constexpr int gemm_epi_warp_bytes() {
     return EPI == EPI_TWELL ? 32 * (GEMM_BN / C) * 4 : (EPI == EPI_F32 ? 0 : 32 * 128 * 2);  // GLU/BF16/BF16_MN
 }
-template <int EPI, int C>
-__host__ __device__ constexpr int gemm_stages() {
-    return (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / GEMM_STAGE_BYTES > 6
-               ? 6
-               : (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / GEMM_STAGE_BYTES;
+// PAIR = 2: CTA-pair (cluster of 2, cta_group::2) variant — a 256 x 256 output tile per pair, each CTA loading
+// its own 128 A rows and HALF of the 256 B rows (128), the leader issuing M=256 MMAs that read both CTAs' SMEM.
+// Per SM this cuts the operand stream from 48 KB to 32 KB per k-block (same MMA work).
+template <int PAIR>
+__host__ __device__ constexpr int gemm_stage_bytes() {
+    return GEMM_A_BYTES + GEMM_B_BYTES / PAIR;
 }
-template <int EPI, int C>
+template <int EPI, int C, int PAIR = 1>
+__host__ __device__ constexpr int gemm_stages() {
+    return (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / gemm_stage_bytes<PAIR>() > 6
+               ? 6
+               : (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / gemm_stage_bytes<PAIR>();
+}
+template <int EPI, int C, int PAIR = 1>
 __host__ __device__ constexpr int gemm_smem_bytes() {
-    return 1024 + gemm_stages<EPI, C>() * GEMM_STAGE_BYTES + 4 * gemm_epi_warp_bytes<EPI, C>() + 256;
+    return 1024 + gemm_stages<EPI, C, PAIR>() * gemm_stage_bytes<PAIR>() + 4 * gemm_epi_warp_bytes<EPI, C>() + 256;
 }
 
 struct GemmArgs {
@@ -74,29 +81,36 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn_tc(uint32_t smem_addr) {
     return d;
 }
 
+template <int GROUP = GEMM_GROUP_M>
 __device__ __forceinline__ void gemm_tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
-    const int group = tile / (GEMM_GROUP_M * num_n);
-    const int first_m = group * GEMM_GROUP_M;
-    const int gm = min(GEMM_GROUP_M, num_m - first_m);
-    const int in = tile - group * GEMM_GROUP_M * num_n;
+    const int group = tile / (GROUP * num_n);
+    const int first_m = group * GROUP;
+    const int gm = min(GROUP, num_m - first_m);
+    const int in = tile - group * GROUP * num_n;
     mb = first_m + in % gm;
     nb = in / gm;
 }
 
-template <int EPI, int C>
+template <int EPI, int C, int PAIR = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmOut,
                    const GemmArgs args) {
-    constexpr int S = gemm_stages<EPI, C>();
+    constexpr int S = gemm_stages<EPI, C, PAIR>();
     constexpr int EWB = gemm_epi_warp_bytes<EPI, C>();
+    constexpr int B_BYTES = GEMM_B_BYTES / PAIR;  // this CTA's share of the B tile
+    constexpr int STAGE_BYTES = gemm_stage_bytes<PAIR>();
+    constexpr int PM = GEMM_BM * PAIR;            // output rows per (pair) tile
+    constexpr int GROUP = GEMM_GROUP_M / PAIR;
     static_assert(S >= 2, "not enough shared memory for a 2-stage ring");
+    static_assert(PAIR == 1 || PAIR == 2, "PAIR is 1 or 2");
+    static_assert(PAIR == 1 || EPI == EPI_TWELL || EPI == EPI_F32 || EPI == EPI_BF16, "pair mode: K-major B only");
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stA = smem;
     uint8_t* stB = smem + S * GEMM_A_BYTES;
-    uint8_t* epi = stB + S * GEMM_B_BYTES;
+    uint8_t* epi = stB + S * B_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * EWB);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
@@ -105,9 +119,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int num_m = args.m_dev ? (min(args.M, __ldg(args.m_dev)) + GEMM_BM - 1) / GEMM_BM : args.num_m;
+    const int num_m = args.m_dev ? (min(args.M, __ldg(args.m_dev)) + PM - 1) / PM : args.num_m;
     const int num_tiles = num_m * args.num_n;
     const int nk = (args.K + GEMM_BK - 1) / GEMM_BK;
+    const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0u;  // CTA rank in the pair (0 = leader / MMA issuer)
+    const int first_tile = blockIdx.x / PAIR, tile_step = gridDim.x / PAIR;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmA);
@@ -120,13 +136,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 4 * PAIR);  // every epilogue warp of the pair releases the leader's accumulator
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    if (warp == 2) {
+        if (PAIR == 2) tmem_alloc_pair(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR == 2) cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -136,11 +156,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint64_t pol = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
                 int mb, nb;
-                gemm_tile_coords(tile, num_m, args.num_n, mb, nb);
+                gemm_tile_coords<GROUP>(tile, num_m, args.num_n, mb, nb);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if constexpr (PAIR == 2) {
+                        // both CTAs' bytes complete on the leader's full barrier; only the leader expects them
+                        const uint32_t fb = mapa_shared(&full[stage], 0);
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                        tma_load_2d_pair(stA + stage * GEMM_A_BYTES, &tmA, fb, kb * GEMM_BK,
+                                         mb * PM + static_cast<int>(rank) * GEMM_BM, pol);
+                        tma_load_2d_pair(stB + stage * B_BYTES, &tmB, fb, kb * GEMM_BK,
+                                         nb * GEMM_BN + static_cast<int>(rank) * (GEMM_BN / 2), pol);
+                    } else {
                     mbar_arrive_expect_tx(&full[stage], GEMM_STAGE_BYTES);
                     tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, pol);
                     if (EPI == EPI_GLU) {
@@ -155,6 +184,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     } else {
                         tma_load_2d(stB + stage * GEMM_B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN, pol);
                     }
+                    }
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -163,34 +193,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, GEMM_BN) | (EPI == EPI_BF16_MN ? (1u << 16) : 0u);
+        // ------------------------------------------------------------ MMA issuer (the leader CTA in pair mode)
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t IDESC = umma_idesc_bf16(PM, GEMM_BN) | (EPI == EPI_BF16_MN ? (1u << 16) : 0u);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
+            for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
+                if (PAIR == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                else mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
-                    const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);
+                    const uint32_t b0 = smem_u32(stB + stage * B_BYTES);
+                    if constexpr (PAIR == 2) {
+#pragma unroll
+                        for (int k = 0; k < GEMM_BK / 16; ++k)
+                            umma_f16_pair(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
+                                          (kb | k) != 0);
+                        umma_commit_pair(&empty[stage]);
+                    } else {
 #pragma unroll
                     for (int k = 0; k < GEMM_BK / 16; ++k)
                         umma_f16(d, umma_desc_sw128(a0 + k * 32),
                                  EPI == EPI_BF16_MN ? umma_desc_sw128_mn_tc(b0 + k * 2048) : umma_desc_sw128(b0 + k * 32),
                                  IDESC, (kb | k) != 0);
                     umma_commit(&empty[stage]);
+                    }
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                if (PAIR == 2) umma_commit_pair(&tfull[acc]);
+                else umma_commit(&tfull[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -203,10 +243,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint8_t* stg = epi + ew * EWB;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const uint32_t tempty_leader = PAIR == 2 ? mapa_shared(tempty, 0) : 0u;
+        auto release_acc = [&](int a) {  // lane 0: this warp is done reading accumulator a
+            if (PAIR == 2) mbar_arrive_cluster(tempty_leader + 8u * static_cast<uint32_t>(a));
+            else mbar_arrive(&tempty[a]);
+        };
+        for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
             int mb, nb;
-            gemm_tile_coords(tile, num_m, args.num_n, mb, nb);
-            const int row0 = mb * GEMM_BM + ew * 32;
+            gemm_tile_coords<GROUP>(tile, num_m, args.num_n, mb, nb);
+            const int row0 = mb * PM + static_cast<int>(rank) * GEMM_BM + ew * 32;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
@@ -249,7 +294,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) release_acc(acc);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -274,7 +319,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) release_acc(acc);
             } else if constexpr (EPI == EPI_GLU) {
                 uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;  // 128 bf16 per row
 #pragma unroll 1
@@ -292,7 +337,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) release_acc(acc);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -319,7 +364,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     if (half == 1) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                        if (lane == 0) release_acc(acc);
                     }
                     fence_async_smem();
                     __syncwarp();
@@ -339,10 +384,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
     __syncwarp();
     tc_fence_before();
-    __syncthreads();
+    if (PAIR == 2) cluster_sync();  // the leader's MMAs write the peer's TMEM; remote arrives target the leader
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, 512);
+        if (PAIR == 2) tmem_dealloc_pair(tmem_base, 512);
+        else tmem_dealloc(tmem_base, 512);
     }
 }
 

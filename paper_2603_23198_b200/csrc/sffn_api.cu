@@ -71,6 +71,13 @@ int env_int(const char* name, int dflt) {
     return x > 0 ? x : dflt;
 }
 
+// on/off switch for A/B comparisons: "0" disables, anything else (or unset) keeps the default
+bool env_flag(const char* name, bool dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    return std::atoi(v) != 0;
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -80,22 +87,41 @@ bool valid_TC(int T, int C) {
     return T / C >= 2;
 }
 
-template <int EPI, int C>
+// PAIR = 2 launches clusters of two CTAs (one CTA pair per TPC, cta_group::2 MMAs); the B tensor map must then
+// have a 128-row box (each CTA loads half of the 256-row B tile).
+template <int EPI, int C, int PAIR = 1>
 int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b2, const CUtensorMap& o,
                 GemmArgs args, int n_tile_cols, cudaStream_t st) {
-    auto kern = gemm_tc_kernel<EPI, C>;
-    constexpr int smem = gemm_smem_bytes<EPI, C>();
+    auto kern = gemm_tc_kernel<EPI, C, PAIR>;
+    constexpr int smem = gemm_smem_bytes<EPI, C, PAIR>();
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
     if (attr_err != cudaSuccess) return SFFN_ERR_CUDA;
-    args.num_m = (args.M + GEMM_BM - 1) / GEMM_BM;
+    args.num_m = (args.M + GEMM_BM * PAIR - 1) / (GEMM_BM * PAIR);
     args.num_n = (args.N + n_tile_cols - 1) / n_tile_cols;
     const int tiles = args.num_m * args.num_n;
     if (tiles == 0) return SFFN_OK;
     DevInfo d = dev_info();
-    const int grid = tiles < d.sms ? tiles : d.sms;
-    kern<<<grid, GEMM_THREADS, smem, st>>>(a, b, b2, o, args);
+    if constexpr (PAIR == 1) {
+        const int grid = tiles < d.sms ? tiles : d.sms;
+        kern<<<grid, GEMM_THREADS, smem, st>>>(a, b, b2, o, args);
+    } else {
+        const int pairs = tiles < d.sms / 2 ? tiles : d.sms / 2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(GEMM_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, a, b, b2, o, args) != cudaSuccess) return SFFN_ERR_CUDA;
+    }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -108,9 +134,12 @@ int check_device() {
 
 int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
               uint32_t* d_overflow, cudaStream_t st) {
+    // CTA-pair gate GEMM by default (SFFN_GATE_PAIR=0 selects the single-CTA kernel)
+    static const bool pair = env_flag("SFFN_GATE_PAIR", true);
     CUtensorMap ta, tb, to;
     if (!tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, GEMM_BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, pair ? GEMM_BN / 2 : GEMM_BN,
+                 CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, twell, N / C, M, GEMM_BN / C, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
         return SFFN_ERR_CUDA;
     GemmArgs args{};
@@ -119,13 +148,18 @@ int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, in
     args.K = static_cast<int>(K);
     args.T = T;
     args.overflow = d_overflow;
+#define SFFN_PACK_CASE(CC)                                                                              \
+    case CC:                                                                                            \
+        return pair ? launch_gemm<EPI_TWELL, CC, 2>(ta, tb, tb, to, args, GEMM_BN, st)                  \
+                    : launch_gemm<EPI_TWELL, CC, 1>(ta, tb, tb, to, args, GEMM_BN, st);
     switch (C) {
-        case 1: return launch_gemm<EPI_TWELL, 1>(ta, tb, tb, to, args, GEMM_BN, st);
-        case 2: return launch_gemm<EPI_TWELL, 2>(ta, tb, tb, to, args, GEMM_BN, st);
-        case 4: return launch_gemm<EPI_TWELL, 4>(ta, tb, tb, to, args, GEMM_BN, st);
-        case 8: return launch_gemm<EPI_TWELL, 8>(ta, tb, tb, to, args, GEMM_BN, st);
-        case 16: return launch_gemm<EPI_TWELL, 16>(ta, tb, tb, to, args, GEMM_BN, st);
+        SFFN_PACK_CASE(1)
+        SFFN_PACK_CASE(2)
+        SFFN_PACK_CASE(4)
+        SFFN_PACK_CASE(8)
+        SFFN_PACK_CASE(16)
     }
+#undef SFFN_PACK_CASE
     return SFFN_ERR_INVALID_ARG;
 }
 
