@@ -240,6 +240,10 @@ def main():
     # synchronization, device-side work counts) and replayed: removes the per-launch CPU/driver gaps
     step_fn = step
     graph = None
+    c0 = sffn.launch_count()
+    step()  # one eager step: the library's own kernel launches per step (host-side counter of the .so)
+    launches_per_step = sffn.launch_count() - c0
+    torch.cuda.synchronize()
     if not args.no_graph and world == 1:
         for _ in range(2):
             step()  # first calls set kernel attributes outside the capture
@@ -270,6 +274,9 @@ def main():
     ms_pack = timed(lambda: sffn.pack(X, Wg, T, C, out=tw), max(5, args.steps // 2), 3)
     ms_ud = timed(lambda: sffn.up_down(X, tw, Wu, Wd, T, C, out=Y, workspace=ud_ws, algo=args.algo),
                   max(5, args.steps // 2), 3)
+    c0 = sffn.launch_count()
+    sffn.up_down(X, tw, Wu, Wd, T, C, out=Y, workspace=ud_ws, algo=args.algo)
+    ud_launches = sffn.launch_count() - c0
     t_pack = float(np.median(ms_pack)) / 1e3
     t_ud = float(np.median(ms_ud)) / 1e3
     twords = tw.cpu().numpy().view(np.uint32).reshape(M, Nl // T, T // C)
@@ -289,7 +296,7 @@ def main():
         st = sffn.union_stats(ud_ws, M, K, Nl)
         tc_flop = 4.0 * 128 * st["padded_sum"] * K  # the two union GEMMs
         kernels["fused_up_down"] = {
-            "ms": t_ud * 1e3, "launches": 7, "algo": "union", "bound": "tensor",
+            "ms": t_ud * 1e3, "launches": ud_launches, "algo": "union", "bound": "tensor",
             "achieved": tc_flop / t_ud / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": tc_flop / t_ud / 1e12 / peaks["bf16_tflops"],
             "algorithmic": "4*128*sum_b |U_b| * K FLOP (union GEMMs)",
@@ -297,11 +304,11 @@ def main():
             "useful_tflops": ud_flop / t_ud / 1e12}
     else:
         kernels["fused_up_down"] = {
-            "ms": t_ud * 1e3, "launches": 1, "algo": "gather", "bound": "alu", "achieved": ud_flop / t_ud / 1e12,
+            "ms": t_ud * 1e3, "launches": ud_launches, "algo": "gather", "bound": "alu", "achieved": ud_flop / t_ud / 1e12,
             "peak": fma_peak, "unit": "TFLOP/s", "frac": ud_flop / t_ud / 1e12 / fma_peak,
             "algorithmic": "4*K*nnz FLOP", "hbm_compulsory_gbs": ud_compulsory / t_ud / 1e9,
             "gathered_gbs": 4.0 * K * nnz_total / t_ud / 1e9}
-    # the dominant single launch: the gate GEMM (the union up/down is 7 launches, none longer than it;
+    # the dominant single launch: the gate GEMM (the union up/down is several launches, none longer than it;
     # see profiles/ launch lists); the gather kernel is one launch and longer than the gate GEMM
     dom = "gate_gemm_twell" if (algo_used == "union" or t_pack >= t_ud) else "fused_up_down"
     traffic = None
@@ -377,9 +384,8 @@ def main():
                "tokens_per_s_per_gpu": value / world,
                "roofline": roofline, "kernels": kernels, "nnz_per_token": nnz_total / M,
                "overflow_tiles": n_ov, "dense": dense, "e2e": e2e, "cpu_baseline": cpu,
-               "gpu_launches": args.steps * (kernels["gate_gemm_twell"]["launches"] +
-                                             kernels["fused_up_down"]["launches"]) *
-                               (1 if world == 1 else max(1, min(args.chunks, (M + 255) // 256))),
+               "gpu_launches": args.steps * launches_per_step,
+               "gpu_launches_per_step": launches_per_step,
                "algo": algo_used,
                "clocks": clk}
         line = json.dumps(out)

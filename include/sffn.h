@@ -68,6 +68,10 @@ typedef enum { SFFN_ALGO_AUTO = 0, SFFN_ALGO_GATHER = 1, SFFN_ALGO_UNION = 2 } s
 /* Human-readable name of a status code (static storage). */
 const char* sffn_status_string(int status);
 /* Library version / build string (static storage). */
+/* Number of CUDA kernels the library has launched so far in this process (host-side counter; a launch
+ * captured into a CUDA graph counts once, at capture).  Benchmarks read it around a step to report how
+ * many of the library's own kernels a step runs.  Thread-safe, never fails. */
+int64_t sffn_launch_count(void);
 const char* sffn_version(void);
 
 /* Number of uint32 words of a packed TwELL for [M, N] with tile T and compression C: M * N / C. */
@@ -165,8 +169,10 @@ int sffn_forward_nongated(const void* X, const void* Wu, const void* Wd, int64_t
 
 /*
  * sffn_forward_host — sffn_forward with X and Y in HOST memory (page-locked for overlap): rows are
- * processed in chunks of `chunk_rows` (a multiple of 128; a multiple of 2048 keeps the UNION row
- * permutation windows, hence the results, identical to one sffn_forward call); the host->device copy of
+ * processed in chunks of at most `chunk_rows` (a multiple of 128; a multiple of 2048 keeps the UNION row
+ * permutation windows, hence the results, identical to one sffn_forward call).  Chunk sizes ramp up
+ * geometrically from chunk_rows/4 at the start and back down at the end (short pipeline fill / drain),
+ * full-size chunks in between (the forward's per-call cost amortised); the host->device copy of
  * chunk i+1 and the device->host copy of chunk i-1 overlap the compute of chunk i on two internal copy
  * streams (created once per device, event-ordered; no host synchronization).  The call is
  * stream-ordered on `stream`: Y_host is complete when `stream` reaches this point.
@@ -174,6 +180,9 @@ int sffn_forward_nongated(const void* X, const void* Wu, const void* Wd, int64_t
  *   workspace: >= sffn_forward_workspace_bytes(min(chunk_rows, M), K, N, T, C, algo)
  */
 size_t sffn_forward_host_stage_bytes(int64_t K, int64_t chunk_rows);
+/* The chunk schedule sffn_forward_host uses (host only, no device work): writes up to `cap` chunk row
+ * counts to `sizes` (may be null) and returns the number of chunks; 0 on a bad argument. */
+int64_t sffn_forward_host_chunks(int64_t M, int64_t chunk_rows, int64_t* sizes, int64_t cap);
 int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y_host, void* workspace, size_t ws_bytes, void* stage,
                       size_t stage_bytes, uint32_t* d_overflow, int algo, int64_t chunk_rows, void* stream);

@@ -68,6 +68,7 @@ struct GemmArgs {
     float* out_f32;      // EPI_F32
     int64_t ld_out;      // EPI_F32 row stride (elements)
     const int* m_dev;    // optional device row count: rows >= min(M, *m_dev) are skipped (dense backup rows)
+    int* row_nnz;        // EPI_TWELL, may be null: += stored entries (min(count, cap)) of each row (zeroed by caller)
 };
 
 // MN-major 128B-swizzled operand: 64-column atoms 8 KB apart (LBO), 8-row groups 1 KB apart (SBO)
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * ROW_WORDS;
                 const int col_base = nb * GEMM_BN;
                 const bool row_ok = row0 + lane < args.M;
-                int z = 0;
+                int z = 0, stored = 0;
 #pragma unroll 1
                 for (int ch = 0; ch < GEMM_BN / 32; ++ch) {
                     uint32_t v[32];
@@ -290,8 +291,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     if ((tcol + 32) % T == 0) {
                         blk[0] = static_cast<uint32_t>(z);  // Alg.1 line 17: true count
                         if (z > cap && row_ok && args.overflow) atomicAdd(args.overflow, 1u);
+                        stored += min(z, cap);
                     }
                 }
+                if (args.row_nnz && row_ok && stored) atomicAdd(args.row_nnz + row0 + lane, stored);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(acc);

@@ -3,6 +3,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -17,6 +19,10 @@
 #include "updown.cuh"
 
 using namespace sffn;
+
+// host-side count of the kernels this library has launched (or captured into a graph): sffn_launch_count()
+static std::atomic<long long> g_launches{0};
+static inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
@@ -105,7 +111,7 @@ int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b
     DevInfo d = dev_info();
     if constexpr (PAIR == 1) {
         const int grid = tiles < d.sms ? tiles : d.sms;
-        kern<<<grid, GEMM_THREADS, smem, st>>>(a, b, b2, o, args);
+        { kern<<<grid, GEMM_THREADS, smem, st>>>(a, b, b2, o, args); note_launch(); }
     } else {
         const int pairs = tiles < d.sms / 2 ? tiles : d.sms / 2;
         cudaLaunchConfig_t cfg{};
@@ -121,6 +127,7 @@ int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b
         cfg.attrs = at;
         cfg.numAttrs = 1;
         if (cudaLaunchKernelEx(&cfg, kern, a, b, b2, o, args) != cudaSuccess) return SFFN_ERR_CUDA;
+        note_launch();
     }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
@@ -133,7 +140,7 @@ int check_device() {
 }
 
 int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
-              uint32_t* d_overflow, cudaStream_t st) {
+              uint32_t* d_overflow, cudaStream_t st, int* row_nnz = nullptr) {
     // CTA-pair gate GEMM by default (SFFN_GATE_PAIR=0 selects the single-CTA kernel)
     static const bool pair = env_flag("SFFN_GATE_PAIR", true);
     CUtensorMap ta, tb, to;
@@ -148,6 +155,7 @@ int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, in
     args.K = static_cast<int>(K);
     args.T = T;
     args.overflow = d_overflow;
+    args.row_nnz = row_nnz;
 #define SFFN_PACK_CASE(CC)                                                                              \
     case CC:                                                                                            \
         return pair ? launch_gemm<EPI_TWELL, CC, 2>(ta, tb, tb, to, args, GEMM_BN, st)                  \
@@ -185,13 +193,13 @@ int updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* W
     const uint4* wd = static_cast<const uint4*>(Wd);
     uint4* y = static_cast<uint4*>(Y);
     if (nch_needed <= 1)
-        updown_kernel<1><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+        { updown_kernel<1><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
     else if (nch_needed <= 2)
-        updown_kernel<2><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+        { updown_kernel<2><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
     else if (nch_needed <= 4)
-        updown_kernel<4><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+        { updown_kernel<4><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
     else if (nch_needed <= 8)
-        updown_kernel<8><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+        { updown_kernel<8><<<grid, block, 0, st>>>(x, tw, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
     else
         return SFFN_ERR_SHAPE;
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
@@ -254,8 +262,14 @@ size_t updown_ws_bytes(int64_t M, int64_t N, int64_t K, int algo, int T = 32, in
     return static_cast<size_t>(union_ws_layout(M, N, K, T, C).total);
 }
 
+// Row nnz buffer of the union workspace (sffn_forward lets the gate GEMM epilogue fill it: nnz_ready)
+int* union_nnz_ptr(void* ws, int64_t M, int64_t N, int64_t K, int T, int C) {
+    return reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + union_ws_layout(M, N, K, T, C).nnz);
+}
+
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
-                      int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true) {
+                      int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true,
+                      bool nnz_ready = false) {
     const int64_t NB = (M + 127) / 128;
     UnionWs L = union_ws_layout(M, N, K, T, C);
     uint8_t* base = static_cast<uint8_t*>(ws);
@@ -277,28 +291,35 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     void* xp = base + L.xp;
     // row permutation pi (per 2048-row window, descending stored nnz) and the permuted copy of X
     int* rnnz = reinterpret_cast<int*>(base + L.nnz);
-    row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz);
-    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    union_perm_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), 1024, 0, st>>>(rnnz, (int)M, perm);
+    int* done_ctr = um.counters + 2;  // union_meta_kernel completion counter (zeroed by union_rank_kernel)
+    if (!nnz_ready) {
+        { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
+        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    }
+    { union_rank_kernel<<<dim3(static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_SPLIT), PERM_W / PERM_SPLIT, 0,
+                        st>>>(rnnz, (int)M, perm, done_ctr); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     if (gated) {
-        permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
-            static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp));
+        { permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+            static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp)); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
 
+    // union lists + the UP work list (one launch), then the compact gate lists (gated) or the scattered G (non-gated)
     const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
-    union_build_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(tw, (int)M, (int)N, T, C, um, perm);
+    { union_meta_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(
+        tw, (int)M, (int)N, T, C, um, perm, done_ctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP)); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    if (gated)  // compact gate lists consumed by the UP epilogue
-        union_gate_list_kernel<<<static_cast<unsigned>(NB * 128 * 32 / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C,
-                                                                                           um, perm);
-    else  // non-gated: H_c = the scattered TwELL values (no up GEMM)
-        union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (128 / GS_ROWS)), 256, 0, st>>>(
-            tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm);
-    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    union_scan_kernel<<<1, 1024, 0, st>>>(um, (int)NB, env_int("SFFN_UP_GROUP", UNION_GROUP_UP));
-    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    if (gated) {
+        { union_gate_list_kernel<<<static_cast<unsigned>(NB * 128 * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
+            tw, (int)M, (int)N, T, C, um, perm); note_launch(); }
+        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    }
+    if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)
+        { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (128 / GS_ROWS)), 256, 0, st>>>(
+            tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm); note_launch(); }
+        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    }
 
     CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
     if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M > 0 ? M : 1, GEMM_BK, GEMM_BM,
@@ -340,12 +361,12 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     if (gated) {
         // UP: the number of (block, chunk) tiles is only known on the device; persistent grid.  For the
         // non-gated variant H_c already holds h = relu(x W_u) (the scattered TwELL values): no UP GEMM.
-        union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua);
+        { union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
     const int64_t dtiles = NB * ua.NJ;
     const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
-    union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud);
+    { union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -378,6 +399,8 @@ const char* sffn_status_string(int s) {
     }
     return "SFFN_ERR_UNKNOWN";
 }
+
+int64_t sffn_launch_count(void) { return static_cast<int64_t>(g_launches.load()); }
 
 const char* sffn_version(void) { return "sffn 0.1 (sm_100a tcgen05/TMEM/TMA)"; }
 
@@ -419,8 +442,8 @@ int sffn_unpack(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int64
     if (warps == 0) return SFFN_OK;
     const int64_t blocks = (warps * 32 + 255) / 256;
     if (blocks > 2147483647) return SFFN_ERR_SHAPE;
-    unpack_kernel<<<static_cast<unsigned>(blocks), 256, 0, S(stream)>>>(twell, (int)M, (int)N, T, C, col_offset,
-                                                                         ld_dense, static_cast<__nv_bfloat16*>(dense));
+    { unpack_kernel<<<static_cast<unsigned>(blocks), 256, 0, S(stream)>>>(twell, (int)M, (int)N, T, C, col_offset,
+                                                                         ld_dense, static_cast<__nv_bfloat16*>(dense)); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -449,9 +472,17 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
     if (M == 0) return SFFN_OK;
     uint32_t* tw = static_cast<uint32_t*>(workspace);
     const int64_t tw_bytes = align1k(sffn_twell_words(M, N, T, C) * 4);
+    uint8_t* udws = static_cast<uint8_t*>(workspace) + tw_bytes;
+    if (resolve_algo(algo, N) == SFFN_ALGO_UNION) {
+        // the gate GEMM epilogue also counts each row's stored entries (the union path's row order pi)
+        int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
+        if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+        if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz)) != SFFN_OK) return r;
+        return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true);
+    }
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
-    return updown_dispatch(X, tw, Wu, Wd, M, K, N, T, C, Y, static_cast<uint8_t*>(workspace) + tw_bytes,
-                           ws_bytes - static_cast<size_t>(tw_bytes), algo, S(stream));
+    return updown_dispatch(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, ws_bytes - static_cast<size_t>(tw_bytes), algo,
+                           S(stream));
 }
 
 int sffn_down(const uint32_t* twell, const void* Wd, int64_t M, int64_t K, int64_t N, int T, int C, void* Y,
@@ -473,10 +504,10 @@ int sffn_down(const uint32_t* twell, const void* Wd, int64_t M, int64_t K, int64
     const uint4* wd = static_cast<const uint4*>(Wd);
     uint4* y = static_cast<uint4*>(Y);
     dim3 g(static_cast<unsigned>(M)), blk(UD_WARPS * 32);
-    if (nch <= 1) down_kernel<1><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
-    else if (nch <= 2) down_kernel<2><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
-    else if (nch <= 4) down_kernel<4><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
-    else if (nch <= 8) down_kernel<8><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C);
+    if (nch <= 1) { down_kernel<1><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
+    else if (nch <= 2) { down_kernel<2><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
+    else if (nch <= 4) { down_kernel<4><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
+    else if (nch <= 8) { down_kernel<8><<<g, blk, 0, st>>>(twell, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
     else return SFFN_ERR_SHAPE;
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
@@ -533,8 +564,8 @@ int sffn_transpose_bf16(const void* in, int64_t rows, int64_t cols, void* out, v
     if (r != SFFN_OK) return r;
     if (rows == 0 || cols == 0) return SFFN_OK;
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32)), block(32, 8);
-    transpose_bf16_kernel<<<grid, block, 0, S(stream)>>>(static_cast<const __nv_bfloat16*>(in), rows, cols,
-                                                         static_cast<__nv_bfloat16*>(out));
+    { transpose_bf16_kernel<<<grid, block, 0, S(stream)>>>(static_cast<const __nv_bfloat16*>(in), rows, cols,
+                                                         static_cast<__nv_bfloat16*>(out)); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -592,7 +623,7 @@ int sffn_pack_f32(const float* X, const float* Wg, int64_t M, int64_t K, int64_t
     if (attr != cudaSuccess) return SFFN_ERR_CUDA;
     dim3 grid(static_cast<unsigned>((N + F32_BN - 1) / F32_BN), static_cast<unsigned>((M + F32_BM - 1) / F32_BM));
     if (grid.y > 65535) return SFFN_ERR_SHAPE;
-    pack_f32_kernel<<<grid, 256, smem, S(stream)>>>(X, Wg, (int)M, (int)K, (int)N, T, C, hv, hi, hnz, d_overflow);
+    { pack_f32_kernel<<<grid, 256, smem, S(stream)>>>(X, Wg, (int)M, (int)K, (int)N, T, C, hv, hi, hnz, d_overflow); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -614,11 +645,11 @@ int sffn_up_down_f32(const float* X, const float* hv, const uint16_t* hi, const 
     float4* y = reinterpret_cast<float4*>(Y);
     dim3 g(static_cast<unsigned>(M));
     cudaStream_t st = S(stream);
-    if (nch <= 1) updown_f32_kernel<1><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
-    else if (nch <= 2) updown_f32_kernel<2><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
-    else if (nch <= 4) updown_f32_kernel<4><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
-    else if (nch <= 8) updown_f32_kernel<8><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
-    else updown_f32_kernel<16><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C);
+    if (nch <= 1) { updown_f32_kernel<1><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
+    else if (nch <= 2) { updown_f32_kernel<2><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
+    else if (nch <= 4) { updown_f32_kernel<4><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
+    else if (nch <= 8) { updown_f32_kernel<8><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
+    else { updown_f32_kernel<16><<<g, 128, 0, st>>>(x, hv, hi, hnz, wu, wd, y, (int)M, (int)K, (int)N, T, C); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -659,6 +690,46 @@ int copy_streams(int dev, CopyStreams* out) {
 }
 }  // namespace
 
+// Row chunks of sffn_forward_host: sizes ramp geometrically (R/4, R/2, ...) up to R = chunk_rows at the start and
+// back down at the end, so the first host->device copy and the last device->host copy (pipeline fill and drain,
+// not overlapped with compute) are short, while the middle chunks are large (the per-call fixed cost of the
+// forward is amortised).  Chunk starts stay multiples of the unit u (2048 when R is, so the UNION permutation
+// windows are those of one sffn_forward call); a ragged remainder goes to the last chunk.  Every size <= R.
+static std::vector<int64_t> host_chunk_plan(int64_t M, int64_t R) {
+    std::vector<int64_t> out;
+    const int64_t u = R % 2048 == 0 ? 2048 : 128;
+    std::vector<int64_t> ramp;
+    for (int64_t s = std::max(u, (R / 4) / u * u); s < R; s *= 2) ramp.push_back(s);
+    int64_t rsum = 0;
+    for (int64_t s : ramp) rsum += s;
+    const int64_t Mu = M / u * u;
+    if (ramp.empty() || 2 * rsum >= Mu || M - Mu + ramp.front() > R) {
+        for (int64_t r0 = 0; r0 < M; r0 += R) out.push_back(std::min(R, M - r0));
+        return out;
+    }
+    const int64_t mid = Mu - 2 * rsum;
+    const int64_t n = (mid + R - 1) / R;
+    const int64_t each = ((mid / n) + u - 1) / u * u;
+    out = ramp;
+    int64_t left = mid;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t s = i + 1 < n ? std::min(each, left) : left;
+        out.push_back(s);
+        left -= s;
+    }
+    for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) out.push_back(*it);
+    out.back() += M - Mu;
+    return out;
+}
+
+int64_t sffn_forward_host_chunks(int64_t M, int64_t chunk_rows, int64_t* sizes, int64_t cap) {
+    if (M <= 0 || chunk_rows <= 0 || chunk_rows % 128 != 0) return 0;
+    const int64_t rows = chunk_rows < M ? chunk_rows : ((M + 127) / 128) * 128;
+    std::vector<int64_t> v = host_chunk_plan(M, rows);
+    for (int64_t i = 0; sizes && i < cap && i < static_cast<int64_t>(v.size()); ++i) sizes[i] = v[static_cast<size_t>(i)];
+    return static_cast<int64_t>(v.size());
+}
+
 size_t sffn_forward_host_stage_bytes(int64_t K, int64_t chunk_rows) {
     if (K <= 0 || chunk_rows <= 0) return 0;
     return static_cast<size_t>(4 * align1k(chunk_rows * K * 2));  // 2 x X slots + 2 x Y slots
@@ -681,7 +752,9 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     CopyStreams cs;
     if ((r = copy_streams(dev, &cs)) != SFFN_OK) return r;
     cudaStream_t st = S(stream);
-    const int64_t nchunks = (M + rows - 1) / rows;
+    // chunk schedule: ramp up / down in size at the ends (short pipeline fill and drain), full chunks between
+    std::vector<int64_t> sizes = host_chunk_plan(M, rows);
+    const int64_t nchunks = static_cast<int64_t>(sizes.size());
     const int64_t slot = align1k(rows * K * 2);
     uint8_t* xs[2] = {static_cast<uint8_t*>(stage), static_cast<uint8_t*>(stage) + slot};
     uint8_t* ys[2] = {static_cast<uint8_t*>(stage) + 2 * slot, static_cast<uint8_t*>(stage) + 3 * slot};
@@ -694,8 +767,9 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     cudaEventRecord(ev.back(), st);
     cudaStreamWaitEvent(cs.h2d, ev.back(), 0);
     cudaStreamWaitEvent(cs.d2h, ev.back(), 0);
-    for (int64_t i = 0; i < nchunks && r == SFFN_OK; ++i) {
-        const int64_t r0 = i * rows, mr = (M - r0) < rows ? (M - r0) : rows;
+    int64_t r0 = 0;
+    for (int64_t i = 0; i < nchunks && r == SFFN_OK; r0 += sizes[static_cast<size_t>(i)], ++i) {
+        const int64_t mr = sizes[static_cast<size_t>(i)];
         const size_t bytes = static_cast<size_t>(mr * K * 2);
         const int sl = static_cast<int>(i & 1);
         if (i >= 2) cudaStreamWaitEvent(cs.h2d, E(1, i - 2), 0);  // X slot free once chunk i-2 computed
@@ -760,8 +834,8 @@ int sffn_forward_hybrid(const void* X, const void* Wg, const void* Wu, const voi
     int* cnt = reinterpret_cast<int*>(b + L.cnt);
     int32_t* list = reinterpret_cast<int32_t*>(b + L.list);
     if (cudaMemsetAsync(cnt, 0, 4, st) != cudaSuccess) return SFFN_ERR_CUDA;
-    ov_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
-        static_cast<const uint32_t*>(workspace), (int)M, (int)N, T, C, cnt, list, (int)R);
+    { ov_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint32_t*>(workspace), (int)M, (int)N, T, C, cnt, list, (int)R); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     if (d_backup_count && cudaMemcpyAsync(d_backup_count, cnt, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return SFFN_ERR_CUDA;
@@ -770,8 +844,8 @@ int sffn_forward_hybrid(const void* X, const void* Wg, const void* Wu, const voi
     void* ho = b + L.ho;
     void* yo = b + L.yo;
     const unsigned g = static_cast<unsigned>((R * 32 + 255) / 256);
-    move_rows_kernel<true><<<g, 256, 0, st>>>(static_cast<const uint4*>(X), static_cast<uint4*>(xo), list, cnt, (int)R,
-                                              (int)(K / 8));
+    { move_rows_kernel<true><<<g, 256, 0, st>>>(static_cast<const uint4*>(X), static_cast<uint4*>(xo), list, cnt, (int)R,
+                                              (int)(K / 8)); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     CUtensorMap tx, tg, tu, th_out, th_in, twd, ty;
     if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xo, K, R, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -794,8 +868,8 @@ int sffn_forward_hybrid(const void* X, const void* Wg, const void* Wu, const voi
     a2.K = (int)N;
     a2.m_dev = cnt;
     if ((r = launch_gemm<EPI_BF16_MN, 1>(th_in, twd, twd, ty, a2, GEMM_BN, st)) != SFFN_OK) return r;
-    move_rows_kernel<false><<<g, 256, 0, st>>>(static_cast<const uint4*>(yo), static_cast<uint4*>(Y), list, cnt,
-                                               (int)R, (int)(K / 8));
+    { move_rows_kernel<false><<<g, 256, 0, st>>>(static_cast<const uint4*>(yo), static_cast<uint4*>(Y), list, cnt,
+                                               (int)R, (int)(K / 8)); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -809,9 +883,9 @@ int sffn_twell_to_hybrid(const uint32_t* twell, int64_t M, int64_t N, int T, int
     if (dense_cap > 0 && (!dense_rows || !dense_map)) return SFFN_ERR_INVALID_ARG;
     int r = check_device();
     if (r != SFFN_OK) return r;
-    twell_to_hybrid_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, S(stream)>>>(
+    { twell_to_hybrid_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, S(stream)>>>(
         twell, (int)M, (int)N, T, C, ell_w, static_cast<uint16_t*>(ell_val), ell_col, row_nnz, row_loc,
-        (int)dense_cap, static_cast<uint16_t*>(dense_rows), dense_map, d_dense_count, d_l0l1);
+        (int)dense_cap, static_cast<uint16_t*>(dense_rows), dense_map, d_dense_count, d_l0l1); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 

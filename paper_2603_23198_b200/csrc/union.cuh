@@ -31,6 +31,7 @@ struct UnionMeta {
 
 constexpr int UNION_GROUP_UP = 8;    // token blocks whose up-GEMM tiles run together (L2 working set)
 constexpr int UNION_GROUP_DOWN = 16;  // token blocks whose down-GEMM tiles run together
+constexpr int UNION_GROUP_MAX = 16;   // largest UP group the work-list builder supports
 
 constexpr int UB_THREADS = 512;
 
@@ -43,12 +44,13 @@ __device__ __forceinline__ void for_each_row_entry(const uint32_t* __restrict__ 
     if (WPT >= 4 && WPT <= 32) {
         const uint4* r4 = reinterpret_cast<const uint4*>(row);
         const int RW4 = RW >> 2;
-        for (int g0 = 0; g0 < RW4; g0 += 64) {
-            uint4 v[2];
+        constexpr int U = 8;  // 8 x 512 bytes of the row in flight per warp
+        for (int g0 = 0; g0 < RW4; g0 += 32 * U) {
+            uint4 v[U];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) v[u] = (g0 + 32 * u + lane < RW4) ? __ldg(r4 + g0 + 32 * u + lane) : make_uint4(0, 0, 0, 0);
+            for (int u = 0; u < U; ++u) v[u] = (g0 + 32 * u + lane < RW4) ? __ldg(r4 + g0 + 32 * u + lane) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int w0 = 4 * (g0 + 32 * u + lane);  // first word of this lane
                 const int s0 = w0 % WPT;                 // slot of v.x
                 const int src = lane - (s0 >> 2);
@@ -72,26 +74,123 @@ __device__ __forceinline__ void for_each_row_entry(const uint32_t* __restrict__ 
     }
 }
 
-// One CTA per block of 128 rows.  Dynamic smem: N/32 uint32 masks + N/32 int32 offsets + scan scratch.
-__global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
-                                                                  int C, UnionMeta um, const int32_t* __restrict__ perm) {
+// Visit every stored entry of one packed TwELL row, lane per tile (ascending tiles over lanes): the count word and
+// the first three entries come in one 16-byte load, further entries 16 bytes at a time only when the tile holds
+// them, so a row of mostly short tiles costs one 32-byte sector per tile instead of the full T/C words.
+// f(word, tile, e) gets the e-th stored entry (0-based) of tile `tile`.  Requires a 16-byte aligned row.
+template <class F>
+__device__ __forceinline__ void for_each_tile_entry(const uint32_t* __restrict__ row, int NT, int WPT, int cap,
+                                                    int t, F&& f) {
+    const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
+    if ((WPT & 3) == 0) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(blk));
+        const int cnt = min(static_cast<int>(a.x), cap);
+        if (cnt >= 1) f(a.y, 0);
+        if (cnt >= 2) f(a.z, 1);
+        if (cnt >= 3) f(a.w, 2);
+        for (int s = 4; s <= cnt; s += 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(blk + s));
+            f(v.x, s - 1);
+            if (s + 1 <= cnt) f(v.y, s);
+            if (s + 2 <= cnt) f(v.z, s + 1);
+            if (s + 3 <= cnt) f(v.w, s + 2);
+        }
+    } else {
+        const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+        for (int e = 0; e < cnt; ++e) f(__ldg(blk + 1 + e), e);
+    }
+}
+__device__ __forceinline__ int tile_count(const uint32_t* __restrict__ row, int WPT, int cap, int t) {
+    return min(static_cast<int>(__ldg(row + static_cast<int64_t>(t) * WPT)), cap);
+}
+
+// UP work list (the former union_scan kernel, now run by the last block CTA of union_meta_kernel): for each group
+// of `group` blocks, chunk-major then block: tiles[] = (b << 8) | c; chunk_off[0] = total tiles; zeroes the two
+// dynamic tile-scheduler counters.  NTH threads, scratch = NTH/32 + 1 ints of shared memory.
+template <int NTH>
+__device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum) {
+    constexpr int NWP = NTH / 32;
+    constexpr int MAXG = UNION_GROUP_MAX;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    group = max(1, min(group, MAXG));
+    const int NG = (NB + group - 1) / group;
+    int carry = 0;
+    for (int base = 0; base < NG; base += NTH) {
+        const int g = base + static_cast<int>(threadIdx.x);
+        const int b0 = g * group;
+        int nchk[MAXG];  // chunks of each block of the group (registers: no dependent loads in the write loop)
+        int tot = 0, maxc = 0;
+#pragma unroll
+        for (int j = 0; j < MAXG; ++j) {
+            const int bb = b0 + j;
+            nchk[j] = (g < NG && j < group && bb < NB) ? (__ldcg(um.ulen + bb) + 255) / 256 : 0;
+            tot += nchk[j];
+            maxc = max(maxc, nchk[j]);
+        }
+        int sc = tot;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, sc, off);
+            if (lane >= off) sc += u;
+        }
+        if (lane == 31) wsum[warp] = sc;
+        __syncthreads();
+        if (warp == 0) {
+            const int x = lane < NWP ? wsum[lane] : 0;
+            int y = x;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, y, off);
+                if (lane >= off) y += u;
+            }
+            if (lane < NWP) wsum[lane] = y - x;
+            if (lane == 31) wsum[NWP] = y;
+        }
+        __syncthreads();
+        int pos = carry + wsum[warp] + sc - tot;
+        for (int c = 0; c < maxc; ++c)
+#pragma unroll
+            for (int j = 0; j < MAXG; ++j)
+                if (c < nchk[j]) um.tiles[pos++] = ((b0 + j) << 8) | c;
+        carry += wsum[NWP];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        um.chunk_off[0] = carry;
+        um.counters[0] = 0;
+        um.counters[1] = 0;
+    }
+}
+
+// Union metadata of one block of 128 pi-ordered rows, one CTA (UB_THREADS) per block:
+//   1. OR of the rows' stored indices into a SMEM bitmask (warp per row, coalesced row reads);
+//   2. prefix sums -> sorted U_b (padded to a multiple of 64 with unit 0), umask / uwoff / ulen / utot;
+//   3. the last CTA to finish (device-scope counter, zeroed by union_rank_kernel) builds the UP work list.
+// Dynamic SMEM: 2 N/32 words + (UB_THREADS/32 + 1) scan ints.
+__global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
+                                                                 int C, UnionMeta um, const int32_t* __restrict__ perm,
+                                                                 int* done_ctr, int up_group) {
     extern __shared__ uint32_t ub_smem[];
+    constexpr int NWP = UB_THREADS / 32;
     const int NW = N >> 5;
     uint32_t* mask = ub_smem;                                  // [NW]
     int32_t* woff = reinterpret_cast<int32_t*>(ub_smem + NW);  // [NW]
-    int32_t* wsum = woff + NW;                                 // [UB_THREADS / 32]
+    int32_t* wsum = woff + NW;                                 // [NWP + 1]
+    __shared__ int s_last;
+    __shared__ int s_prow[128];
     const int b = blockIdx.x;
+    const int NB = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = UB_THREADS / 32;
+    const int rows = min(128, M - b * 128);
     for (int w = threadIdx.x; w < NW; w += UB_THREADS) mask[w] = 0u;
+    if (threadIdx.x < rows) s_prow[threadIdx.x] = __ldg(perm + b * 128 + threadIdx.x);
     __syncthreads();
 
-    // OR the stored indices of the block's rows.  Warp per row, lanes over consecutive words (coalesced);
-    // when a tile's words fit a 32-word group (T/C <= 32) the count is taken from the owning lane by shuffle.
+    // warp per row, coalesced 16-byte reads of the whole packed row (measured faster than reading only the tiles'
+    // first sectors: the strided 32-byte reads do not save DRAM bursts)
     const int NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
-    const int rows = min(128, M - b * 128);
-    for (int r = warp; r < rows; r += nwarps) {
-        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
+    for (int r = warp; r < rows; r += NWP) {
+        const uint32_t* row = tw + static_cast<int64_t>(s_prow[r]) * RW;
         for_each_row_entry(row, RW, NT, WPT, cap, lane, [&](uint32_t w) {
             const uint32_t n = w & 0xFFFFu;
             atomicOr(&mask[n >> 5], 1u << (n & 31));
@@ -113,15 +212,15 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        int v = lane < nwarps ? wsum[lane] : 0;
-        int s = v;
+        int v = lane < NWP ? wsum[lane] : 0;
+        int sc = v;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const int u = __shfl_up_sync(0xffffffffu, s, off);
-            if (lane >= off) s += u;
+            const int u = __shfl_up_sync(0xffffffffu, sc, off);
+            if (lane >= off) sc += u;
         }
-        if (lane < nwarps) wsum[lane] = s - v;  // exclusive warp offsets
-        if (lane == nwarps - 1) wsum[nwarps] = s;  // total
+        if (lane < NWP) wsum[lane] = sc - v;  // exclusive warp offsets
+        if (lane == NWP - 1) wsum[NWP] = sc;  // total
     }
     __syncthreads();
     int run = wsum[warp] + incl - local;
@@ -130,7 +229,7 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
         run += __popc(mask[w]);
     }
     __syncthreads();
-    const int total = wsum[nwarps];
+    const int total = wsum[NWP];
     const int padded = max(64, (total + 63) & ~63);
 
     int32_t* ul = um.ulist + static_cast<int64_t>(b) * N;
@@ -151,6 +250,77 @@ __global__ void __launch_bounds__(UB_THREADS) union_build_kernel(const uint32_t*
         um.utot[b] = total;
     }
 
+    // the last CTA builds the UP work list from every block's ulen
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1) == NB - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        union_scan_body<UB_THREADS>(um, NB, up_group, wsum);
+    }
+}
+
+// Compact gate lists for the UP epilogue (instead of materialising G in H_c): warp per pi-ordered row i (8 per
+// CTA); the row's stored entries in ascending neuron order = ascending union position (lane per tile, warp prefix
+// of the tile counts); position = uwoff + popc(umask prefix); coff[i][c] = entries with position < 256 c, from
+// per-warp SMEM chunk counters.  Dynamic SMEM: 8 x (nchunk + 1) ints.
+__global__ void __launch_bounds__(256) union_gate_list_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
+                                                              int C, UnionMeta um, const int32_t* __restrict__ perm) {
+    extern __shared__ int32_t gl_smem[];
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NB = (M + 127) / 128;
+    if (i >= static_cast<int64_t>(NB) * 128) return;
+    const int b = static_cast<int>(i >> 7);
+    const int nch = um.nchunk;
+    int32_t* cc = gl_smem + warp * (nch + 1);
+    for (int c = lane; c <= nch; c += 32) cc[c] = 0;
+    __syncwarp();
+    const int NW = N >> 5, NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
+    const uint32_t* msk = um.umask + static_cast<int64_t>(b) * NW;
+    const int32_t* wof = um.uwoff + static_cast<int64_t>(b) * NW;
+    uint32_t* gl = um.glist + i * um.lmax;
+    auto emit = [&](uint32_t w, int idx) {
+        const int n = static_cast<int>(w & 0xFFFFu);
+        const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
+        gl[idx] = (static_cast<uint32_t>(j) << 16) | (w >> 16);
+        atomicAdd(&cc[j >> 8], 1);
+    };
+    if (i < M) {
+        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + i)) * RW;
+        // lane per tile (ascending): measured faster here than coalesced whole-row reads (the row's
+        // first-touch DRAM read happened in union_meta_kernel; these sector reads mostly hit L2)
+        int base = 0;
+        for (int t0 = 0; t0 < NT; t0 += 32) {
+            const int t = t0 + lane;
+            const int cnt = t < NT ? tile_count(row, WPT, cap, t) : 0;
+            int inc = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += v;
+            }
+            const int start = base + inc - cnt;
+            if (t < NT) for_each_tile_entry(row, NT, WPT, cap, t, [&](uint32_t w, int e) { emit(w, start + e); });
+            base += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    __syncwarp();
+    uint16_t* co = um.coff + i * (nch + 1);
+    int carry = 0;
+    for (int c0 = 0; c0 <= nch; c0 += 32) {
+        const int c = c0 + lane;
+        const int v = c <= nch ? cc[c] : 0;
+        int inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += u;
+        }
+        if (c <= nch) co[c] = static_cast<uint16_t>(carry + inc - v);
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
 }
 
 // G_b: the stored gate values in union coordinates, H_c[b*128 + r, j] (bf16), zero elsewhere; the up-GEMM
@@ -179,57 +349,6 @@ __global__ void __launch_bounds__(256) union_gate_scatter_kernel(const uint32_t*
     });
 }
 
-// Compact gate lists for the UP epilogue (instead of materialising G in H_c): warp per pi-ordered row i;
-// the row's stored entries in ascending neuron order = ascending union position; warp ballot/popc
-// compaction; then coff[i][c] = #entries with position < 256 c (lower bounds, lanes over chunks).
-__global__ void union_gate_list_kernel(const uint32_t* __restrict__ tw, int M, int N, int T, int C, UnionMeta um,
-                                       const int32_t* __restrict__ perm) {
-    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int NB = (M + 127) / 128;
-    if (i >= static_cast<int64_t>(NB) * 128) return;
-    const int b = static_cast<int>(i >> 7);
-    const int NW = N >> 5, NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
-    const uint32_t* msk = um.umask + static_cast<int64_t>(b) * NW;
-    const int32_t* wof = um.uwoff + static_cast<int64_t>(b) * NW;
-    uint32_t* gl = um.glist + i * um.lmax;
-    int base = 0;
-    if (i < M) {
-        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + i)) * RW;
-        // visit the row in word order; compact with ballot/popc in lane order (ascending)
-        for (int t0 = 0; t0 < NT; t0 += 32) {
-            const int t = t0 + lane;
-            const uint32_t* blk = row + static_cast<int64_t>(t) * WPT;
-            const int cnt = t < NT ? min(static_cast<int>(__ldg(blk)), cap) : 0;
-            int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            const int start = base + incl - cnt;
-            for (int e = 0; e < cnt; ++e) {
-                const uint32_t w = __ldg(blk + 1 + e);
-                const int n = static_cast<int>(w & 0xFFFFu);
-                const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));
-                gl[start + e] = (static_cast<uint32_t>(j) << 16) | (w >> 16);
-            }
-            base += __shfl_sync(0xffffffffu, incl, 31);
-        }
-    }
-    __syncwarp();
-    uint16_t* co = um.coff + i * (um.nchunk + 1);
-    for (int c = lane; c <= um.nchunk; c += 32) {
-        int lo = 0, hi = base;  // first entry with position >= 256 c
-        const uint32_t key = static_cast<uint32_t>(256 * c) << 16;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (gl[mid] < key) lo = mid + 1; else hi = mid;
-        }
-        co[c] = static_cast<uint16_t>(lo);
-    }
-}
-
 // Row permutation pi (Alg.2 iterates m in pi(0..M-1); descending-nnz order): within each
 // window of PERM_W consecutive rows (one 2048-token sequence), rows sorted by stored non-zeros
 // descending, ties by row index -> unique keys, deterministic.  Blocks of 128 never straddle windows.
@@ -249,34 +368,36 @@ __global__ void row_nnz_kernel(const uint32_t* __restrict__ tw, int M, int N, in
     if (lane == 0) nnz[gw] = s;
 }
 
-__global__ void __launch_bounds__(1024) union_perm_kernel(const int* __restrict__ nnz, int M, int32_t* __restrict__ perm) {
-    __shared__ unsigned long long keys[PERM_W];
+// pi by ranking (replaces a bitonic sort): row i of a window goes to position
+//   #{ j in window : nnz_j > nnz_i  or  (nnz_j == nnz_i and j < i) }
+// i.e. stable descending order of stored non-zeros.  Grid (windows, PERM_SPLIT); every CTA holds its window's
+// counts in SMEM (padding rows = -1, never counted) and ranks PERM_W / PERM_SPLIT rows (thread per row, four
+// keys per 16-byte SMEM read).  Block (0,0) also zeroes the completion counter of union_meta_kernel, which runs
+// after it on the same stream.
+constexpr int PERM_SPLIT = 16;
+static_assert(PERM_W == 2048, "rank keys pack the window index in 11 bits");
+__global__ void __launch_bounds__(PERM_W / PERM_SPLIT) union_rank_kernel(const int* __restrict__ nnz, int M,
+                                                                        int32_t* __restrict__ perm, int* done_ctr) {
+    // packed key (nnz << 11) | (2047 - j): key_j > key_i  <=>  nnz_j > nnz_i or (nnz_j == nnz_i and j < i)
+    // (stored non-zeros of a row <= N <= 65536 < 2^20); padding rows get -1 and are never counted
+    __shared__ __align__(16) int key[PERM_W];
     const int w0 = blockIdx.x * PERM_W;
     const int rows = min(PERM_W, M - w0);
-    for (int i = threadIdx.x; i < PERM_W; i += 1024) {
-        unsigned long long key = ~0ull;  // padding sorts last
-        if (i < rows)
-            key = (static_cast<unsigned long long>(0x7FFFFFFF - __ldg(nnz + w0 + i)) << 32) | static_cast<unsigned>(w0 + i);
-        keys[i] = key;
-    }
+    for (int i = threadIdx.x; i < PERM_W; i += blockDim.x)
+        key[i] = i < rows ? (__ldg(nnz + w0 + i) << 11) | (PERM_W - 1 - i) : -1;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *done_ctr = 0;
     __syncthreads();
-    for (int k = 2; k <= PERM_W; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < PERM_W; i += 1024) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const unsigned long long a = keys[i], c = keys[l];
-                    const bool up = (i & k) == 0;
-                    if ((a > c) == up) {
-                        keys[i] = c;
-                        keys[l] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
+    const int i = blockIdx.y * (PERM_W / PERM_SPLIT) + threadIdx.x;
+    if (i >= rows) return;
+    const int ki = key[i];
+    int rank = 0;
+    const int4* k4 = reinterpret_cast<const int4*>(key);
+#pragma unroll 8
+    for (int j4 = 0; j4 < PERM_W / 4; ++j4) {
+        const int4 v = k4[j4];
+        rank += (v.x > ki) + (v.y > ki) + (v.z > ki) + (v.w > ki);
     }
-    for (int i = threadIdx.x; i < rows; i += 1024) perm[w0 + i] = static_cast<int32_t>(keys[i] & 0xFFFFFFFFu);
+    perm[w0 + rank] = w0 + i;
 }
 
 // Xp[i, :] = X[perm[i], :]  (warp per row, 16-byte vectors)
@@ -288,63 +409,6 @@ __global__ void permute_rows_kernel(const uint4* __restrict__ X, const int32_t* 
     const uint4* src = X + static_cast<int64_t>(__ldg(perm + gw)) * K8;
     uint4* dst = Xp + gw * K8;
     for (int c = lane; c < K8; c += 32) dst[c] = __ldg(src + c);
-}
-
-// UP work list: for each group of UNION_GROUP blocks, chunk-major then block: tiles[] = (b << 8) | c.
-// One CTA; thread per group; chunk_off[0] = total tiles.
-__global__ void __launch_bounds__(1024) union_scan_kernel(UnionMeta um, int NB, int UNION_GROUP) {
-    __shared__ int wsum[33];
-    __shared__ int carry;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int NG = (NB + UNION_GROUP - 1) / UNION_GROUP;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < NG; base += 1024) {
-        const int g = base + threadIdx.x;
-        int tot = 0, maxc = 0;
-        if (g < NG) {
-            for (int b = g * UNION_GROUP; b < min(NB, (g + 1) * UNION_GROUP); ++b) {
-                const int c = (um.ulen[b] + 255) / 256;
-                tot += c;
-                maxc = max(maxc, c);
-            }
-        }
-        int s = tot;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int u = __shfl_up_sync(0xffffffffu, s, off);
-            if (lane >= off) s += u;
-        }
-        if (lane == 31) wsum[warp] = s;
-        __syncthreads();
-        if (warp == 0) {
-            int x = wsum[lane];
-            int y = x;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, y, off);
-                if (lane >= off) y += u;
-            }
-            wsum[lane] = y - x;
-            if (lane == 31) wsum[32] = y;
-        }
-        __syncthreads();
-        if (g < NG) {
-            int pos = carry + wsum[warp] + s - tot;
-            const int b0 = g * UNION_GROUP, b1 = min(NB, (g + 1) * UNION_GROUP);
-            for (int c = 0; c < maxc; ++c)
-                for (int b = b0; b < b1; ++b)
-                    if (c < (um.ulen[b] + 255) / 256) um.tiles[pos++] = (b << 8) | c;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) carry += wsum[32];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        um.chunk_off[0] = carry;
-        um.counters[0] = 0;
-        um.counters[1] = 0;
-    }
 }
 
 }  // namespace sffn

@@ -57,6 +57,8 @@ _SIGS = {
     "sffn_down": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _int, _vp]),
     "sffn_forward_nongated": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _int, _vp]),
     "sffn_forward_host_stage_bytes": (_sz, [_i64, _i64]),
+    "sffn_forward_host_chunks": (_i64, [_i64, _i64, _vp, _i64]),
+    "sffn_launch_count": (_i64, []),
     "sffn_forward_host": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _sz, _vp, _int,
                                  _i64, _vp]),
     "sffn_pack_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
@@ -192,6 +194,19 @@ def forward(x, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, o
                             _bf16(out, "out"), _p(workspace), workspace.numel() * workspace.element_size(),
                             _p(overflow), a, _stream(stream)), "sffn_forward")
     return out
+
+
+def launch_count() -> int:
+    """Kernels launched (or captured) by the library so far in this process."""
+    return int(lib().sffn_launch_count())
+
+
+def forward_host_chunks(M: int, chunk_rows: int = 4096) -> list:
+    """The row-chunk schedule of forward_host (host-side planner of the C library)."""
+    n = int(lib().sffn_forward_host_chunks(M, chunk_rows, None, 0))
+    buf = (ctypes.c_int64 * max(1, n))()
+    lib().sffn_forward_host_chunks(M, chunk_rows, ctypes.cast(buf, ctypes.c_void_p), n)
+    return [int(buf[i]) for i in range(n)]
 
 
 def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, stage=None,

@@ -80,3 +80,21 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 s = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in s and "from oracle" not in s and "oracle_" not in s, f
+
+
+@pytest.mark.parametrize("M,R", [(32768, 8192), (32768, 16384), (32768, 4096), (32768, 2048), (32845, 8192),
+                                 (5000, 8192), (100000, 8192), (4096, 8192), (12288, 4096), (1000, 256), (129, 128)])
+def test_host_chunk_plan(lib, M, R):
+    """sffn_forward_host's chunk schedule: covers M exactly, no chunk above the stage slot (chunk_rows rounded
+    to the rows actually staged), chunk starts on the 2048-row permutation windows when chunk_rows allows it,
+    and ramps (short first and last chunks) when there is room."""
+    from paper_2603_23198_b200 import sffn
+    v = sffn.forward_host_chunks(M, R)
+    rows = R if R < M else (M + 127) // 128 * 128
+    assert sum(v) == M and all(0 < s <= rows for s in v)
+    u = 2048 if R % 2048 == 0 else 128
+    starts = [sum(v[:i]) for i in range(len(v))]
+    assert all(s0 % u == 0 for s0 in starts)
+    if M >= 4 * R and R >= 4096:
+        assert v[0] < R and v[-1] < R and max(v) == R
+    assert sffn.forward_host_chunks(M, 100) == [] and sffn.forward_host_chunks(0, 128) == []

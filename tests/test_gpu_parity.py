@@ -343,14 +343,16 @@ def test_fp32_forward_gaussian(sffn):
 
 
 @pytest.mark.parametrize("algo", ALGOS)
-def test_forward_host_pipeline(sffn, algo):
-    """Host-buffer forward (chunked copy/compute overlap) == device forward, bit-identical (chunks are
-    multiples of the 2048-row permutation window)."""
-    cfg = synth.CONFIGS["1B"].replace(M=5000, K=256, N=1024, Kb=16, sparsity=0.97)
+@pytest.mark.parametrize("M,chunk", [(5000, 2048), (20000, 8192)])
+def test_forward_host_pipeline(sffn, algo, M, chunk):
+    """Host-buffer forward (chunked copy/compute overlap; 20000/8192 takes the ramped schedule
+    2048, 4096, 6144, 4096, 3616) == device forward, bit-identical (chunks start on the 2048-row
+    permutation windows)."""
+    cfg = synth.CONFIGS["1B"].replace(M=M, K=256, N=1024, Kb=16, sparsity=0.97)
     X, Wg, Wu, Wd = inputs(cfg)
     ref = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo)
     xh = torch.from_numpy(X.view(np.int16)).view(torch.bfloat16).pin_memory()
-    yh = sffn.forward_host(xh, to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo, chunk_rows=2048)
+    yh = sffn.forward_host(xh, to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo, chunk_rows=chunk)
     torch.cuda.synchronize()
     assert torch.equal(yh.view(torch.int16), ref.cpu().view(torch.int16))
 

@@ -20,3 +20,18 @@ def t(fn, n=15):
     return float(np.median(ts))
 print(os.environ.get("SFFN_LIB", "default"), f"pack {t(lambda: sffn.pack(X, Wg, cfg.T, cfg.C, out=tw)):.3f} ms",
       f"up_down {t(lambda: sffn.up_down(X, tw, Wu, Wd, cfg.T, cfg.C, out=Y, workspace=ws, algo='union')):.3f} ms", flush=True)
+if os.environ.get("KPROF"):
+    from torch.profiler import profile, ProfilerActivity
+    fws = torch.empty(sffn.workspace_bytes(cfg.M, cfg.K, cfg.N, cfg.T, cfg.C, "union"), dtype=torch.uint8, device="cuda")
+    fn = (lambda: sffn.forward(X, Wg, Wu, Wd, cfg.T, cfg.C, out=Y, workspace=fws, algo='union')) if os.environ.get("KPROF") == "fwd" else \
+         (lambda: sffn.up_down(X, tw, Wu, Wd, cfg.T, cfg.C, out=Y, workspace=ws, algo='union'))
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(5):
+            flush.fill_(1); fn()
+        torch.cuda.synchronize()
+    agg = {}
+    for e in prof.events():
+        if e.device_type.name == "CUDA" and "Fill" not in e.name:
+            agg.setdefault(e.name[:60], []).append(e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total)
+    for k, v in agg.items():
+        print(f"   {k:60s} {np.mean(v):9.1f} us x{len(v)}")
