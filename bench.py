@@ -312,12 +312,23 @@ def main():
     # see profiles/ launch lists); the gather kernel is one launch and longer than the gate GEMM
     dom = "gate_gemm_twell" if (algo_used == "union" or t_pack >= t_ud) else "fused_up_down"
     traffic = None
+    hbm = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
                 tr = json.load(f)
             traffic = tr.get(args.config, {}).get(dom)
+            # the metric's "HBM %": DRAM bytes of the step's kernels (one ncu --set full capture of the same
+            # forward, tools/prof_step.sh) over the measured step time, against the measured copy bandwidth
+            step_k = (["gate_gemm_twell", "union_rank", "permute_rows", "union_meta", "union_gate_list",
+                       "union_up_gemm", "union_down_gemm"] if algo_used == "union" else [])
+            tk = tr.get(args.config, {})
+            if world == 1 and step_k and all(k in tk for k in step_k):
+                b = float(sum(tk[k] for k in step_k))
+                hbm = {"step_dram_bytes": b, "achieved_gbs": b / (ms_per_step / 1e3) / 1e9,
+                       "peak_gbs": peaks["hbm_gbs"], "frac": b / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],
+                       "source": "ncu dram__bytes_read+write per kernel (profiles/ncu_traffic.json) / bench step time"}
         except (OSError, ValueError):
             traffic = None
     kd = kernels[dom]
@@ -384,6 +395,7 @@ def main():
                "tokens_per_s_per_gpu": value / world,
                "roofline": roofline, "kernels": kernels, "nnz_per_token": nnz_total / M,
                "overflow_tiles": n_ov, "dense": dense, "e2e": e2e, "cpu_baseline": cpu,
+               "hbm": hbm,
                "gpu_launches": args.steps * launches_per_step,
                "gpu_launches_per_step": launches_per_step,
                "algo": algo_used,
