@@ -294,13 +294,14 @@ def main():
     algo_used = args.algo if args.algo != "auto" else ("union" if Nl % 64 == 0 else "gather")
     if algo_used == "union":
         st = sffn.union_stats(ud_ws, M, K, Nl)
-        tc_flop = 4.0 * 128 * st["padded_sum"] * K  # the two union GEMMs
+        br = st["block_rows"]
+        tc_flop = 4.0 * br * st["padded_sum"] * K  # the two union GEMMs
         kernels["fused_up_down"] = {
             "ms": t_ud * 1e3, "launches": ud_launches, "algo": "union", "bound": "tensor",
             "achieved": tc_flop / t_ud / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": tc_flop / t_ud / 1e12 / peaks["bf16_tflops"],
-            "algorithmic": "4*128*sum_b |U_b| * K FLOP (union GEMMs)",
-            "union_frac_of_N": st["union_sum"] / ((M + 127) // 128) / Nl,
+            "algorithmic": f"4*{br}*sum_b |U_b| * K FLOP (union GEMMs, {br}-row union blocks)",
+            "union_frac_of_N": st["union_sum"] / ((M + br - 1) // br) / Nl, "union_block_rows": br,
             "useful_tflops": ud_flop / t_ud / 1e12}
     else:
         kernels["fused_up_down"] = {

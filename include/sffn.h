@@ -208,10 +208,13 @@ int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int6
 
 /*
  * sffn_union_stats — measurement helper for SFFN_ALGO_UNION: after sffn_up_down (workspace = its
- * workspace) synchronizes `stream` and returns the sum over 128-row blocks of the padded union sizes
- * (the tensor-core work is 4 * 128 * padded_sum * K FLOP), of the exact union sizes, and the number of
- * up-GEMM tiles.  Any output pointer may be NULL.
+ * workspace) synchronizes `stream` and returns the sum over union blocks (B = sffn_union_block_rows()
+ * token rows each) of the padded union sizes (the tensor-core work is 4 * B * padded_sum * K FLOP), of
+ * the exact union sizes, and the number of up-GEMM tiles.  Any output pointer may be NULL.
  */
+/* Token rows per union block of SFFN_ALGO_UNION in this process: 128 (single-CTA union GEMMs, M=128 tiles)
+ * or 256 (CTA-pair union GEMMs, cta_group::2 M=256 tiles; environment SFFN_UNION_PAIR=1 at first use). */
+int sffn_union_block_rows(void);
 int sffn_union_stats(const void* workspace, int64_t M, int64_t K, int64_t N, int64_t* padded_sum, int64_t* real_sum,
                      int64_t* up_tiles, void* stream);
 

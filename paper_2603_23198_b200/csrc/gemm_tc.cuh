@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 int mb, nb;
                 gemm_tile_coords<GROUP>(tile, num_m, args.num_n, mb, nb);
                 for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_wait_relaxed(&empty[stage], phase ^ 1);
                     if constexpr (PAIR == 2) {
                         // both CTAs' bytes complete on the leader's full barrier; only the leader expects them
                         const uint32_t fb = mapa_shared(&full[stage], 0);
@@ -202,8 +202,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
-                if (PAIR == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
-                else mbar_wait(&tempty[acc], acc_phase ^ 1);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
                 for (int kb = 0; kb < nk; ++kb) {
@@ -246,7 +245,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = PAIR == 2 ? mapa_shared(tempty, 0) : 0u;
         auto release_acc = [&](int a) {  // lane 0: this warp is done reading accumulator a
-            if (PAIR == 2) mbar_arrive_cluster(tempty_leader + 8u * static_cast<uint32_t>(a));
+            if (PAIR == 2) mbar_arrive_remote(tempty_leader + 8u * static_cast<uint32_t>(a));
             else mbar_arrive(&tempty[a]);
         };
         for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
@@ -332,11 +331,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     tmem_ld32(tb + 128 + ch * 32, u);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const float h0 = fmaxf(__uint_as_float(g[2 * j]), 0.0f) * __uint_as_float(u[2 * j]);
-                        const float h1 = fmaxf(__uint_as_float(g[2 * j + 1]), 0.0f) * __uint_as_float(u[2 * j + 1]);
-                        srow[ch * 16 + j] = pack_bf16x2(h0, h1);
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        g[j] = __float_as_uint(fmaxf(__uint_as_float(g[j]), 0.0f) * __uint_as_float(u[j]));
+                    st_row32_bf16(srow + ch * 16, g, lane);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -360,9 +357,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         uint32_t v[32];
                         tmem_ld32(tb + half * 128 + ch * 32, v);
                         tmem_wait_ld();
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            srow[ch * 16 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                        st_row32_bf16(srow + ch * 16, v, lane);
                     }
                     if (half == 1) {
                         tc_fence_before();

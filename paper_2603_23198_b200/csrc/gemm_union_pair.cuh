@@ -1,132 +1,65 @@
-// gemm_union.cuh — tensor-core sparse up/down over per-block neuron unions.
+// gemm_union_pair.cuh — CTA-pair (cluster of 2, tcgen05 cta_group::2) variant of the union up/down GEMMs
+// (gemm_union.cuh).  Union blocks are 256 token rows (UnionMeta::brows == 256): one pair tile is M = 256 rows
+// (128 per CTA, each CTA's A rows by TMA) x N = up to 256 union positions (UP) / 256 output columns (DOWN), and
+// each CTA gathers only HALF of the B operand (N/2 weight rows / columns), the leader issuing M=256 MMAs that read
+// both CTAs' shared memory.  Per SM this halves the gathered bytes per MMA FLOP and cuts the operand stream from
+// 48 KB to 32 KB per k-block (same MMA work), at the price of unions over 256 rows instead of 128.
 //
-// Eq.3 regrouped: for a block b of 128 token rows and U_b = union of their active neurons,
-//   H_b = G_b ⊙ (X_b · W_u[U_b]^T)        (UP kernel;  G_b = TwELL gate values scattered into U_b
-//                                           coordinates, 0 where (m, n) is not stored)
-//   Y_b = H_b · W_d[U_b, :]               (DOWN kernel)
-// Every term skipped relative to Eq.1 has h_g = 0, exactly as in Alg.2; the terms computed
-// with G = 0 add exact zeros.  Both kernels are persistent warp-specialized tcgen05 GEMMs like
-// gemm_tc.cuh; the dense A operand comes by TMA, the weight rows of U_b are gathered by four producer
-// warps with 16-byte cp.async.cg into the 128-byte-swizzled UMMA layout (TMA tile::gather4 measured
-// ~70 SM cycles per instruction on B200 — 8x too slow to feed the tensor cores, profiles/r01):
-//   UP   B operand: W_u[U_b[256c + r], k0:k0+64]       K-major
-//   DOWN B operand: W_d[U_b[k0 + r], 256j:256j+256]     MN-major (4 x 64-column atoms)
-// cp.async completion is signalled with cp.async.mbarrier.arrive.noinc on the stage's full barrier.
+// Cross-CTA protocol (both CTAs run identical role loops over the same tile sequence):
+//   tile ring   : the leader's warp 0 claims tiles (atomic counter) and publishes each into BOTH CTAs' SMEM ring
+//                 (st.shared::cluster + remote mbarrier arrive); every reader of both CTAs releases a slot by
+//                 arriving on the LEADER's sempty barrier.
+//   operands    : A tiles by TMA (.cta_group::2: completion on the leader's full barrier, expect_tx by the leader
+//                 for both CTAs); B rows by 16-byte cp.async into the CTA's own SMEM, completion on a CTA-local
+//                 gfull barrier (cp.async.mbarrier.arrive.noinc), relayed by one thread per CTA (warp 3) to the
+//                 leader's full barrier after a generic->async proxy fence.
+//   stage reuse : tcgen05.commit multicast arrives on both CTAs' empty barriers.
+//   accumulators: commit multicast on both CTAs' tfull; every epilogue warp of both CTAs arrives on the leader's
+//                 tempty.
 #pragma once
-#include "gemm_tc.cuh"
-#include "union.cuh"
+#include "gemm_union.cuh"
 
 namespace sffn {
 
-typedef unsigned short bf16_t;
-
-struct UnionArgs {
-    int M, K, N, T, C;
-    int NB;             // token blocks of 128
-    int NJ;             // DOWN: output column tiles of 256
-    int group;          // DOWN: token blocks per raster group
-    const uint32_t* tw;  // UP: packed TwELL [M, N/C]
-    UnionMeta um;
-    const bf16_t* wsrc;  // UP: W_u, DOWN: W_d, both [N, K]
-    const int32_t* perm;  // DOWN: output row of permuted row i
-    int* counter;         // dynamic tile scheduler (zeroed by union_scan_kernel)
-    bf16_t* Y;            // DOWN: output [M, K]
-};
-
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t col, int32_t r0,
-                                            int32_t r1, int32_t r2, int32_t r3) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-        : "memory");
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 
-#ifndef UG_WPOL
-#define UG_WPOL 0
+#ifndef UGP_RELAY_FENCE
+#define UGP_RELAY_FENCE 1
 #endif
-// gathered weight rows: optional L2 evict_last hint (UG_WPOL=1)
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-#if UG_WPOL
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
-                 "r"(src_bytes), "l"(pol)
-                 : "memory");
-#else
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+#ifndef UGP_FULL_CLUSTER_WAIT
+#define UGP_FULL_CLUSTER_WAIT 0
 #endif
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// 1-D bulk copy shared -> global (bulk-group completion)
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-// MN-major operand, 128-byte swizzle: 64-element MN atoms LBO apart, 8-row K groups SBO apart.
-__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
-    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-    d |= static_cast<uint64_t>(1) << 46;
-    d |= static_cast<uint64_t>(2) << 61;
-    return d;
-}
-
-__device__ __forceinline__ int upper_bound_i32(const int32_t* a, int n, int key) {  // first i with a[i] > key
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) <= key) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-// byte offset of element (r, c) in a [32 rows x 64 bf16] 128B-swizzled TMA box (1024-aligned base)
-__device__ __forceinline__ uint32_t sw128_off(int r, int c) {
-    return static_cast<uint32_t>(r * 128 + ((((c >> 3) ^ r) & 7) << 4) + ((c & 7) << 1));
-}
-
-constexpr int UG_STAGES = 4;
-constexpr int UG_GPRE = 8;  // UP epilogue: gate entries per row prefetched before the accumulator wait
-#ifndef FENCE_CPASYNC
-#define FENCE_CPASYNC 1
+#ifndef UGP_EXP
+#define UGP_EXP 0  // experiments only (wrong results): 1 = no B gathers, 2 = no epilogue work
 #endif
-#ifndef UG_NGW
-#define UG_NGW 8
-#endif
-constexpr int UG_GW = UG_NGW;                  // gather producer warps (8..8+UG_GW-1)
-constexpr int UG_THREADS = 256 + 32 * UG_GW;   // warps 0-7 as gemm_tc + gather producer warps
-constexpr int UG_GATHER = 32 * UG_GW;
-constexpr int UG_EWB = 8192;  // epilogue staging per warp
-constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 1024;
-constexpr int UG_RING = 8;       // tile-scheduler ring depth
-constexpr int UG_READERS = UG_GW + 5;  // gather warps + MMA thread + 4 epilogue warps
+constexpr int UGP_B_BYTES = GEMM_B_BYTES / 2;                 // this CTA's half of the B tile (16 KB)
+constexpr int UGP_STAGE = GEMM_A_BYTES + UGP_B_BYTES;         // 32 KB
+constexpr int UGP_STAGES = 6;
+constexpr int UGP_SMEM = 1024 + UGP_STAGES * UGP_STAGE + 4 * UG_EWB + 1024;
+constexpr int UGP_READERS = 2 * (UG_GW + 6);  // per CTA: gather warps + 4 epilogue + relay + (leader MMA | peer A producer)
+static_assert(UGP_SMEM <= GEMM_SMEM_LIMIT, "pair union GEMM shared memory");
 
 template <bool UP>
 __global__ void __launch_bounds__(UG_THREADS, 1)
-    union_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const __grid_constant__ CUtensorMap tmOut, const UnionArgs args) {
-    constexpr int S = UG_STAGES;
+    union_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmOut, const UnionArgs args) {
+    constexpr int S = UGP_STAGES;
+    constexpr int BM2 = 2 * GEMM_BM;  // rows per pair tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stA = smem;
     uint8_t* stB = smem + S * GEMM_A_BYTES;
-    uint8_t* epi = stB + S * GEMM_B_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * UG_EWB);
-    uint64_t* empty = full + S;
-    uint64_t* tfull = empty + S;
-    uint64_t* tempty = tfull + 2;
-    uint64_t* gbar = tempty + 2;  // [4] epilogue: G tile loaded
-    uint64_t* sfull = gbar + 4;   // [UG_RING] tile ring
-    uint64_t* sempty = sfull + UG_RING;
-    int* sched = reinterpret_cast<int*>(sempty + UG_RING);  // [UG_RING]
+    uint8_t* epi = stB + S * UGP_B_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * UG_EWB);  // [S] leader: A bytes + 2 relay arrivals
+    uint64_t* gfull = full + S;                                        // [S] local: cp.async completion
+    uint64_t* empty = gfull + S;                                       // [S]
+    uint64_t* tfull = empty + S;                                       // [2]
+    uint64_t* tempty = tfull + 2;                                      // [2] leader
+    uint64_t* sfull = tempty + 2;                                      // [UG_RING]
+    uint64_t* sempty = sfull + UG_RING;                                // [UG_RING] leader
+    int* sched = reinterpret_cast<int*>(sempty + UG_RING);             // [UG_RING]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched + UG_RING);
 
     const int warp = threadIdx.x >> 5;
@@ -135,54 +68,52 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     const int NB = args.NB;
     const int num_tiles = UP ? __ldg(args.um.chunk_off) : NB * args.NJ;
     const int nk_up = (args.K + GEMM_BK - 1) / GEMM_BK;
+    const uint32_t rank = cluster_ctarank();
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmA);
-        tma_prefetch(&tmB);
         tma_prefetch(&tmOut);
         for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 1 + UG_GATHER);
+            mbar_init(&full[i], 3);  // leader producer (expect_tx) + the two CTAs' relays
+            mbar_init(&gfull[i], UG_GATHER);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 8);
         }
-        for (int i = 0; i < 4; ++i) mbar_init(&gbar[i], 1);
         for (int i = 0; i < UG_RING; ++i) {
             mbar_init(&sfull[i], 1);
-            mbar_init(&sempty[i], UG_READERS);
+            mbar_init(&sempty[i], UGP_READERS);
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrive / store
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t full_leader = mapa_shared(full, 0);
+    const uint32_t sempty_leader = mapa_shared(sempty, 0);
+    const uint32_t tempty_leader = mapa_shared(tempty, 0);
 
-    // dynamic scheduler ring: warp 0 lane 0 claims tiles (atomicAdd) in the raster order and publishes them;
-    // every role reads the same sequence.  next_tile() returns -1 when the work is exhausted.
     auto next_tile = [&](int& ridx, uint32_t& rphase, bool arrive_lane) -> int {
-        mbar_wait(&sfull[ridx], rphase);
+        mbar_wait_cluster(&sfull[ridx], rphase);
         const int t = *reinterpret_cast<volatile int*>(&sched[ridx]);
-        if (arrive_lane) mbar_arrive(&sempty[ridx]);
+        if (arrive_lane) mbar_arrive_cluster(sempty_leader + 8u * static_cast<uint32_t>(ridx));
         if (++ridx == UG_RING) {
             ridx = 0;
             rphase ^= 1;
         }
         return t;
     };
-
-    // tile -> (b, c | j, rows/len)
     auto tile_info = [&](int tile, int& b, int& cj, int& len) {
         if (UP) {
             const int v = __ldg(args.um.tiles + tile);
             b = v >> 8;
             cj = v & 255;
-            len = min(256, __ldg(args.um.ulen + b) - 256 * cj);  // rows of this chunk (multiple of 64)
+            len = min(256, __ldg(args.um.ulen + b) - 256 * cj);
         } else {
-            // grouped raster: args.group blocks sweep all output column tiles together (L2 working set)
             const int G = args.group;
             const int per = G * args.NJ;
             const int grp = tile / per;
@@ -190,26 +121,36 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             const int in = tile - grp * per;
             b = grp * G + in % gb;
             cj = in / gb;
-            len = __ldg(args.um.ulen + b);  // reduction length (multiple of 64)
+            len = __ldg(args.um.ulen + b);
         }
     };
 
     if (warp == 0) {
-        // ------------------------------------------------------------ A operand by TMA (one thread)
+        // ------------------------------------------------------------ tile claims (leader) + A operand by TMA
         if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
             int widx = 0;
             uint32_t wphase = 0;
+            int ridx = 0;
+            uint32_t rphase = 0;
             for (;;) {
-                mbar_wait(&sempty[widx], wphase ^ 1);
-                int tile = atomicAdd(args.counter, 1);
-                if (tile >= num_tiles) tile = -1;
-                sched[widx] = tile;
-                mbar_arrive(&sfull[widx]);
-                if (++widx == UG_RING) {
-                    widx = 0;
-                    wphase ^= 1;
+                int tile;
+                if (rank == 0) {
+                    mbar_wait_cluster(&sempty[widx], wphase ^ 1);
+                    tile = atomicAdd(args.counter, 1);
+                    if (tile >= num_tiles) tile = -1;
+                    sched[widx] = tile;
+                    st_cluster_u32(mapa_shared(&sched[widx], 1), static_cast<uint32_t>(tile));
+                    mbar_arrive(&sfull[widx]);
+                    mbar_arrive_cluster(mapa_shared(&sfull[widx], 1));
+                    if (++widx == UG_RING) {
+                        widx = 0;
+                        wphase ^= 1;
+                    }
+                } else {
+                    tile = next_tile(ridx, rphase, true);
                 }
                 if (tile < 0) break;
                 int b, cj, len;
@@ -217,9 +158,33 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 const int nk = UP ? nk_up : len / GEMM_BK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES);
-                    tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
-                                UG_WPOL ? policy_evict_first() : policy_evict_last());
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * GEMM_A_BYTES);
+                    tma_load_2d_pair(stA + stage * GEMM_A_BYTES, &tmA, full_leader + 8u * static_cast<uint32_t>(stage),
+                                     kb * GEMM_BK, b * BM2 + static_cast<int>(rank) * GEMM_BM, pol);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ------------------------------------------------------------ relay: local gather completion -> leader
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int ridx = 0;
+            uint32_t rphase = 0;
+            for (;;) {
+                const int tile = next_tile(ridx, rphase, true);
+                if (tile < 0) break;
+                int b, cj, len;
+                tile_info(tile, b, cj, len);
+                const int nk = UP ? nk_up : len / GEMM_BK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait_relaxed(&gfull[stage], phase);  // per stage: no L1 invalidation
+                    if (UGP_RELAY_FENCE) fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+                    mbar_arrive_remote(full_leader + 8u * static_cast<uint32_t>(stage));
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -228,11 +193,9 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             }
         }
     } else if (warp >= 8) {
-        // ------------------------------------------------------------ B operand: gathered weight rows
-        // 8 consecutive lanes copy one 128-B row segment (16 B each), so every warp instruction moves whole
-        // 128-B lines: UP 4 rows x 128 B, DOWN one neuron row's 4 adjacent 64-column atoms (512 B).
-        const int gw = warp - 8;          // 0..UG_GW-1
-        const int c8 = lane & 7, sub = lane >> 3;
+        // ------------------------------------------------------------ B operand: this CTA's half, gathered
+        const int gw = warp - 8;
+        const int c8 = lane & 7;
         int stage = 0;
         uint32_t phase = 0;
         int ridx = 0;
@@ -244,57 +207,62 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             tile_info(tile, b, cj, len);
             const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
             if (UP) {
-                // pass i covers chunk rows 4 UG_GW i + 4 gw + sub
-                constexpr int NP = 64 / UG_GW;
+                // rows rr = 4 UG_GW i + 4 gw + sub of this CTA's half (half = len/2 chunk positions)
+                constexpr int NP = 128 / (4 * UG_GW);
+                const int sub = lane >> 3;
+                const int half = len >> 1;
+                const int p0 = 256 * cj + static_cast<int>(rank) * half;
                 int nidx[NP];
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
-                    const int r = 4 * UG_GW * i + 4 * gw + sub;
-                    nidx[i] = r < len ? __ldg(ul + 256 * cj + r) : -1;
+                    const int rr = 4 * UG_GW * i + 4 * gw + sub;
+                    nidx[i] = rr < half ? __ldg(ul + p0 + rr) : -1;
                 }
                 for (int kb = 0; kb < nk_up; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
-                    const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES);
+                    const uint32_t dst = smem_u32(stB + stage * UGP_B_BYTES);
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
-                        const int r = 4 * UG_GW * i + 4 * gw + sub;
-                        if (nidx[i] >= 0)
-                            cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
+                        const int rr = 4 * UG_GW * i + 4 * gw + sub;
+                        if (nidx[i] >= 0 && UGP_EXP != 1)
+                            cp_async16(dst + rr * 128 + ((c8 ^ (rr & 7)) << 4),
                                        args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * GEMM_BK + 8 * c8, 16);
                     }
-                    cp_async_arrive_noinc(&full[stage]);
+                    cp_async_arrive_noinc(&gfull[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
             } else {
-                // pass i covers k-block row r = UG_GW i + gw, MN atom a = sub (columns 256 cj + 64 a + 8 c8)
-                constexpr int NP = 64 / UG_GW;
+                // k-block row r = 16 i + 2 gw + rsub, MN atom a (columns 256 cj + 128 rank + 64 a + 8 c8)
+                constexpr int NP = 64 / (2 * UG_GW);
+                const int a = (lane >> 3) & 1, rsub = lane >> 4;
                 const int nk = len / GEMM_BK;
-                const int col = cj * 256 + sub * 64 + 8 * c8;
+                const int col = cj * 256 + static_cast<int>(rank) * 128 + a * 64 + 8 * c8;
                 const bool in = col < args.K;
                 // union indices two k-blocks ahead (an L2 round trip is about one k-block of MMA time)
                 int nidx[NP], n1[NP];
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
-                    nidx[i] = __ldg(ul + UG_GW * i + gw);
-                    n1[i] = __ldg(ul + (nk > 1 ? GEMM_BK : 0) + UG_GW * i + gw);
+                    nidx[i] = __ldg(ul + 2 * UG_GW * i + 2 * gw + rsub);
+                    n1[i] = __ldg(ul + (nk > 1 ? GEMM_BK : 0) + 2 * UG_GW * i + 2 * gw + rsub);
                 }
                 for (int kb = 0; kb < nk; ++kb) {
                     int nxt[NP];
                     const int kn = kb + 2 < nk ? kb + 2 : nk - 1;
 #pragma unroll
-                    for (int i = 0; i < NP; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + UG_GW * i + gw);
+                    for (int i = 0; i < NP; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + 2 * UG_GW * i + 2 * gw + rsub);
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
-                    const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES) + sub * 8192;
+                    const uint32_t dst = smem_u32(stB + stage * UGP_B_BYTES) + a * 8192;
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
-                        const int r = UG_GW * i + gw;
+                        const int r = 2 * UG_GW * i + 2 * gw + rsub;
+                        if (UGP_EXP != 1)
                         cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
                                    args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + (in ? col : 0), in ? 16 : 0);
                     }
-                    cp_async_arrive_noinc(&full[stage]);
+                    cp_async_arrive_noinc(&gfull[stage]);
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
                         nidx[i] = n1[i];
@@ -308,8 +276,8 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // ------------------------------------------------------------ MMA issuer (leader only)
+        if (lane == 0 && rank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -322,30 +290,28 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 int b, cj, len;
                 tile_info(tile, b, cj, len);
                 const int nk = UP ? nk_up : len / GEMM_BK;
-                const uint32_t idesc = UP ? umma_idesc_bf16(GEMM_BM, len) : (umma_idesc_bf16(GEMM_BM, 256) | (1u << 16));
+                const uint32_t idesc = UP ? umma_idesc_bf16(BM2, len) : (umma_idesc_bf16(BM2, 256) | (1u << 16));
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
                 for (int kb = 0; kb < nk; ++kb) {
-                    // relaxed per-stage wait (an acquire wait invalidates the SM's L1 every k-block, hurting the
-                    // gather warps' index loads); the cp.async data is complete when the stage's barrier flips
-                    mbar_wait_relaxed(&full[stage], phase);
-                    if (FENCE_CPASYNC) fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+                    if (UGP_FULL_CLUSTER_WAIT) mbar_wait_cluster(&full[stage], phase);
+                    else mbar_wait_relaxed(&full[stage], phase);  // per stage: no L1 invalidation
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
-                    const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);
+                    const uint32_t b0 = smem_u32(stB + stage * UGP_B_BYTES);
 #pragma unroll
                     for (int k = 0; k < GEMM_BK / 16; ++k) {
                         const uint64_t bd = UP ? umma_desc_sw128(b0 + k * 32) : umma_desc_sw128_mn(b0 + k * 2048, 8192, 1024);
-                        umma_f16(d, umma_desc_sw128(a0 + k * 32), bd, idesc, (kb | k) != 0);
+                        umma_f16_pair(d, umma_desc_sw128(a0 + k * 32), bd, idesc, (kb | k) != 0);
                     }
-                    umma_commit(&empty[stage]);
+                    umma_commit_pair(&empty[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                umma_commit_pair(&tfull[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -353,7 +319,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             }
         }
     } else if (warp >= 4) {
-        // ------------------------------------------------------------ epilogue
+        // ------------------------------------------------------------ epilogue (both CTAs, own 128 rows)
         const int ew = warp - 4;
         uint8_t* stg = epi + ew * UG_EWB;
         int acc = 0;
@@ -365,7 +331,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             if (tile < 0) break;
             int b, cj, len;
             tile_info(tile, b, cj, len);
-            const int row0 = b * GEMM_BM + ew * 32;
+            const int row0 = b * BM2 + static_cast<int>(rank) * GEMM_BM + ew * 32;
             // UP: this row's gate entries of the chunk, loaded before waiting for the accumulator
             int e0 = 0, e1 = 0;
             const uint32_t* gl = nullptr;
@@ -382,14 +348,17 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
-            if constexpr (UP) {
-                // staging <- this row's gate values for the chunk (from the compact gate list, zero elsewhere),
-                // then H = G * (X W_u^T) in place, then TMA store of the H_c tile.
+            const uint32_t release = tempty_leader + 8u * static_cast<uint32_t>(acc);
+            if (UGP_EXP == 2) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(release);
+            } else if constexpr (UP) {
                 const int p0 = 256 * cj;
 #pragma unroll 1
                 for (int h = 0; h < 2 && 128 * h < len; ++h) {
                     const int nbox = min(2, (len - 128 * h) / 64);
-                    if (lane == 0) bulk_wait_read0();  // previous TMA store has finished reading the staging buffer
+                    if (lane == 0) bulk_wait_read0();
                     __syncwarp();
 #pragma unroll
                     for (int q = 0; q < 2; ++q)
@@ -414,7 +383,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                         tmem_wait_ld();
 #pragma unroll
                         for (int p = 0; p < 16; ++p) {
-                            const int c = 32 * q32 + 2 * p;  // column within the half
+                            const int c = 32 * q32 + 2 * p;
                             uint32_t* sp = reinterpret_cast<uint32_t*>(stg + (c >> 6) * 4096 + sw128_off(lane, c & 63));
                             const uint32_t gg = *sp;
                             if (gg) {
@@ -428,7 +397,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     if (h == 1 || 128 * (h + 1) >= len) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                        if (lane == 0) mbar_arrive_remote(release);
                     }
                     fence_async_smem();
                     __syncwarp();
@@ -438,15 +407,12 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     }
                 }
             } else {
-                // DOWN: rows were processed in pi order; row i of the tile goes to Y[perm[row0 + i]].
-                // Stage 32 rows x 128 columns (bf16) per half in SMEM, then one 256-byte bulk copy per row.
                 uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
-                const int ncols = min(128, args.K - cj * 256);  // per half, K tail
 #pragma unroll 1
                 for (int half = 0; half < 2; ++half) {
                     const int c0 = cj * 256 + half * 128;
                     const int nc = min(128, args.K - c0);
-                    bulk_wait_read0();  // every lane's own bulk copy (per-thread bulk group) has read its row
+                    bulk_wait_read0();
                     __syncwarp();
 #pragma unroll 1
                     for (int ch = 0; ch < 4; ++ch) {
@@ -458,7 +424,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     if (half == 1) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                        if (lane == 0) mbar_arrive_remote(release);
                     }
                     fence_async_smem();
                     __syncwarp();
@@ -471,7 +437,6 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                         bulk_commit();
                     }
                 }
-                (void)ncols;
             }
             if (++acc == 2) {
                 acc = 0;
@@ -481,16 +446,16 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         if (UP) {
             if (lane == 0) bulk_wait0();
         } else {
-            bulk_wait0();  // per-thread bulk groups of the row copies
+            bulk_wait0();
         }
     }
 
     __syncwarp();
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();  // remote arrivals / stores and the leader's MMAs into the peer's TMEM are finished
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, 512);
+        tmem_dealloc_pair(tmem_base, 512);
     }
 }
 

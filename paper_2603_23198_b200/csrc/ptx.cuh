@@ -33,7 +33,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     do {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// Relaxed wait (no acquire): for producers waiting on a stage's `empty` barrier before overwriting it with
+// cp.async / TMA.  The default (.acquire) wait compiles to TRYWAIT + CCTL.IVALL (an L1 invalidation after
+// every successful wait), which made the gather warps' __ldg index loads miss L1 once per k-block.
+__device__ __forceinline__ void mbar_wait_relaxed(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.relaxed.cta.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
             : "r"(a), "r"(parity)
@@ -158,9 +174,20 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
     return r;
 }
+// Arrive on an mbarrier given by its shared::cluster address (possibly in the peer CTA), .release at CLUSTER
+// scope: orders this thread's prior shared::cluster stores (e.g. a tile index written into the peer's SMEM)
+// before the arrival.  Compiles to MEMBAR.ALL.GPU + ERRBAR: use only where cross-CTA data is published.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Remote arrive with the default semantics (.release at CTA scope, as CUTLASS's ClusterBarrier::arrive): for
+// pure signalling (operand stage complete, accumulator drained).  The .release.cluster form above throttled the
+// pair union GEMMs' per-stage relays ~2.5x (a GPU-scope membar per arrival).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Wait with .acquire at cluster scope (pairs with mbar_arrive_cluster: the published data is visible after it).
+// Adds an L1 invalidation (CCTL.IVALL) after the wait: not for per-stage waits.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     uint32_t done;
@@ -216,6 +243,28 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// 32 fp32 accumulator columns of one row (tcgen05.ld 32x32b: thread = row) -> 32 bf16 (64 bytes) at `dst` in a
+// row-contiguous SMEM staging buffer whose rows are 256 B apart (lane = row).  Four 16-byte stores, the chunk
+// order rotated by lane: 2-way bank conflicts instead of the 32-way of per-word stores at a 256-byte row stride.
+__device__ __forceinline__ void st_row32_bf16(uint32_t* dst, const uint32_t (&v)[32], int lane) {
+    uint4 c[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        c[q] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1])),
+                          pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                          pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                          pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int qq = (q + lane) & 3;
+        uint4 x = c[0];
+        if (qq == 1) x = c[1];
+        if (qq == 2) x = c[2];
+        if (qq == 3) x = c[3];
+        *reinterpret_cast<uint4*>(dst + 4 * qq) = x;
+    }
 }
 
 }  // namespace sffn

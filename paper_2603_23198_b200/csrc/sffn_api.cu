@@ -15,6 +15,7 @@
 #include "gemm_tc.cuh"
 #include "fp32_path.cuh"
 #include "gemm_union.cuh"
+#include "gemm_union_pair.cuh"
 #include "hybrid.cuh"
 #include "updown.cuh"
 
@@ -225,11 +226,18 @@ struct UnionWs {
     int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, glist, coff, total;
     int lmax, nchunk;
 };
+// Token rows per union block: 128 (single-CTA union GEMMs) or 256 (CTA-pair union GEMMs, SFFN_UNION_PAIR=1).
+int union_brows() {
+    static const int br = env_flag("SFFN_UNION_PAIR", false) ? 256 : 128;
+    return br;
+}
+
 UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8) {
-    const int64_t NB = (M + 127) / 128;
+    const int64_t BR = union_brows();
+    const int64_t NB = (M + BR - 1) / BR;
     UnionWs w{};
     int64_t o = 0;
-    w.hc = o;    o = align1k(o + NB * 128 * N * 2);
+    w.hc = o;    o = align1k(o + NB * BR * N * 2);
     w.ulist = o; o = align1k(o + NB * N * 4);
     w.ulen = o;  o = align1k(o + NB * 4);
     w.utot = o;  o = align1k(o + NB * 4);
@@ -243,8 +251,8 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8)
     w.nnz = o;   o = align1k(o + M * 4);
     w.lmax = static_cast<int>((N / T) * (T / C - 1));  // most stored entries a row can have
     w.nchunk = static_cast<int>((N + 255) / 256);
-    w.glist = o; o = align1k(o + NB * 128 * static_cast<int64_t>(w.lmax) * 4);
-    w.coff = o;  o = align1k(o + NB * 128 * static_cast<int64_t>(w.nchunk + 1) * 2);
+    w.glist = o; o = align1k(o + NB * BR * static_cast<int64_t>(w.lmax) * 4);
+    w.coff = o;  o = align1k(o + NB * BR * static_cast<int64_t>(w.nchunk + 1) * 2);
     w.total = o;
     return w;
 }
@@ -270,7 +278,8 @@ int* union_nnz_ptr(void* ws, int64_t M, int64_t N, int64_t K, int T, int C) {
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true,
                       bool nnz_ready = false) {
-    const int64_t NB = (M + 127) / 128;
+    const int BR = union_brows();
+    const int64_t NB = (M + BR - 1) / BR;
     UnionWs L = union_ws_layout(M, N, K, T, C);
     uint8_t* base = static_cast<uint8_t*>(ws);
     UnionMeta um;
@@ -286,6 +295,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     um.coff = reinterpret_cast<uint16_t*>(base + L.coff);
     um.lmax = L.lmax;
     um.nchunk = L.nchunk;
+    um.brows = BR;
     void* hc = base + L.hc;
     int32_t* perm = reinterpret_cast<int32_t*>(base + L.perm);
     void* xp = base + L.xp;
@@ -311,12 +321,12 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         tw, (int)M, (int)N, T, C, um, perm, done_ctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP)); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     if (gated) {
-        { union_gate_list_kernel<<<static_cast<unsigned>(NB * 128 * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
+        { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
             tw, (int)M, (int)N, T, C, um, perm); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
     if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)
-        { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (128 / GS_ROWS)), 256, 0, st>>>(
+        { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (BR / GS_ROWS)), 256, 0, st>>>(
             tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
@@ -325,8 +335,8 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M > 0 ? M : 1, GEMM_BK, GEMM_BM,
                  CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&thc_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * 128, GEMM_BK, GEMM_BM,
+        !tmap_2d(&thc_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * BR, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * BR, GEMM_BK, GEMM_BM,
                  CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wd, K, N, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, K, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
@@ -355,16 +365,49 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         attr = cudaFuncSetAttribute(union_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UG_SMEM);
         if (attr == cudaSuccess)
             attr = cudaFuncSetAttribute(union_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UG_SMEM);
+        if (attr == cudaSuccess)
+            attr = cudaFuncSetAttribute(union_gemm_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        UGP_SMEM);
+        if (attr == cudaSuccess)
+            attr = cudaFuncSetAttribute(union_gemm_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        UGP_SMEM);
     });
     if (attr != cudaSuccess) return SFFN_ERR_CUDA;
     const int sms = env_int("SFFN_UNION_GRID", dev_info().sms);  // tuning override (default: all SMs)
+    const int64_t dtiles = NB * ua.NJ;
+    if (BR == 256) {
+        // CTA pairs: clusters of two, every role loop runs the same tile sequence in both CTAs
+        auto launch_pair = [&](auto kern, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o,
+                               const UnionArgs& args, int64_t max_tiles) -> int {
+            const int64_t pairs = std::min<int64_t>(max_tiles, sms / 2);
+            if (pairs <= 0) return SFFN_OK;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+            cfg.blockDim = dim3(UG_THREADS);
+            cfg.dynamicSmemBytes = UGP_SMEM;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, kern, a, b, o, args) != cudaSuccess) return SFFN_ERR_CUDA;
+            note_launch();
+            return SFFN_OK;
+        };
+        int r = SFFN_OK;
+        if (gated && (r = launch_pair(union_gemm_pair_kernel<true>, tx, twu, thc_st, ua, sms)) != SFFN_OK) return r;
+        if ((r = launch_pair(union_gemm_pair_kernel<false>, thc_ld, twd, ty, ud, dtiles)) != SFFN_OK) return r;
+        return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+    }
     if (gated) {
         // UP: the number of (block, chunk) tiles is only known on the device; persistent grid.  For the
         // non-gated variant H_c already holds h = relu(x W_u) (the scattered TwELL values): no UP GEMM.
         { union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
-    const int64_t dtiles = NB * ua.NJ;
     const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
     { union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
@@ -889,10 +932,12 @@ int sffn_twell_to_hybrid(const uint32_t* twell, int64_t M, int64_t N, int T, int
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
+int sffn_union_block_rows(void) { return union_brows(); }
+
 int sffn_union_stats(const void* workspace, int64_t M, int64_t K, int64_t N, int64_t* padded_sum, int64_t* real_sum,
                      int64_t* up_tiles, void* stream) {
     if (!workspace || M <= 0 || N <= 0 || K <= 0) return SFFN_ERR_INVALID_ARG;
-    const int64_t NB = (M + 127) / 128;
+    const int64_t NB = (M + union_brows() - 1) / union_brows();
     UnionWs L = union_ws_layout(M, N, K);
     const uint8_t* base = static_cast<const uint8_t*>(workspace);
     int32_t* h = static_cast<int32_t*>(std::malloc(static_cast<size_t>(2 * NB + 1) * 4));

@@ -27,6 +27,7 @@ struct UnionMeta {
     uint32_t* glist;     // [NB*128, lmax] per (pi-ordered) row: (union position << 16) | bf16 gate, ascending
     uint16_t* coff;      // [NB*128, nchunk + 1] per row: entries before union chunk c (256 positions per chunk)
     int lmax, nchunk;
+    int brows;           // token rows per union block: 128 (one tcgen05 M tile) or 256 (a CTA pair's M=256 tile)
 };
 
 constexpr int UNION_GROUP_UP = 8;    // token blocks whose up-GEMM tiles run together (L2 working set)
@@ -177,13 +178,14 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
     int32_t* woff = reinterpret_cast<int32_t*>(ub_smem + NW);  // [NW]
     int32_t* wsum = woff + NW;                                 // [NWP + 1]
     __shared__ int s_last;
-    __shared__ int s_prow[128];
+    __shared__ int s_prow[256];
     const int b = blockIdx.x;
     const int NB = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rows = min(128, M - b * 128);
+    const int BR = um.brows;
+    const int rows = min(BR, M - b * BR);
     for (int w = threadIdx.x; w < NW; w += UB_THREADS) mask[w] = 0u;
-    if (threadIdx.x < rows) s_prow[threadIdx.x] = __ldg(perm + b * 128 + threadIdx.x);
+    for (int r = threadIdx.x; r < rows; r += UB_THREADS) s_prow[r] = __ldg(perm + static_cast<int64_t>(b) * BR + r);
     __syncthreads();
 
     // warp per row, coalesced 16-byte reads of the whole packed row (measured faster than reading only the tiles'
@@ -270,9 +272,10 @@ __global__ void __launch_bounds__(256) union_gate_list_kernel(const uint32_t* __
     extern __shared__ int32_t gl_smem[];
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int NB = (M + 127) / 128;
-    if (i >= static_cast<int64_t>(NB) * 128) return;
-    const int b = static_cast<int>(i >> 7);
+    const int BR = um.brows;
+    const int NB = (M + BR - 1) / BR;
+    if (i >= static_cast<int64_t>(NB) * BR) return;
+    const int b = static_cast<int>(i / BR);
     const int nch = um.nchunk;
     int32_t* cc = gl_smem + warp * (nch + 1);
     for (int c = lane; c <= nch; c += 32) cc[c] = 0;
@@ -329,19 +332,20 @@ constexpr int GS_ROWS = 8;
 __global__ void __launch_bounds__(256) union_gate_scatter_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
                                                                  int C, UnionMeta um, uint16_t* __restrict__ hc,
                                                                  const int32_t* __restrict__ perm) {
-    const int b = blockIdx.x / (128 / GS_ROWS);
-    const int r0 = (blockIdx.x % (128 / GS_ROWS)) * GS_ROWS;
+    const int BR = um.brows;
+    const int b = blockIdx.x / (BR / GS_ROWS);
+    const int r0 = (blockIdx.x % (BR / GS_ROWS)) * GS_ROWS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp w handles row r0 + w
     const int NW = N >> 5, NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
     const int padded = __ldg(um.ulen + b);
     const uint32_t* msk = um.umask + static_cast<int64_t>(b) * NW;
     const int32_t* wof = um.uwoff + static_cast<int64_t>(b) * NW;
     const int r = r0 + warp;
-    uint16_t* hrow = hc + (static_cast<int64_t>(b) * 128 + r) * N;
+    uint16_t* hrow = hc + (static_cast<int64_t>(b) * BR + r) * N;
     for (int c = lane; c < padded / 8; c += 32) *reinterpret_cast<uint4*>(hrow + 8 * c) = make_uint4(0, 0, 0, 0);
     __syncwarp();
-    if (b * 128 + r >= M) return;
-    const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + b * 128 + r)) * RW;
+    if (static_cast<int64_t>(b) * BR + r >= M) return;
+    const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + static_cast<int64_t>(b) * BR + r)) * RW;
     for_each_row_entry(row, RW, NT, WPT, cap, lane, [&](uint32_t w) {
         const int n = static_cast<int>(w & 0xFFFFu);
         const int j = __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));

@@ -59,6 +59,7 @@ _SIGS = {
     "sffn_forward_host_stage_bytes": (_sz, [_i64, _i64]),
     "sffn_forward_host_chunks": (_i64, [_i64, _i64, _vp, _i64]),
     "sffn_launch_count": (_i64, []),
+    "sffn_union_block_rows": (_int, []),
     "sffn_forward_host": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _sz, _vp, _int,
                                  _i64, _vp]),
     "sffn_pack_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
@@ -331,7 +332,8 @@ def union_stats(up_down_workspace: torch.Tensor, M: int, K: int, N: int, stream=
     a, b, t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     _chk(lib().sffn_union_stats(_p(up_down_workspace), M, K, N, ctypes.byref(a), ctypes.byref(b), ctypes.byref(t),
                                 _stream(stream)), "sffn_union_stats")
-    return {"padded_sum": a.value, "union_sum": b.value, "up_tiles": t.value}
+    return {"padded_sum": a.value, "union_sum": b.value, "up_tiles": t.value,
+            "block_rows": int(lib().sffn_union_block_rows())}
 
 
 def overflow_check(overflow: torch.Tensor, stream=None) -> int:
