@@ -407,13 +407,17 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     }
                 }
             } else {
+                // DOWN: rows were processed in pi order; row i of the tile goes to Y[perm[row0 + i]].  Stage
+                // 32 rows x 128 columns (bf16) per half in SMEM (conflict-free rotated 16-byte stores), then the
+                // warp writes two rows per instruction with coalesced 16-byte global stores (LSU, not per-row
+                // bulk copies: those were 256 small TMA requests per tile competing with the A-tile loads).
                 uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
+                const int prow_l = row0 + lane;
+                const int64_t yrow_l = prow_l < args.M ? static_cast<int64_t>(__ldg(args.perm + prow_l)) : -1;
 #pragma unroll 1
                 for (int half = 0; half < 2; ++half) {
                     const int c0 = cj * 256 + half * 128;
                     const int nc = min(128, args.K - c0);
-                    bulk_wait_read0();
-                    __syncwarp();
 #pragma unroll 1
                     for (int ch = 0; ch < 4; ++ch) {
                         uint32_t v[32];
@@ -426,16 +430,17 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                         __syncwarp();
                         if (lane == 0) mbar_arrive_remote(release);
                     }
-                    fence_async_smem();
                     __syncwarp();
-                    if (nc > 0) {
-                        const int prow = row0 + lane;
-                        if (prow < args.M) {
-                            bf16_t* dst = args.Y + static_cast<int64_t>(__ldg(args.perm + prow)) * args.K + c0;
-                            bulk_s2g(dst, stg + lane * 256, static_cast<uint32_t>(nc) * 2);
-                        }
-                        bulk_commit();
+                    const int chunk = lane & 15;
+#pragma unroll 4
+                    for (int it = 0; it < 16; ++it) {
+                        const int r = 2 * it + (lane >> 4);
+                        const int64_t yrow = __shfl_sync(0xffffffffu, yrow_l, r);
+                        const uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + chunk * 16);
+                        if (yrow >= 0 && chunk * 8 < nc)
+                            *reinterpret_cast<uint4*>(args.Y + yrow * args.K + c0 + chunk * 8) = val;
                     }
+                    __syncwarp();  // staging rows read before the next half overwrites them
                 }
             }
             if (++acc == 2) {
@@ -445,8 +450,6 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         }
         if (UP) {
             if (lane == 0) bulk_wait0();
-        } else {
-            bulk_wait0();
         }
     }
 
