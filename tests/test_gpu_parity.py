@@ -4,6 +4,8 @@ Bars (north_star): TwELL counts / indices / values bit-exact (on dyadic-grid inp
 fp32 accumulation is exact), Y within relative Frobenius 1e-2 (bf16 inputs,
 fp32 accumulation, bf16 output).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -505,3 +507,22 @@ def test_twell_to_hybrid(sffn):
         assert dmap[s] == m and np.array_equal(dense[s], H[m])
     g = h["l0l1"].cpu().numpy()
     assert abs(g[0] - l0) < 1e-9 * l0 and abs(g[1] - l1) < 1e-5 * abs(l1)
+
+
+# ----------------------------------------------------------------- CTA-pair union GEMMs (SFFN_UNION_PAIR=1)
+@pytest.mark.gpu
+def test_union_pair_mode(sffn):
+    """The CTA-pair union GEMMs (cta_group::2, 256-row unions) are chosen once per process from the environment:
+    re-run the union parity tests in a child process with SFFN_UNION_PAIR=1 (same oracle, same tolerances)."""
+    if os.environ.get("SFFN_UNION_PAIR") == "1":
+        assert sffn.sffn.lib().sffn_union_block_rows() == 256
+        pytest.skip("already running in pair mode")
+    import subprocess
+    import sys
+    env = dict(os.environ, SFFN_UNION_PAIR="1")
+    sel = ("union and (up_down_vs_oracle or union_tiles or dense_rows or forward_vs_oracle or nongated or "
+           "70b or forward_host or ragged or overflow or down_from) or test_union_pair_mode")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-m", "gpu", "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", sel], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
