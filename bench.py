@@ -162,6 +162,9 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunks", type=int, default=4, help="M chunks overlapping compute and all-reduce (N>1)")
+    ap.add_argument("--allreduce", choices=["nccl", "sym"], default="nccl",
+                    help="N>1: NCCL all-reduce (chunked overlap) or the library's symmetric-memory reduction kernel "
+                         "(NEXT-3: NVLS multimem / P2P over an NCCL symmetric window; falls back to nccl if unsupported)")
     ap.add_argument("--algo", default="auto", choices=["auto", "gather", "union"], help="fused up/down algorithm")
     ap.add_argument("--e2e-chunk", type=int, default=4096, help="rows per chunk of the host-buffer pipeline")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
@@ -208,13 +211,21 @@ def main():
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     comm = sffn.Comm(rank, world, local) if world > 1 else None
+    allreduce = "none"
+    if comm is not None:
+        allreduce = "nccl"
+        if args.allreduce == "sym" and comm.symmetric_init(M, K):
+            allreduce = "sym-nvls" if comm.symmetric_info()["multimem"] else "sym-p2p"
 
     def step():
         if comm is None:
             sffn.forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
         else:
-            comm.sharded_forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo,
-                                 n_chunks=args.chunks)
+            if allreduce.startswith("sym"):
+                comm.sharded_forward_sym(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
+            else:
+                comm.sharded_forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo,
+                                     n_chunks=args.chunks)
 
     def barrier():
         if world > 1:
@@ -390,7 +401,7 @@ def main():
                "data": "synthetic (seeded dyadic-grid generator: 99% sparsity, lognormal per-token nnz, "
                        "30% dead neurons)",
                "config": {"workload": cfg.name, "M": M, "K": K, "N": N, "T": T, "C": C, "sparsity": cfg.sparsity,
-                          "parallelism": f"hidden-dim x{world}" if world > 1 else "single",
+                          "parallelism": f"hidden-dim x{world}" if world > 1 else "single", "allreduce": allreduce,
                           "l2": "flushed (512 MiB write) between timed steps", "seed": cfg.seed,
                           "launch": "cuda_graph" if graph is not None else "eager"},
                "tokens_per_s_per_gpu": value / world,

@@ -271,6 +271,35 @@ int sffn_sharded_forward(sffn_comm* comm, const void* X, const void* Wg_s, const
 /* Plain in-place all-reduce (sum) of a bf16 buffer on the communicator (used by tests). */
 int sffn_allreduce_bf16(sffn_comm* comm, void* buf, int64_t count, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-3: symmetric-memory all-reduce
+ * The NCCL all-reduce above launches NCCL's kernels.  The symmetric path replaces it with the library's
+ * own reduction kernel over peer memory (SURVEY §8(e) "B200-native upgrade", §8(f) NEXT-3):
+ *   - sffn_comm_symmetric_init (collective: every rank calls it with the same arguments) allocates one
+ *     buffer of max_rows x K bf16 with ncclMemAlloc, registers it as a symmetric window
+ *     (ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC) and creates an NCCL device communicator with
+ *     SYM_CTAS load/store-accessible (LSA) barriers and, when NCCL can build one (NVSwitch, >= 2 ranks),
+ *     a multicast (NVLS) object.  Returns SFFN_ERR_UNSUPPORTED when the platform cannot (the NCCL path
+ *     stays available); once per communicator; freed by sffn_comm_destroy.
+ *   - sffn_sharded_forward_sym: sffn_forward of the local shard whose DOWN epilogue writes the partial Y
+ *     straight into the window, then ONE launch of the library's reduction kernel: LSA barrier; rank r
+ *     reduces its 1/G slice of 16-byte chunks — multimem.ld_reduce.add.acc::f32 (the switch sums the G
+ *     copies in fp32) + multimem.st (the switch writes the sum into every rank's window) with NVLS, else
+ *     P2P loads of the slice from every peer window, fp32 sum, P2P stores into every window; LSA barrier;
+ *     local copy window -> Y.  Y [M, K] bf16 (caller-owned device memory), M <= max_rows, same K.
+ *     Sum order: fp32 over ranks, one rounding to bf16 (the NCCL bf16 ring rounds per hop).
+ *   - sffn_allreduce_sym_bf16: the reduction alone on `rows` x K bf16 (src copied into the window first
+ *     unless src is NULL, i.e. already there); result in Y.
+ * Errors: SFFN_ERR_UNSUPPORTED if symmetric_init has not succeeded; SFFN_ERR_SHAPE if M > max_rows or K
+ * differs; all enqueued on `stream`, no host synchronization.
+ */
+int sffn_comm_symmetric_init(sffn_comm* comm, int64_t max_rows, int64_t K);
+/* multimem = 1 when the NVLS (multicast) reduction is used, 0 for P2P loads / stores. */
+int sffn_comm_symmetric_info(const sffn_comm* comm, int* multimem, int64_t* max_rows, int64_t* K);
+int sffn_allreduce_sym_bf16(sffn_comm* comm, const void* src, void* Y, int64_t rows, int64_t K, void* stream);
+int sffn_sharded_forward_sym(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
+                             int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
+                             size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -3,6 +3,9 @@
 // of chunk i runs on an internal communication stream while chunk i+1 computes (event-ordered).
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>  // NCCL 2.28 device API: symmetric windows, LSA peer pointers, multimem, LSA barriers
+
+#include <cuda_bf16.h>
 
 #include <cstring>
 #include <vector>
@@ -14,7 +17,74 @@ struct sffn_comm {
     int nranks = 0, rank = 0, device = 0;
     cudaStream_t comm_stream = nullptr;
     std::vector<cudaEvent_t> events;  // per-chunk "compute done" events (+1 "comm done")
+    // NEXT-3 symmetric path (sffn_comm_symmetric_init): one registered window holding this rank's partial Y
+    void* sym_buf = nullptr;
+    size_t sym_bytes = 0;
+    int64_t sym_rows = 0, sym_K = 0;
+    ncclWindow_t win = nullptr;
+    ncclDevComm dev{};
+    bool has_dev = false, multimem = false;
 };
+
+// ---------------------------------------------------------------- NEXT-3: symmetric-memory all-reduce kernel
+// One launch after the DOWN GEMM (whose epilogue wrote this rank's partial Y straight into the registered
+// window).  Every rank owns 1/G of the 16-byte chunks of Y:
+//   LSA barrier (all ranks' partials are in their windows)
+//   multimem path (NVSwitch NVLS): multimem.ld_reduce.add.acc::f32 of the chunk through the multicast address
+//     (the switch reads the G copies and returns their fp32-accumulated bf16 sum), multimem.st of the result
+//     (the switch writes it into every rank's window);
+//   LSA path (no multicast object): loads of the chunk from every peer's window over NVLink (P2P), fp32 sum,
+//     stores of the bf16 result into every peer's window;
+//   LSA barrier (every slice is back in every window), then the local copy window -> Y.
+// Rank r reads and writes only its own slice in every window, so the reduction is in place without races.
+constexpr int SYM_CTAS = 128;
+constexpr int SYM_THREADS = 512;
+
+__device__ __forceinline__ void bf16x8_acc(float (&a)[8], const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        a[2 * i] += __uint_as_float(w[i] << 16);
+        a[2 * i + 1] += __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+}
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(SYM_THREADS) sym_allreduce_kernel(ncclDevComm dc, ncclWindow_t win, int64_t n16,
+                                                                   int rank, int nranks, int multimem, uint4* Y) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    const int64_t q0 = n16 * rank / nranks, q1 = n16 * (rank + 1) / nranks;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    if (multimem) {
+        uint4* mc = static_cast<uint4*>(ncclGetLsaMultimemPointer(win, 0, dc));
+        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
+            uint4 v;
+            asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "l"(mc + q)
+                         : "memory");
+            asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(mc + q), "r"(v.x),
+                         "r"(v.y), "r"(v.z), "r"(v.w)
+                         : "memory");
+        }
+    } else {
+        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
+            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int p = 0; p < nranks; ++p)
+                bf16x8_acc(a, __ldcg(static_cast<const uint4*>(ncclGetLsaPointer(win, 0, p)) + q));
+            const uint4 o = make_uint4(bf16x2_rn(a[0], a[1]), bf16x2_rn(a[2], a[3]), bf16x2_rn(a[4], a[5]),
+                                       bf16x2_rn(a[6], a[7]));
+            for (int p = 0; p < nranks; ++p) static_cast<uint4*>(ncclGetLsaPointer(win, 0, p))[q] = o;
+        }
+    }
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    const uint4* loc = static_cast<const uint4*>(ncclGetLocalPointer(win, 0));
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n16; q += stride) Y[q] = loc[q];
+}
 
 static int ensure_events(sffn_comm* c, int n) {
     while (static_cast<int>(c->events.size()) < n + 1) {
@@ -63,6 +133,12 @@ int sffn_comm_destroy(sffn_comm* c) {
     if (!c) return SFFN_ERR_INVALID_ARG;
     int r = SFFN_OK;
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    if (c->has_dev) {
+        cudaDeviceSynchronize();
+        if (ncclDevCommDestroy(c->nccl, &c->dev) != ncclSuccess) r = SFFN_ERR_NCCL;
+        if (c->win && ncclCommWindowDeregister(c->nccl, c->win) != ncclSuccess) r = SFFN_ERR_NCCL;
+        if (c->sym_buf && ncclMemFree(c->sym_buf) != ncclSuccess) r = SFFN_ERR_NCCL;
+    }
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->nccl && ncclCommDestroy(c->nccl) != ncclSuccess) r = SFFN_ERR_NCCL;
@@ -79,6 +155,81 @@ int sffn_allreduce_bf16(sffn_comm* c, void* buf, int64_t count, void* stream) {
                       reinterpret_cast<cudaStream_t>(stream)) != ncclSuccess)
         return SFFN_ERR_NCCL;
     return SFFN_OK;
+}
+
+int sffn_comm_symmetric_init(sffn_comm* c, int64_t max_rows, int64_t K) {
+    if (!c || max_rows < 1 || K < 8 || K % 8 != 0) return SFFN_ERR_INVALID_ARG;
+    if (c->sym_buf) return SFFN_ERR_INVALID_ARG;  // once per communicator
+    const size_t bytes = (static_cast<size_t>(max_rows) * K * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) /
+                         NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    if (ncclMemAlloc(&c->sym_buf, bytes) != ncclSuccess) {
+        c->sym_buf = nullptr;
+        return SFFN_ERR_UNSUPPORTED;
+    }
+    if (ncclCommWindowRegister(c->nccl, c->sym_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
+        ncclMemFree(c->sym_buf);
+        c->sym_buf = nullptr;
+        return SFFN_ERR_UNSUPPORTED;
+    }
+    ncclDevCommRequirements req;
+    std::memset(&req, 0, sizeof(req));
+    req.lsaBarrierCount = SYM_CTAS;
+    req.lsaMultimem = c->nranks > 1;  // NVLS multicast when NCCL can set it up (NVSwitch systems)
+    ncclResult_t nr = ncclDevCommCreate(c->nccl, &req, &c->dev);
+    if (nr != ncclSuccess && req.lsaMultimem) {  // no NVLS on this system: peer loads / stores instead
+        req.lsaMultimem = false;
+        nr = ncclDevCommCreate(c->nccl, &req, &c->dev);
+    }
+    if (nr != ncclSuccess) {
+        ncclCommWindowDeregister(c->nccl, c->win);
+        ncclMemFree(c->sym_buf);
+        c->sym_buf = nullptr;
+        c->win = nullptr;
+        return SFFN_ERR_UNSUPPORTED;
+    }
+    c->has_dev = true;
+    c->multimem = req.lsaMultimem;
+    c->sym_bytes = bytes;
+    c->sym_rows = max_rows;
+    c->sym_K = K;
+    return SFFN_OK;
+}
+
+int sffn_comm_symmetric_info(const sffn_comm* c, int* multimem, int64_t* max_rows, int64_t* K) {
+    if (!c) return SFFN_ERR_INVALID_ARG;
+    if (multimem) *multimem = c->multimem ? 1 : 0;
+    if (max_rows) *max_rows = c->has_dev ? c->sym_rows : 0;
+    if (K) *K = c->has_dev ? c->sym_K : 0;
+    return c->has_dev ? SFFN_OK : SFFN_ERR_UNSUPPORTED;
+}
+
+int sffn_allreduce_sym_bf16(sffn_comm* c, const void* src, void* Y, int64_t rows, int64_t K, void* stream) {
+    if (!c || !Y || rows < 0 || K < 8 || K % 8 != 0) return SFFN_ERR_INVALID_ARG;
+    if (!c->has_dev) return SFFN_ERR_UNSUPPORTED;
+    if (rows > c->sym_rows || K != c->sym_K) return SFFN_ERR_SHAPE;
+    if (rows == 0) return SFFN_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t bytes = static_cast<size_t>(rows) * K * 2;
+    if (src && src != c->sym_buf &&
+        cudaMemcpyAsync(c->sym_buf, src, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return SFFN_ERR_CUDA;
+    sym_allreduce_kernel<<<SYM_CTAS, SYM_THREADS, 0, st>>>(c->dev, c->win, static_cast<int64_t>(bytes / 16), c->rank,
+                                                           c->nranks, c->multimem ? 1 : 0, static_cast<uint4*>(Y));
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_sharded_forward_sym(sffn_comm* c, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
+                             int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
+                             size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream) {
+    if (!c) return SFFN_ERR_INVALID_ARG;
+    if (!c->has_dev) return SFFN_ERR_UNSUPPORTED;
+    if (M < 0 || M > c->sym_rows || K != c->sym_K) return SFFN_ERR_SHAPE;
+    if (!Y) return SFFN_ERR_INVALID_ARG;
+    // the DOWN epilogue writes this rank's partial Y straight into the registered window (no staging copy)
+    int r = sffn_forward(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, c->sym_buf, workspace, ws_bytes, d_overflow, algo,
+                         stream);
+    if (r != SFFN_OK) return r;
+    return sffn_allreduce_sym_bf16(c, nullptr, Y, M, K, stream);
 }
 
 int sffn_sharded_forward(sffn_comm* c, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s, int64_t M,

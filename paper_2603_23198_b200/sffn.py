@@ -58,6 +58,11 @@ _SIGS = {
     "sffn_forward_nongated": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _int, _vp]),
     "sffn_forward_host_stage_bytes": (_sz, [_i64, _i64]),
     "sffn_forward_host_chunks": (_i64, [_i64, _i64, _vp, _i64]),
+    "sffn_comm_symmetric_init": (_int, [_vp, _i64, _i64]),
+    "sffn_comm_symmetric_info": (_int, [_vp, _vp, _vp, _vp]),
+    "sffn_allreduce_sym_bf16": (_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "sffn_sharded_forward_sym": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
+                                        _int, _vp]),
     "sffn_launch_count": (_i64, []),
     "sffn_union_block_rows": (_int, []),
     "sffn_forward_host": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _sz, _vp, _int,
@@ -415,6 +420,43 @@ class Comm:
                                         _bf16(wd_s, "wd"), M, K, N_local, T, C, _bf16(out, "out"), _p(workspace),
                                         workspace.numel() * workspace.element_size(), _p(overflow), a, n_chunks,
                                         _stream(stream)), "sffn_sharded_forward")
+        return out
+
+    # ------------------------------------------------------------ NEXT-3: symmetric-memory all-reduce
+    def symmetric_init(self, max_rows: int, K: int) -> bool:
+        """Collective: registers a max_rows x K bf16 symmetric window + NCCL device communicator.  False when
+        the platform cannot (SFFN_ERR_UNSUPPORTED); other errors raise."""
+        st = int(lib().sffn_comm_symmetric_init(self.h, max_rows, K))
+        if st == 6:
+            return False
+        _chk(st, "sffn_comm_symmetric_init")
+        return True
+
+    def symmetric_info(self) -> dict:
+        mm, rows, k = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+        st = int(lib().sffn_comm_symmetric_info(self.h, ctypes.byref(mm), ctypes.byref(rows), ctypes.byref(k)))
+        return {"ready": st == 0, "multimem": bool(mm.value), "max_rows": rows.value, "K": k.value}
+
+    def allreduce_sym(self, src, out=None, stream=None):
+        rows, K = src.shape
+        if out is None:
+            out = torch.empty_like(src)
+        _chk(lib().sffn_allreduce_sym_bf16(self.h, _bf16(src, "src"), _bf16(out, "out"), rows, K, _stream(stream)),
+             "sffn_allreduce_sym_bf16")
+        return out
+
+    def sharded_forward_sym(self, x, wg_s, wu_s, wd_s, T=256, C=8, out=None, workspace=None, overflow=None,
+                            algo="auto", stream=None):
+        M, K = x.shape
+        N_local = wg_s.shape[0]
+        a = _algo(algo)
+        if out is None:
+            out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+        workspace = _ws(workspace_bytes(M, K, N_local, T, C, a), x.device, workspace)
+        _chk(lib().sffn_sharded_forward_sym(self.h, _bf16(x, "x"), _bf16(wg_s, "wg"), _bf16(wu_s, "wu"),
+                                            _bf16(wd_s, "wd"), M, K, N_local, T, C, _bf16(out, "out"), _p(workspace),
+                                            workspace.numel() * workspace.element_size(), _p(overflow), a,
+                                            _stream(stream)), "sffn_sharded_forward_sym")
         return out
 
     def allreduce(self, buf, stream=None):

@@ -297,6 +297,35 @@ def test_sharded_forward_single_rank(sffn, algo):
     assert rel_fro(parts.cpu().numpy().astype(np.float64), bf16_np(ref)) < Y_TOL
 
 
+@pytest.mark.parametrize("algo", ALGOS)
+def test_sharded_forward_symmetric_single_rank(sffn, algo):
+    """NEXT-3 symmetric path on a 1-rank communicator (the harness has one GPU): NCCL symmetric window +
+    device communicator, the DOWN epilogue writing into the window, the library's reduction kernel (LSA
+    barriers, P2P path — NVLS needs >= 2 ranks) and the copy-out: bit-identical to sffn_forward; the
+    stand-alone reduction of a random buffer is the identity at G = 1; M above the window is refused."""
+    cfg = synth.CONFIGS["1B"].replace(M=700, K=512, N=2048, Kb=32, sparsity=0.97)
+    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    ref = sffn.forward(X, Wg, Wu, Wd, 256, 8, algo=algo)
+    comm = sffn.Comm(0, 1, torch.cuda.current_device())
+    try:
+        if not comm.symmetric_init(1024, cfg.K):
+            pytest.skip("NCCL symmetric windows unsupported on this platform")
+        info = comm.symmetric_info()
+        assert info["ready"] and info["max_rows"] == 1024 and info["K"] == cfg.K and not info["multimem"]
+        for _ in range(2):  # the LSA barrier epochs advance across calls
+            Y = comm.sharded_forward_sym(X, Wg, Wu, Wd, 256, 8, algo=algo)
+            torch.cuda.synchronize()
+            assert torch.equal(Y.view(torch.int16), ref.view(torch.int16))
+        src = torch.randn(333, cfg.K, device="cuda").to(torch.bfloat16)
+        out = comm.allreduce_sym(src)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), src.view(torch.int16))
+        with pytest.raises(sffn.SffnError):
+            comm.allreduce_sym(torch.zeros(2048, cfg.K, dtype=torch.bfloat16, device="cuda"))
+    finally:
+        comm.close()
+
+
 # ----------------------------------------------------------------- fp32 mode (R19): Y within 1e-5
 F32_TOL = 1e-5
 
