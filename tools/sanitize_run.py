@@ -23,5 +23,11 @@ f = lambda a: a.float().contiguous()
 sffn.forward_f32(f(X), f(Wg), f(Wu), f(Wd), 256, 8)
 xh = X.cpu().pin_memory()
 sffn.forward_host(xh, Wg, Wu, Wd, 256, 8, chunk_rows=128)
+if os.environ.get("SFFN_UNION_PAIR") != "1":  # NEXT-3 symmetric path on a 1-rank communicator
+    comm = sffn.Comm(0, 1, torch.cuda.current_device())
+    if comm.symmetric_init(cfg.M, cfg.K):
+        comm.sharded_forward_sym(X, Wg, Wu, Wd, 256, 8, algo="union")
+    torch.cuda.synchronize()
+    comm.close()
 torch.cuda.synchronize()
 print("sanitize run done")
