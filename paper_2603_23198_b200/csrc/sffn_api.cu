@@ -223,7 +223,7 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, glist, coff, total;
+    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, glist, coff, bctr, total;
     int lmax, nchunk;
 };
 // Token rows per union block: 128 (single-CTA union GEMMs) or 256 (CTA-pair union GEMMs, SFFN_UNION_PAIR=1).
@@ -253,6 +253,7 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8)
     w.nchunk = static_cast<int>((N + 255) / 256);
     w.glist = o; o = align1k(o + NB * BR * static_cast<int64_t>(w.lmax) * 4);
     w.coff = o;  o = align1k(o + NB * BR * static_cast<int64_t>(w.nchunk + 1) * 2);
+    w.bctr = o;  o = align1k(o + (NB + 1) * 4);  // union_meta_kernel: per-block + global completion counters
     w.total = o;
     return w;
 }
@@ -301,13 +302,13 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     void* xp = base + L.xp;
     // row permutation pi (per 2048-row window, descending stored nnz) and the permuted copy of X
     int* rnnz = reinterpret_cast<int*>(base + L.nnz);
-    int* done_ctr = um.counters + 2;  // union_meta_kernel completion counter (zeroed by union_rank_kernel)
+    int* bctr = reinterpret_cast<int*>(base + L.bctr);  // union_meta_kernel counters (zeroed by union_rank_kernel)
     if (!nnz_ready) {
         { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
     { union_rank_kernel<<<dim3(static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_SPLIT), PERM_W / PERM_SPLIT, 0,
-                        st>>>(rnnz, (int)M, perm, done_ctr); note_launch(); }
+                        st>>>(rnnz, (int)M, perm, um.umask, NB * (N / 32), bctr, (int)NB + 1); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     if (gated) {
         { permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
@@ -317,8 +318,12 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
 
     // union lists + the UP work list (one launch), then the compact gate lists (gated) or the scattered G (non-gated)
     const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
-    { union_meta_kernel<<<static_cast<unsigned>(NB), UB_THREADS, ub_smem, st>>>(
-        tw, (int)M, (int)N, T, C, um, perm, done_ctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP)); note_launch(); }
+    const int sms_meta = dev_info().sms;
+    // CTAs per union block: a power of two (it must divide the block rows), up to ~1.5 waves of CTAs
+    int split = 1;
+    while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms_meta) split *= 2;
+    { union_meta_kernel<<<static_cast<unsigned>(NB * split), UB_THREADS, ub_smem, st>>>(
+        tw, (int)M, (int)N, T, C, um, perm, bctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     if (gated) {
         { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(

@@ -163,14 +163,21 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum) {
     }
 }
 
-// Union metadata of one block of 128 pi-ordered rows, one CTA (UB_THREADS) per block:
-//   1. OR of the rows' stored indices into a SMEM bitmask (warp per row, coalesced row reads);
-//   2. prefix sums -> sorted U_b (padded to a multiple of 64 with unit 0), umask / uwoff / ulen / utot;
-//   3. the last CTA to finish (device-scope counter, zeroed by union_rank_kernel) builds the UP work list.
-// Dynamic SMEM: 2 N/32 words + (UB_THREADS/32 + 1) scan ints.
+// Union metadata of one block of brows pi-ordered rows, `split` CTAs (UB_THREADS) per block (split = 1 when
+// there are already enough blocks to fill the GPU, up to META_SPLIT_MAX for small M):
+//   1. each CTA ORs the stored indices of its brows/META_SPLIT rows into a SMEM bitmask (warp per row,
+//      coalesced row reads, 8 x 512 B in flight per warp) and (split > 1) merges it into the block's global umask
+//      (atomicOr of the non-zero words; umask and the counters were zeroed by union_rank_kernel);
+//   2. the last CTA of the block (per-block counter) reloads the merged mask, prefix sums -> sorted U_b
+//      (padded to a multiple of 64 with unit 0), uwoff / ulen / utot;
+//   3. the last block to finish (global counter) builds the UP work list.
+// Splitting a block's rows over several CTAs shortens the per-CTA chain of dependent row reads, which
+// bounded the kernel (one CTA per block took ~57 us at any M).  Dynamic SMEM: 2 N/32 words + (UB_THREADS/32
+// + 1) scan ints.
+constexpr int META_SPLIT_MAX = 8;
 __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
                                                                  int C, UnionMeta um, const int32_t* __restrict__ perm,
-                                                                 int* done_ctr, int up_group) {
+                                                                 int* bctr, int up_group, int split) {
     extern __shared__ uint32_t ub_smem[];
     constexpr int NWP = UB_THREADS / 32;
     const int NW = N >> 5;
@@ -179,17 +186,17 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
     int32_t* wsum = woff + NW;                                 // [NWP + 1]
     __shared__ int s_last;
     __shared__ int s_prow[256];
-    const int b = blockIdx.x;
-    const int NB = gridDim.x;
+    const int b = blockIdx.x / split, part = blockIdx.x % split;
+    const int NB = gridDim.x / split;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int BR = um.brows;
-    const int rows = min(BR, M - b * BR);
+    const int BR = um.brows, PR = BR / split;
+    const int r0 = part * PR;
+    const int rows = max(0, min(PR, M - b * BR - r0));
     for (int w = threadIdx.x; w < NW; w += UB_THREADS) mask[w] = 0u;
-    for (int r = threadIdx.x; r < rows; r += UB_THREADS) s_prow[r] = __ldg(perm + static_cast<int64_t>(b) * BR + r);
+    for (int r = threadIdx.x; r < rows; r += UB_THREADS)
+        s_prow[r] = __ldg(perm + static_cast<int64_t>(b) * BR + r0 + r);
     __syncthreads();
 
-    // warp per row, coalesced 16-byte reads of the whole packed row (measured faster than reading only the tiles'
-    // first sectors: the strided 32-byte reads do not save DRAM bursts)
     const int NT = N / T, WPT = T / C, cap = WPT - 1, RW = N / C;
     for (int r = warp; r < rows; r += NWP) {
         const uint32_t* row = tw + static_cast<int64_t>(s_prow[r]) * RW;
@@ -199,6 +206,21 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
         });
     }
     __syncthreads();
+    uint32_t* gmask = um.umask + static_cast<int64_t>(b) * NW;
+    if (split > 1) {
+        for (int w = threadIdx.x; w < NW; w += UB_THREADS)
+            if (mask[w]) atomicOr(gmask + w, mask[w]);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(bctr + b, 1) == split - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        for (int w = threadIdx.x; w < NW; w += UB_THREADS) mask[w] = __ldcg(gmask + w);
+        __syncthreads();
+    } else {
+        for (int w = threadIdx.x; w < NW; w += UB_THREADS) gmask[w] = mask[w];
+    }
 
     // exclusive scan of popc(mask[w]) over w (each thread owns a contiguous segment)
     const int seg = (NW + UB_THREADS - 1) / UB_THREADS;
@@ -238,7 +260,6 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
     for (int w = threadIdx.x; w < NW; w += UB_THREADS) {
         uint32_t m = mask[w];
         int pos = woff[w];
-        um.umask[static_cast<int64_t>(b) * NW + w] = m;
         um.uwoff[static_cast<int64_t>(b) * NW + w] = pos;
         while (m) {
             const int bit = __ffs(m) - 1;
@@ -255,7 +276,7 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
     // the last CTA builds the UP work list from every block's ulen
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1) == NB - 1;
+    if (threadIdx.x == 0) s_last = atomicAdd(bctr + NB, 1) == NB - 1;
     __syncthreads();
     if (s_last) {
         __threadfence();
@@ -376,12 +397,19 @@ __global__ void row_nnz_kernel(const uint32_t* __restrict__ tw, int M, int N, in
 //   #{ j in window : nnz_j > nnz_i  or  (nnz_j == nnz_i and j < i) }
 // i.e. stable descending order of stored non-zeros.  Grid (windows, PERM_SPLIT); every CTA holds its window's
 // counts in SMEM (padding rows = -1, never counted) and ranks PERM_W / PERM_SPLIT rows (thread per row, four
-// keys per 16-byte SMEM read).  Block (0,0) also zeroes the completion counter of union_meta_kernel, which runs
-// after it on the same stream.
+// keys per 16-byte SMEM read).  The grid also zeroes union_meta_kernel's merged masks and counters.
 constexpr int PERM_SPLIT = 16;
 static_assert(PERM_W == 2048, "rank keys pack the window index in 11 bits");
 __global__ void __launch_bounds__(PERM_W / PERM_SPLIT) union_rank_kernel(const int* __restrict__ nnz, int M,
-                                                                        int32_t* __restrict__ perm, int* done_ctr) {
+                                                                        int32_t* __restrict__ perm,
+                                                                        uint32_t* __restrict__ zero_a, int64_t na,
+                                                                        int* __restrict__ zero_b, int nb) {
+    {  // zero union_meta_kernel's merged masks and counters (it runs after this kernel on the same stream)
+        const int64_t t = (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+        const int64_t nt = static_cast<int64_t>(gridDim.x) * gridDim.y * blockDim.x;
+        for (int64_t i = t; i < na; i += nt) zero_a[i] = 0u;
+        for (int64_t i = t; i < nb; i += nt) zero_b[i] = 0;
+    }
     // packed key (nnz << 11) | (2047 - j): key_j > key_i  <=>  nnz_j > nnz_i or (nnz_j == nnz_i and j < i)
     // (stored non-zeros of a row <= N <= 65536 < 2^20); padding rows get -1 and are never counted
     __shared__ __align__(16) int key[PERM_W];
@@ -389,7 +417,6 @@ __global__ void __launch_bounds__(PERM_W / PERM_SPLIT) union_rank_kernel(const i
     const int rows = min(PERM_W, M - w0);
     for (int i = threadIdx.x; i < PERM_W; i += blockDim.x)
         key[i] = i < rows ? (__ldg(nnz + w0 + i) << 11) | (PERM_W - 1 - i) : -1;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *done_ctr = 0;
     __syncthreads();
     const int i = blockIdx.y * (PERM_W / PERM_SPLIT) + threadIdx.x;
     if (i >= rows) return;

@@ -6,6 +6,8 @@ sys.path.insert(0, ROOT)
 import torch, synth
 import paper_2603_23198_b200 as sffn
 cfg = synth.CONFIGS[os.environ.get("CFG", "7B")]
+if os.environ.get("M"):
+    cfg = cfg.replace(M=int(os.environ["M"]))
 dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
 X = dev(synth.gen_x(cfg)); Wg, Wu, Wd = (dev(synth.gen_w(cfg, w)) for w in "gud")
 tw = sffn.pack(X, Wg, cfg.T, cfg.C)
