@@ -215,11 +215,24 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 int b, cj, len;
                 tile_info(tile, b, cj, len);
                 const int nk = UP ? nk_up : len / GEMM_BK;
+                // dense block (union forced to all N units, union_meta_kernel): B by TMA tiles, no gathers
+                const bool dense = __ldg(args.um.utot + b) == N;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], GEMM_A_BYTES);
+                    mbar_arrive_expect_tx(&full[stage], dense ? GEMM_STAGE_BYTES : GEMM_A_BYTES);
                     tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
                                 UG_WPOL ? policy_evict_first() : policy_evict_last());
+                    if (dense) {
+                        uint8_t* bdst = stB + stage * GEMM_B_BYTES;
+                        if (UP) {  // W_u rows [256 cj, 256 cj + 256), k-slice kb: K-major box {64, 256}
+                            tma_load_2d(bdst, &tmB, &full[stage], kb * GEMM_BK, 256 * cj, policy_evict_last());
+                        } else {   // W_d rows [64 kb, 64 kb + 64), columns 256 cj + 64 q: four MN-major {64, 64} atoms
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                tma_load_2d(bdst + q * 8192, &tmB, &full[stage], 256 * cj + 64 * q, kb * GEMM_BK,
+                                            policy_evict_last());
+                        }
+                    }
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -243,7 +256,18 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             int b, cj, len;
             tile_info(tile, b, cj, len);
             const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
-            if (UP) {
+            if (__ldg(args.um.utot + b) == N) {
+                // dense block: B comes by TMA (warp 0); keep the per-stage arrivals of the full barrier
+                const int nk = UP ? nk_up : len / GEMM_BK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait_relaxed(&empty[stage], phase ^ 1);
+                    cp_async_arrive_noinc(&full[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            } else if (UP) {
                 // pass i covers chunk rows 4 UG_GW i + 4 gw + sub
                 constexpr int NP = 64 / UG_GW;
                 int nidx[NP];

@@ -276,6 +276,18 @@ int* union_nnz_ptr(void* ws, int64_t M, int64_t N, int64_t K, int T, int C) {
     return reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + union_ws_layout(M, N, K, T, C).nnz);
 }
 
+// Union size from which a block is made dense (all N units; its weight tiles then come by TMA instead of
+// gathers): SFFN_UNION_DENSE (fraction of N, default 0.7; >= 1 disables).  Only the single-CTA kernels have the
+// TMA path (and it needs N >= 256 for the UP box); the pair kernels would keep gathering an identity list.
+int union_dense_units(int64_t N, bool has_tma_path) {
+    static const double frac = [] {
+        const char* e = std::getenv("SFFN_UNION_DENSE");
+        return e ? std::atof(e) : 0.7;
+    }();
+    if (!has_tma_path || frac >= 1.0) return static_cast<int>(N) + 1;
+    return std::max(1, static_cast<int>(frac * static_cast<double>(N)));
+}
+
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true,
                       bool nnz_ready = false) {
@@ -323,7 +335,8 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     int split = 1;
     while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms_meta) split *= 2;
     { union_meta_kernel<<<static_cast<unsigned>(NB * split), UB_THREADS, ub_smem, st>>>(
-        tw, (int)M, (int)N, T, C, um, perm, bctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split); note_launch(); }
+        tw, (int)M, (int)N, T, C, um, perm, bctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split,
+        union_dense_units(N, BR == 128 && N >= 256)); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     if (gated) {
         { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
@@ -339,11 +352,12 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
     if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M > 0 ? M : 1, GEMM_BK, GEMM_BM,
                  CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, N >= 256 ? 256 : 64,
+                 CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&thc_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * BR, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * BR, GEMM_BK, GEMM_BM,
                  CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wd, K, N, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wd, K, N, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, K, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
         return SFFN_ERR_CUDA;
     UnionArgs ua{};

@@ -177,7 +177,8 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum) {
 constexpr int META_SPLIT_MAX = 8;
 __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
                                                                  int C, UnionMeta um, const int32_t* __restrict__ perm,
-                                                                 int* bctr, int up_group, int split) {
+                                                                 int* bctr, int up_group, int split,
+                                                                 int dense_units) {
     extern __shared__ uint32_t ub_smem[];
     constexpr int NWP = UB_THREADS / 32;
     const int NW = N >> 5;
@@ -222,7 +223,10 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
         for (int w = threadIdx.x; w < NW; w += UB_THREADS) gmask[w] = mask[w];
     }
 
-    // exclusive scan of popc(mask[w]) over w (each thread owns a contiguous segment)
+    // exclusive scan of popc(mask[w]) over w (each thread owns a contiguous segment); a block whose union
+    // reaches dense_units is made dense (all N units, identity list): the union GEMMs then load its weight
+    // tiles by TMA instead of gathering (cheaper than gathering most of the rows anyway)
+    for (int pass = 0; pass < 2; ++pass) {
     const int seg = (NW + UB_THREADS - 1) / UB_THREADS;
     const int w0 = threadIdx.x * seg, w1 = min(NW, w0 + seg);
     int local = 0;
@@ -253,8 +257,18 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
         run += __popc(mask[w]);
     }
     __syncthreads();
+    if (pass == 0 && wsum[NWP] >= dense_units && wsum[NWP] < N) {
+        __syncthreads();
+        for (int w = threadIdx.x; w < NW; w += UB_THREADS) mask[w] = 0xFFFFFFFFu;
+        __syncthreads();
+        continue;
+    }
+    break;
+    }
     const int total = wsum[NWP];
     const int padded = max(64, (total + 63) & ~63);
+    if (total == N)  // dense (forced or natural): the gate lists read the all-ones mask
+        for (int w = threadIdx.x; w < NW; w += UB_THREADS) gmask[w] = mask[w];
 
     int32_t* ul = um.ulist + static_cast<int64_t>(b) * N;
     for (int w = threadIdx.x; w < NW; w += UB_THREADS) {

@@ -555,3 +555,34 @@ def test_union_pair_mode(sffn):
                         "-k", sel], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("sparsity", [0.90, 0.95])
+def test_union_low_sparsity_dense_blocks(sffn, sparsity):
+    """At 90-95% sparsity most 128-row unions exceed 0.7 N: those blocks run with the identity union (all units)
+    and TMA-loaded weight tiles instead of gathers; Y still equals Eq.3 / Eq.1 within 1e-2."""
+    cfg = synth.CONFIGS["1B"].replace(M=520, K=512, N=2048, Kb=32, sparsity=sparsity, C=2, dead_frac=0.1,
+                                      pmax_ratio=3.0)
+    X, Wg, Wu, Wd = inputs(cfg)
+    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo="union")
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    y = bf16_np(Y)
+    assert rel_fro(y, oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
+    assert rel_fro(y, oracle.ffn_dense(X, Wg, Wu, Wd)) < Y_TOL
+
+
+@pytest.mark.gpu
+def test_union_all_blocks_dense(sffn):
+    """SFFN_UNION_DENSE=0.01 (read once per process) makes every union block dense: re-run the union parity
+    tests in a child process so the TMA-tile path covers every shape they cover."""
+    if os.environ.get("SFFN_UNION_DENSE"):
+        pytest.skip("already running with a forced dense threshold")
+    import subprocess
+    import sys
+    env = dict(os.environ, SFFN_UNION_DENSE="0.01")
+    sel = ("union and (up_down_vs_oracle or union_tiles or dense_rows or forward_vs_oracle or nongated or "
+           "70b or forward_host or ragged or overflow or down_from or low_sparsity)")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-m", "gpu", "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", sel], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
