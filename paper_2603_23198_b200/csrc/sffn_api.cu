@@ -288,6 +288,18 @@ int union_dense_units(int64_t N, bool has_tma_path) {
     return std::max(1, static_cast<int>(frac * static_cast<double>(N)));
 }
 
+// Stored entries of a block (summed over its rows) from which the block is made dense without computing its
+// union: SFFN_UNION_DENSE_NNZ (multiple of N, default 4; 0 disables).  At 99% sparsity a 128-row block holds
+// ~1.3 N entries (union ~0.35 N); at 90% ~13 N (union ~N).
+int64_t union_dense_nnz(int64_t N, bool has_tma_path) {
+    static const double f = [] {
+        const char* e = std::getenv("SFFN_UNION_DENSE_NNZ");
+        return e ? std::atof(e) : 4.0;
+    }();
+    if (!has_tma_path || f <= 0.0) return INT64_MAX;
+    return static_cast<int64_t>(f * static_cast<double>(N));
+}
+
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true,
                       bool nnz_ready = false) {
@@ -336,7 +348,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms_meta) split *= 2;
     { union_meta_kernel<<<static_cast<unsigned>(NB * split), UB_THREADS, ub_smem, st>>>(
         tw, (int)M, (int)N, T, C, um, perm, bctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split,
-        union_dense_units(N, BR == 128 && N >= 256)); note_launch(); }
+        union_dense_units(N, BR == 128 && N >= 256), rnnz, union_dense_nnz(N, BR == 128 && N >= 256)); note_launch(); }
     if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     if (gated) {
         { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
