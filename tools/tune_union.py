@@ -18,6 +18,6 @@ def t(fn, n=10):
     for _ in range(n):
         flush.fill_(1); s, e = torch.cuda.Event(True), torch.cuda.Event(True); s.record(); fn(); e.record(); torch.cuda.synchronize(); ts.append(s.elapsed_time(e))
     return float(np.median(ts))
-for up, down in itertools.product([8, 16, 32, 64, 128], [4, 8, 16, 32, 64]):
+for up, down in itertools.product([int(v) for v in os.environ.get("UPS", "2,4,8,16").split(",")], [int(v) for v in os.environ.get("DOWNS", "4,8,16,32,64").split(",")]):
     os.environ["SFFN_UP_GROUP"], os.environ["SFFN_DOWN_GROUP"] = str(up), str(down)
     print(f"up_group {up:4d} down_group {down:3d}: up_down {t(lambda: sffn.up_down(X, tw, Wu, Wd, cfg.T, cfg.C, out=Y, workspace=ws, algo='union')):.3f} ms", flush=True)
