@@ -586,3 +586,16 @@ def test_union_all_blocks_dense(sffn):
                         "-k", sel], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("algo,expected", [("union", 7), ("gather", 2)])
+def test_launch_count(sffn, algo, expected):
+    """sffn_launch_count (what bench.py reports as gpu_launches): one union forward = gate GEMM + rank + permute
+    + union metadata + gate lists + UP + DOWN; one gather forward = gate GEMM + fused up/down kernel."""
+    cfg = synth.CONFIGS["1B"].replace(M=600, K=256, N=1024, Kb=16, sparsity=0.97)
+    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    sffn.forward(X, Wg, Wu, Wd, 256, 8, algo=algo)
+    c0 = sffn.launch_count()
+    sffn.forward(X, Wg, Wu, Wd, 256, 8, algo=algo)
+    torch.cuda.synchronize()
+    assert sffn.launch_count() - c0 == expected
