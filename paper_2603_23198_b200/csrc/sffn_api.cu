@@ -289,12 +289,13 @@ int union_dense_units(int64_t N, bool has_tma_path) {
 }
 
 // Stored entries of a block (summed over its rows) from which the block is made dense without computing its
-// union: SFFN_UNION_DENSE_NNZ (multiple of N, default 4; 0 disables).  At 99% sparsity a 128-row block holds
-// ~1.3 N entries (union ~0.35 N); at 90% ~13 N (union ~N).
+// union: SFFN_UNION_DENSE_NNZ (multiple of N, default 8; 0 disables).  At 99% sparsity a 128-row block holds
+// ~1.3 N entries on average and up to ~4.5 N in the densest blocks (union <= 0.66 N: with a threshold of 4 those
+// went dense and the 7B union GEMMs lost 9%); at 95% ~6.4 N, at 90% ~13 N (union ~N).
 int64_t union_dense_nnz(int64_t N, bool has_tma_path) {
     static const double f = [] {
         const char* e = std::getenv("SFFN_UNION_DENSE_NNZ");
-        return e ? std::atof(e) : 4.0;
+        return e ? std::atof(e) : 8.0;
     }();
     if (!has_tma_path || f <= 0.0) return INT64_MAX;
     return static_cast<int64_t>(f * static_cast<double>(N));

@@ -87,6 +87,8 @@ def lib():
                               "there is no CPU fallback")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if not hasattr(L, name) and os.environ.get("SFFN_LIB"):
+                continue  # an older build under A/B (SFFN_LIB): bind what it exports
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
         _lib = L
