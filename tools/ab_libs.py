@@ -32,7 +32,11 @@ def t(fn, n=3):
     return float(np.median(r))
 res = {i: {"pack": [], "fwd": []} for i in range(len(L))}
 for rnd in range(int(os.environ.get("ROUNDS", "6"))):
-    for i, l in enumerate(L):
+    idx = list(range(len(L)))
+    if rnd % 2:
+        idx.reverse()  # ABBA order: no library always runs on the hotter GPU
+    for i in idx:
+        l = L[i]
         res[i]["pack"].append(t(lambda: l.sffn_pack(P(X), P(Wg), M, K, N, T, C, P(tw), None, None)))
         res[i]["fwd"].append(t(lambda: l.sffn_forward(P(X), P(Wg), P(Wu), P(Wd), M, K, N, T, C, P(Y), P(ws), ws.numel(), None, 2, None)))
 for i, p in enumerate(libs):
