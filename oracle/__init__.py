@@ -50,6 +50,8 @@ def _load():
         lib.oracle_down_twell.argtypes = [vp, vp, i64, i64, i64, ci, ci, ci, vp, vp]
         lib.oracle_pack_soa.argtypes = [vp, i64, i64, ci, ci, vp, vp, vp]
         lib.oracle_twell_to_ell.argtypes = [vp, i64, i64, ci, ci, i64, vp, vp, vp, vp]
+        lib.oracle_hybrid_sddmm.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp, vp, i64, vp, vp, ci, vp, vp]
+        lib.oracle_hybrid_spmm.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp, i64, i64, vp]
         lib.oracle_pack_soa.restype = i64
         lib.oracle_ffn_dense_f32.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp]
         lib.oracle_ffn_soa_f32.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, ci, ci, vp]
@@ -250,3 +252,67 @@ def twell_to_ell(words, N: int, T: int, C: int, ell_w: int):
     _load().oracle_twell_to_ell(words.ctypes.data, M, N, T, C, ell_w, val.ctypes.data, col.ctypes.data,
                                 nnz.ctypes.data, l.ctypes.data)
     return val, col, nnz, (float(l[0]), float(l[1]))
+
+
+# ---------------------------------------------------------------- training forward on the hybrid format (NEXT-4)
+def hybrid_sddmm(A, B, ell_col, row_nnz, row_loc, P_ell, dense_map, P_dense, gate: bool):
+    """Listing 5 + Alg.3 dense tail (oracle_hybrid_sddmm): (out_ell fp64 [M, ell_w], out_dense fp64 [n_dense, N]);
+    entries outside the pattern are 0."""
+    A, B = _u16(A), _u16(B)
+    M, K = A.shape
+    N = B.shape[0]
+    ell_col = np.ascontiguousarray(ell_col, dtype=np.int16)
+    ell_w = ell_col.shape[1]
+    row_nnz = np.ascontiguousarray(row_nnz, dtype=np.int32)
+    row_loc = np.ascontiguousarray(row_loc, dtype=np.int32)
+    P_ell = _u16(P_ell) if P_ell is not None else np.zeros((M, ell_w), dtype=np.uint16)
+    dense_map = np.ascontiguousarray(dense_map, dtype=np.int32)
+    nd = dense_map.shape[0]
+    P_dense = _u16(P_dense) if nd else np.zeros((1, N), dtype=np.uint16)
+    out_ell = np.zeros((M, ell_w), dtype=np.float64)
+    out_dense = np.zeros((max(nd, 1), N), dtype=np.float64)
+    _load().oracle_hybrid_sddmm(A.ctypes.data, B.ctypes.data, M, K, N, ell_w, ell_col.ctypes.data, row_nnz.ctypes.data,
+                                row_loc.ctypes.data, P_ell.ctypes.data, nd, dense_map.ctypes.data, P_dense.ctypes.data,
+                                1 if gate else 0, out_ell.ctypes.data, out_dense.ctypes.data)
+    return out_ell, out_dense[:nd]
+
+
+def hybrid_spmm(ell_val, ell_col, row_nnz, row_loc, dense_map, D, W) -> np.ndarray:
+    """Listing 6 + Alg.3 (oracle_hybrid_spmm): Y fp64 [M, K]; values ell_val / D given in fp64."""
+    W = _u16(W)
+    N, K = W.shape
+    ell_val = np.ascontiguousarray(ell_val, dtype=np.float64)
+    M, ell_w = ell_val.shape
+    ell_col = np.ascontiguousarray(ell_col, dtype=np.int16)
+    row_nnz = np.ascontiguousarray(row_nnz, dtype=np.int32)
+    row_loc = np.ascontiguousarray(row_loc, dtype=np.int32)
+    dense_map = np.ascontiguousarray(dense_map, dtype=np.int32)
+    nd = dense_map.shape[0]
+    D = np.ascontiguousarray(D, dtype=np.float64) if nd else np.zeros((1, N), dtype=np.float64)
+    Y = np.empty((M, K), dtype=np.float64)
+    _load().oracle_hybrid_spmm(ell_val.ctypes.data, ell_col.ctypes.data, row_nnz.ctypes.data, row_loc.ctypes.data, M,
+                               ell_w, nd, dense_map.ctypes.data, D.ctypes.data, W.ctypes.data, N, K, Y.ctypes.data)
+    return Y
+
+
+def hybrid_from_dense(H, ell_w: int, dense_cap: int):
+    """Reference hybrid partition of a dense matrix: rows with <= ell_w non-zeros -> ELL (ascending columns),
+    wider rows -> dense tail in row order (row_loc = slot), beyond dense_cap -> dropped (-2).  Plain numpy; used to
+    build SpMM / SDDMM test inputs, not a GPU-kernel model."""
+    H = np.asarray(H)
+    M, N = H.shape
+    col = np.full((M, ell_w), -1, dtype=np.int16)
+    nnz = np.zeros(M, dtype=np.int32)
+    loc = np.full(M, -1, dtype=np.int32)
+    dmap = []
+    for m in range(M):
+        idx = np.flatnonzero(H[m])
+        nnz[m] = len(idx)
+        if len(idx) <= ell_w:
+            col[m, :len(idx)] = idx.astype(np.int64).astype(np.uint16).view(np.int16)
+        elif len(dmap) < dense_cap:
+            loc[m] = len(dmap)
+            dmap.append(m)
+        else:
+            loc[m] = -2
+    return col, nnz, loc, np.array(dmap, dtype=np.int32)

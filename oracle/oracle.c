@@ -328,3 +328,75 @@ void oracle_twell_to_ell(const uint32_t* words, int64_t M, int64_t N, int T, int
     l0l1[0] = l0;
     l0l1[1] = l1;
 }
+
+/*
+ * Hybrid SDDMM, dense -> hybrid (training forward h = h_g (.) x W_u on the gate pattern; Listing 5 P:1316-1378 for
+ * the ELL part, Alg.3 P:220-239 and P:1380 "multiplied by a binary mask containing the sparsity pattern" for the
+ * dense tail).  ELL rows (row_loc[m] == -1), j < row_nnz[m]:
+ *   out_ell[m, j] = g * sum_k A[m, k] B[n, k],  n = (uint16) ell_col[m, j],  g = P_ell[m, j] (gate) or 1;
+ * dense-tail slots s < n_dense, m = dense_map[s]:
+ *   out_dense[s, n] = P_dense[s, n] != 0 ? g * sum_k A[m, k] B[n, k] : 0,  g = P_dense[s, n] (gate) or 1.
+ * Other entries untouched.  A [M, K], B [N, K] (hidden-major weights), P_* bf16; fp64, k ascending.
+ */
+void oracle_hybrid_sddmm(const uint16_t* A, const uint16_t* B, int64_t M, int64_t K, int64_t N, int64_t ell_w,
+                         const int16_t* ell_col, const int32_t* row_nnz, const int32_t* row_loc,
+                         const uint16_t* P_ell, int64_t n_dense, const int32_t* dense_map, const uint16_t* P_dense,
+                         int gate, double* out_ell, double* out_dense) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        if (row_loc[m] != -1) continue;
+        int64_t z = row_nnz[m] < ell_w ? row_nnz[m] : ell_w;
+        for (int64_t j = 0; j < z; ++j) {
+            int64_t n = (int64_t)(uint16_t)ell_col[m * ell_w + j];
+            double s = 0.0;
+            for (int64_t k = 0; k < K; ++k) s += oracle_bf16_to_double(A[m * K + k]) * oracle_bf16_to_double(B[n * K + k]);
+            double g = gate ? oracle_bf16_to_double(P_ell[m * ell_w + j]) : 1.0;
+            out_ell[m * ell_w + j] = g * s;
+        }
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < n_dense; ++s) {
+        int64_t m = dense_map[s];
+        for (int64_t n = 0; n < N; ++n) {
+            double p = oracle_bf16_to_double(P_dense[s * N + n]);
+            if (p == 0.0) {
+                out_dense[s * N + n] = 0.0;
+                continue;
+            }
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k) acc += oracle_bf16_to_double(A[m * K + k]) * oracle_bf16_to_double(B[n * K + k]);
+            out_dense[s * N + n] = (gate ? p : 1.0) * acc;
+        }
+    }
+}
+
+/*
+ * Hybrid SpMM, hybrid -> dense (training forward y = h W_d; Listing 6, Alg.3):
+ *   ELL rows (row_loc[m] == -1): Y[m, :] = sum_{j < min(row_nnz[m], ell_w)} v[m, j] W[(uint16) ell_col[m, j], :];
+ *   dense-tail slots s < n_dense: Y[dense_map[s], :] = sum_n D[s, n] W[n, :];
+ *   dropped rows (row_loc[m] == -2, tail full): Y[m, :] = 0.
+ * Values v / D in fp64 (so the oracle chain SDDMM -> SpMM stays unrounded), W [N, K] bf16; fp64, n ascending.
+ */
+void oracle_hybrid_spmm(const double* ell_val, const int16_t* ell_col, const int32_t* row_nnz, const int32_t* row_loc,
+                        int64_t M, int64_t ell_w, int64_t n_dense, const int32_t* dense_map, const double* D,
+                        const uint16_t* W, int64_t N, int64_t K, double* Y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t k = 0; k < K; ++k) Y[m * K + k] = 0.0;
+        if (row_loc[m] != -1) continue;
+        int64_t z = row_nnz[m] < ell_w ? row_nnz[m] : ell_w;
+        for (int64_t j = 0; j < z; ++j) {
+            int64_t n = (int64_t)(uint16_t)ell_col[m * ell_w + j];
+            double v = ell_val[m * ell_w + j];
+            for (int64_t k = 0; k < K; ++k) Y[m * K + k] += v * oracle_bf16_to_double(W[n * K + k]);
+        }
+    }
+    for (int64_t s = 0; s < n_dense; ++s) {
+        int64_t m = dense_map[s];
+        for (int64_t n = 0; n < N; ++n) {
+            double v = D[s * N + n];
+            if (v == 0.0) continue;
+            for (int64_t k = 0; k < K; ++k) Y[m * K + k] += v * oracle_bf16_to_double(W[n * K + k]);
+        }
+    }
+}

@@ -462,3 +462,73 @@ def test_twell_to_ell_pins():
         assert np.array_equal(synth.bf16_to_f32(val[m, :k]), H[m, nzc[:k]])
     assert abs(l0 - counts.sum() / cfg.M) < 1e-12
     assert abs(l1 - H.astype(np.float64).sum() / cfg.M) < 1e-9 * max(1.0, abs(l1))
+
+
+# ---------------------------------------------------------------- training forward on the hybrid format (NEXT-4)
+def _hybrid_case(M=40, K=128, N=256, sparsity=0.95, ell_w=16, dense_cap=4, seed=3):
+    cfg = synth.CONFIGS["1B"].replace(M=M, K=K, N=N, Kb=16, sparsity=sparsity, seed=seed)
+    X, Wg, Wu, Wd = synth.gen_x(cfg), synth.gen_w(cfg, "g"), synth.gen_w(cfg, "u"), synth.gen_w(cfg, "d")
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wg, 256, 8)
+    H = oracle.unpack(words, N, 256, 8)                       # bf16(relu(x W_g)) (stored entries)
+    col, nnz, loc, dmap = oracle.hybrid_from_dense(H, ell_w, dense_cap)
+    Hbits = oracle.bf16_rne(H.astype(np.float32)).reshape(H.shape)
+    P_ell = np.zeros((M, ell_w), dtype=np.uint16)
+    for m in range(M):
+        if loc[m] == -1:
+            P_ell[m, :nnz[m]] = Hbits[m, col[m, :nnz[m]].view(np.uint16)]
+    P_dense = Hbits[dmap] if len(dmap) else np.zeros((0, N), dtype=np.uint16)
+    return X, Wu, Wd, H, col, nnz, loc, dmap, P_ell, P_dense
+
+
+def test_hybrid_partition_covers_rows():
+    """every row is ELL (nnz <= ell_w), dense tail (slot order), or dropped once the tail is full."""
+    X, Wu, Wd, H, col, nnz, loc, dmap, P_ell, P_dense = _hybrid_case()
+    assert ((loc == -1) == (nnz <= 16)).all() and len(dmap) <= 4
+    assert (loc[nnz > 16] != -1).all() and ((loc >= 0).sum() == len(dmap))
+    assert (dmap == np.flatnonzero(loc >= 0)).all() and (loc[dmap] == np.arange(len(dmap))).all()
+
+
+@pytest.mark.parametrize("gate", [False, True])
+def test_hybrid_sddmm_equals_masked_dense_product(gate):
+    """Listing 5 + Alg.3 mask: on dyadic-grid inputs the dense product x W_u^T is exact in fp64 (numpy matmul, a
+    different summation order): the oracle SDDMM must equal it at every pattern position (times the gate)."""
+    X, Wu, Wd, H, col, nnz, loc, dmap, P_ell, P_dense = _hybrid_case()
+    assert len(dmap) > 0 and (loc == -1).sum() > 0 and nnz.max() > 16
+    out_ell, out_dense = oracle.hybrid_sddmm(X, Wu, col, nnz, loc, P_ell, dmap, P_dense, gate)
+    U = synth.bf16_to_f32(X).astype(np.float64) @ synth.bf16_to_f32(Wu).astype(np.float64).T
+    G = H.astype(np.float64) if gate else (H != 0).astype(np.float64)
+    for m in np.flatnonzero(loc == -1):
+        c = col[m, :nnz[m]].view(np.uint16).astype(np.int64)
+        assert np.array_equal(out_ell[m, :nnz[m]], G[m, c] * U[m, c])
+        assert (out_ell[m, nnz[m]:] == 0).all()
+    for s, m in enumerate(dmap):
+        assert np.array_equal(out_dense[s], G[m] * U[m])
+
+
+def test_hybrid_spmm_equals_dense_matmul():
+    """Listing 6 + Alg.3: SpMM of the hybrid form of a dense matrix equals its dense product (exact on the grid,
+    numpy matmul); dropped rows are zero."""
+    X, Wu, Wd, H, col, nnz, loc, dmap, P_ell, P_dense = _hybrid_case(dense_cap=2)
+    assert (loc == -2).any(), "case must exercise the dropped-row path"
+    ell_val = np.zeros(col.shape, dtype=np.float64)
+    for m in np.flatnonzero(loc == -1):
+        ell_val[m, :nnz[m]] = H[m, col[m, :nnz[m]].view(np.uint16).astype(np.int64)]
+    Y = oracle.hybrid_spmm(ell_val, col, nnz, loc, dmap, H[dmap], Wd)
+    ref = H.astype(np.float64) @ synth.bf16_to_f32(Wd).astype(np.float64)
+    keep = loc != -2
+    assert np.array_equal(Y[keep], ref[keep]) and (Y[~keep] == 0).all()
+
+
+def test_hybrid_training_forward_equals_eq3():
+    """The training forward on the hybrid format, SpMM(SDDMM(x, W_u; gate h_g), W_d), is Eq.3 with the stored gate
+    (oracle.ffn_twell) for every non-dropped row, up to fp64 summation order."""
+    cfg_N = 256
+    X, Wu, Wd, H, col, nnz, loc, dmap, P_ell, P_dense = _hybrid_case(dense_cap=8)
+    out_ell, out_dense = oracle.hybrid_sddmm(X, Wu, col, nnz, loc, P_ell, dmap, P_dense, True)
+    Y = oracle.hybrid_spmm(out_ell, col, nnz, loc, dmap, out_dense, Wd)
+    words, _, _, _ = oracle.pack_from_inputs(X, synth.gen_w(synth.CONFIGS["1B"].replace(M=40, K=128, N=cfg_N, Kb=16,
+                                                                                        sparsity=0.95, seed=3), "g"),
+                                             256, 8)
+    ref = oracle.ffn_twell(X, words, Wu, Wd, cfg_N, 256, 8)
+    keep = loc != -2
+    assert np.abs(Y[keep] - ref[keep]).max() <= 1e-12 * max(1.0, np.abs(ref).max())
