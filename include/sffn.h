@@ -242,6 +242,34 @@ int sffn_forward_f32(const float* X, const float* Wg, const float* Wu, const flo
                      int64_t N, int T, int C, float* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
                      void* stream);
 
+/* ---------------------------------------------------------------- training forward on the hybrid format (NEXT-4)
+ * After sffn_twell_to_hybrid (the pattern of h_g), the paper's training forward computes h = h_g (.) x W_u on that
+ * pattern (dense -> hybrid, Listing 5; dense tail: tensor-core GEMM times the pattern mask, Alg.3
+ * P:220-239) and y = h W_d (hybrid -> dense, Listing 6; dense tail: tensor-core GEMM, rows
+ * scattered to their tokens, Alg.3 lines 14-17).  Hybrid operands use sffn_twell_to_hybrid's layout: ell_col
+ * int16 [M, ell_w] (read as uint16 unit ids), row_nnz [M], row_loc [M] (-1 ELL row, s >= 0 dense-tail slot,
+ * -2 dropped), dense_map [D] (slot -> row), *d_dense_count (device; slots used = min(count, D)), values bf16.
+ *
+ * sffn_hybrid_sddmm: A [M, K] bf16, B [N, K] bf16 (hidden-major, e.g. W_u).  ELL rows: out_ell[m, j] =
+ *   bf16(g * sum_k A[m,k] B[ell_col[m,j], k]) for j < min(row_nnz[m], ell_w) (other slots untouched), g =
+ *   P_ell[m, j] when gate != 0, else 1; dense tail slots s: out_dense[s, n] = P_dense[s, n] != 0 ?
+ *   bf16(g * (A[dense_map[s]] . B[n])) : 0, g = P_dense[s, n] (gate) or 1.  fp32 accumulation (the tail dot
+ *   products on tcgen05 in fp32, rounded once with the gate).  Requires K % 64 == 0, N % 16 == 0 and, with a
+ *   dense tail (D > 0), N >= 256 and workspace >= sffn_hybrid_mm_workspace_bytes(D, K, N).
+ * sffn_hybrid_spmm: Y [M, K] bf16: ELL rows Y[m] = sum_j ell_val[m,j] W[ell_col[m,j], :] (CUDA cores, fp32);
+ *   tail slots Y[dense_map[s]] = dense[s, :] W (tcgen05, W [N, K] read MN-major by TMA, no transpose); dropped
+ *   rows are zero.  Requires K % 64 == 0, K >= 256, N % 64 == 0; workspace as above when D > 0.
+ * Caller-owned device memory, stream-ordered, no host synchronization. */
+size_t sffn_hybrid_mm_workspace_bytes(int64_t D, int64_t K, int64_t N);
+int sffn_hybrid_sddmm(const void* A, const void* B, int64_t M, int64_t K, int64_t N, int ell_w, const int16_t* ell_col,
+                      const int32_t* row_nnz, const int32_t* row_loc, const void* P_ell, int64_t D,
+                      const int32_t* dense_map, const int* d_dense_count, const void* P_dense, int gate, void* out_ell,
+                      void* out_dense, void* workspace, size_t ws_bytes, void* stream);
+int sffn_hybrid_spmm(const void* ell_val, const int16_t* ell_col, const int32_t* row_nnz, const int32_t* row_loc,
+                     int64_t M, int ell_w, int64_t D, const int32_t* dense_map, const int* d_dense_count,
+                     const void* dense, const void* W, int64_t N, int64_t K, void* Y, void* workspace, size_t ws_bytes,
+                     void* stream);
+
 /* ---------------------------------------------------------------- multi-GPU (hidden-dim shards)
  * One process per GPU.  Rank r owns hidden units [n_offset, n_offset + N_local) — contiguous row
  * blocks of all three [N, K] weights — packs its own TwELL (local indices), computes the partial

@@ -1,0 +1,123 @@
+// hybrid_mm.cuh — the training forward on the hybrid format (after sffn_twell_to_hybrid):
+//   SDDMM (dense -> hybrid): h = h_g (.) x W_u on the gate pattern — Listing 5 for the ELL rows, the
+//         dense tail by a tcgen05 GEMM times the pattern mask (Alg.3);
+//   SpMM  (hybrid -> dense): y = h W_d — Listing 6 for the ELL rows, the dense tail by a tcgen05 GEMM
+//         whose rows are scattered to their token rows (Alg.3 lines 14-17).
+// The CUDA-core ELL kernels follow the paper's mapping (one CTA per row); the dense tails reuse gemm_tc.cuh.
+#pragma once
+#include "ptx.cuh"
+
+namespace sffn {
+
+constexpr int HMM_WARPS = 4;
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ float dot8_bf16(const uint4& a, const uint4& b) {
+    float s = bf16_lo(a.x) * bf16_lo(b.x);
+    s = fmaf(bf16_hi(a.x), bf16_hi(b.x), s);
+    s = fmaf(bf16_lo(a.y), bf16_lo(b.y), s);
+    s = fmaf(bf16_hi(a.y), bf16_hi(b.y), s);
+    s = fmaf(bf16_lo(a.z), bf16_lo(b.z), s);
+    s = fmaf(bf16_hi(a.z), bf16_hi(b.z), s);
+    s = fmaf(bf16_lo(a.w), bf16_lo(b.w), s);
+    return fmaf(bf16_hi(a.w), bf16_hi(b.w), s);
+}
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+// SDDMM, ELL rows (row_loc == -1): one CTA per row, warps over the row's entries, lanes over K in 16-byte chunks
+// (A row and the entry's B row both 128-bit loads), fp32 FMA, warp shuffle reduction (Listing 5);
+// out = bf16(g * dot), g = the pattern value (gate) or 1.
+__global__ void __launch_bounds__(HMM_WARPS * 32)
+    hybrid_sddmm_ell_kernel(const uint4* __restrict__ A, const uint4* __restrict__ B, int K8, int ell_w,
+                            const int16_t* __restrict__ ell_col, const int32_t* __restrict__ row_nnz,
+                            const int32_t* __restrict__ row_loc, const uint16_t* __restrict__ P_ell, int gate,
+                            uint16_t* __restrict__ out_ell) {
+    const int64_t m = blockIdx.x;
+    if (__ldg(row_loc + m) != -1) return;
+    const int z = min(__ldg(row_nnz + m), ell_w);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint4* a = A + m * K8;
+    for (int j = warp; j < z; j += HMM_WARPS) {
+        const int64_t n = static_cast<uint16_t>(__ldg(ell_col + m * ell_w + j));
+        const uint4* b = B + n * K8;
+        float acc = 0.f;
+#pragma unroll 4
+        for (int c = lane; c < K8; c += 32) acc += dot8_bf16(__ldg(a + c), __ldg(b + c));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) {
+            const float g = gate ? __uint_as_float(static_cast<uint32_t>(__ldg(P_ell + m * ell_w + j)) << 16) : 1.f;
+            out_ell[m * ell_w + j] = f32_to_bf16_bits(g * acc);
+        }
+    }
+}
+
+// SDDMM dense tail: out[s, n] = P[s, n] != 0 ? bf16(g * S[s, n]) : 0 for s < min(*count, D) (S = the fp32 GEMM of
+// the gathered A rows with B), g = P (gate) or 1 — the mask of Alg.3's dense portion.
+__global__ void hybrid_tail_mask_kernel(const float* __restrict__ S, const uint16_t* __restrict__ P, int64_t N,
+                                        const int* __restrict__ count, int D, int gate, uint16_t* __restrict__ out) {
+    const int64_t rows = min(D, __ldg(count));
+    const int64_t tot = rows * N;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < tot;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t p = __ldg(P + i);
+        const float pf = __uint_as_float(p << 16);
+        out[i] = pf != 0.f ? f32_to_bf16_bits((gate ? pf : 1.f) * __ldg(S + i)) : uint16_t(0);
+    }
+}
+
+// SpMM, ELL rows: one CTA per row; each thread owns HMM_CH 8-column chunks of the output row in fp32 registers and
+// sweeps the row's entries once, loading 16 bytes of W[col, :] per chunk (Listing 6); bf16 16-byte stores.
+// Rows with row_loc == -2 (dropped) are written as zeros; dense-tail rows are left to the tail GEMM.
+constexpr int HMM_CH = 4;
+__global__ void __launch_bounds__(128)
+    hybrid_spmm_ell_kernel(const uint16_t* __restrict__ ell_val, const int16_t* __restrict__ ell_col,
+                           const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ row_loc, int ell_w,
+                           const uint4* __restrict__ W, int K8, uint4* __restrict__ Y) {
+    const int64_t m = blockIdx.x;
+    const int loc = __ldg(row_loc + m);
+    if (loc >= 0) return;
+    uint4* y = Y + m * K8;
+    if (loc == -2) {
+        for (int c = threadIdx.x; c < K8; c += blockDim.x) y[c] = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const int z = min(__ldg(row_nnz + m), ell_w);
+    for (int c0 = threadIdx.x; c0 < K8; c0 += blockDim.x * HMM_CH) {
+        float acc[HMM_CH][8];
+#pragma unroll
+        for (int q = 0; q < HMM_CH; ++q)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
+        for (int j = 0; j < z; ++j) {
+            const float v = __uint_as_float(static_cast<uint32_t>(__ldg(ell_val + m * ell_w + j)) << 16);
+            const int64_t n = static_cast<uint16_t>(__ldg(ell_col + m * ell_w + j));
+            const uint4* w = W + n * K8;
+#pragma unroll
+            for (int q = 0; q < HMM_CH; ++q) {
+                const int c = c0 + q * blockDim.x;
+                if (c < K8) {
+                    const uint4 b = __ldg(w + c);
+                    const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        acc[q][2 * i] = fmaf(v, bf16_lo(bw[i]), acc[q][2 * i]);
+                        acc[q][2 * i + 1] = fmaf(v, bf16_hi(bw[i]), acc[q][2 * i + 1]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < HMM_CH; ++q) {
+            const int c = c0 + q * blockDim.x;
+            if (c < K8)
+                y[c] = make_uint4(pack_bf16x2(acc[q][0], acc[q][1]), pack_bf16x2(acc[q][2], acc[q][3]),
+                                  pack_bf16x2(acc[q][4], acc[q][5]), pack_bf16x2(acc[q][6], acc[q][7]));
+        }
+    }
+}
+
+}  // namespace sffn

@@ -17,6 +17,7 @@
 #include "gemm_union.cuh"
 #include "gemm_union_pair.cuh"
 #include "hybrid.cuh"
+#include "hybrid_mm.cuh"
 #include "updown.cuh"
 
 using namespace sffn;
@@ -961,6 +962,100 @@ int sffn_twell_to_hybrid(const uint32_t* twell, int64_t M, int64_t N, int T, int
     { twell_to_hybrid_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, S(stream)>>>(
         twell, (int)M, (int)N, T, C, ell_w, static_cast<uint16_t*>(ell_val), ell_col, row_nnz, row_loc,
         (int)dense_cap, static_cast<uint16_t*>(dense_rows), dense_map, d_dense_count, d_l0l1); note_launch(); }
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- training forward on the hybrid format (NEXT-4)
+size_t sffn_hybrid_mm_workspace_bytes(int64_t D, int64_t K, int64_t N) {
+    if (D < 0 || K <= 0 || N <= 0) return 0;
+    const int64_t Dp = ((D + 127) / 128) * 128;
+    const int64_t sddmm = align1k(Dp * K * 2) + align1k(Dp * N * 4);
+    return static_cast<size_t>(std::max<int64_t>(sddmm, align1k(Dp * K * 2)));
+}
+
+int sffn_hybrid_sddmm(const void* A, const void* B, int64_t M, int64_t K, int64_t N, int ell_w, const int16_t* ell_col,
+                      const int32_t* row_nnz, const int32_t* row_loc, const void* P_ell, int64_t D,
+                      const int32_t* dense_map, const int* d_dense_count, const void* P_dense, int gate, void* out_ell,
+                      void* out_dense, void* workspace, size_t ws_bytes, void* stream) {
+    if (M < 0 || D < 0 || ell_w < 1 || K < 64 || K % 64 != 0 || N < 16 || N % 16 != 0 || N > 65536)
+        return SFFN_ERR_SHAPE;
+    if (M == 0) return SFFN_OK;
+    if (!A || !B || !ell_col || !row_nnz || !row_loc || !out_ell || (gate && !P_ell)) return SFFN_ERR_INVALID_ARG;
+    if (D > 0 && (!dense_map || !d_dense_count || !P_dense || !out_dense || !workspace)) return SFFN_ERR_INVALID_ARG;
+    if (!aligned16(A) || !aligned16(B)) return SFFN_ERR_INVALID_ARG;
+    if (D > 0 && ws_bytes < sffn_hybrid_mm_workspace_bytes(D, K, N)) return SFFN_ERR_SHAPE;
+    if (D > 0 && N < GEMM_BN) return SFFN_ERR_SHAPE;  // the tail GEMM's B box is 256 rows
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    cudaStream_t st = S(stream);
+    { hybrid_sddmm_ell_kernel<<<static_cast<unsigned>(M), HMM_WARPS * 32, 0, st>>>(
+        static_cast<const uint4*>(A), static_cast<const uint4*>(B), (int)(K / 8), ell_w, ell_col, row_nnz, row_loc,
+        static_cast<const uint16_t*>(P_ell), gate, static_cast<uint16_t*>(out_ell)); note_launch(); }
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    if (D == 0) return SFFN_OK;
+    // dense tail: gather the tail rows of A, fp32 tcgen05 GEMM against B, mask (and gate) by the pattern
+    const int64_t Dp = ((D + 127) / 128) * 128;
+    uint8_t* w = static_cast<uint8_t*>(workspace);
+    void* Ad = w;
+    float* S32 = reinterpret_cast<float*>(w + align1k(Dp * K * 2));
+    const unsigned g = static_cast<unsigned>((Dp * 32 + 255) / 256);
+    { move_rows_kernel<true><<<g, 256, 0, st>>>(static_cast<const uint4*>(A), static_cast<uint4*>(Ad), dense_map,
+                                              d_dense_count, (int)D, (int)(K / 8)); note_launch(); }
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    CUtensorMap ta, tb;
+    if (!tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Ad, K, Dp, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, K, N, GEMM_BK, GEMM_BN, CU_TENSOR_MAP_SWIZZLE_128B))
+        return SFFN_ERR_CUDA;
+    GemmArgs ga{};
+    ga.M = (int)Dp;
+    ga.N = (int)N;
+    ga.K = (int)K;
+    ga.out_f32 = S32;
+    ga.ld_out = N;
+    ga.m_dev = d_dense_count;
+    if ((r = launch_gemm<EPI_F32, 1>(ta, tb, tb, tb, ga, GEMM_BN, st)) != SFFN_OK) return r;
+    { hybrid_tail_mask_kernel<<<dev_info().sms * 4, 256, 0, st>>>(S32, static_cast<const uint16_t*>(P_dense), N,
+                                                                 d_dense_count, (int)D, gate,
+                                                                 static_cast<uint16_t*>(out_dense)); note_launch(); }
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_hybrid_spmm(const void* ell_val, const int16_t* ell_col, const int32_t* row_nnz, const int32_t* row_loc,
+                     int64_t M, int ell_w, int64_t D, const int32_t* dense_map, const int* d_dense_count,
+                     const void* dense, const void* W, int64_t N, int64_t K, void* Y, void* workspace, size_t ws_bytes,
+                     void* stream) {
+    if (M < 0 || D < 0 || ell_w < 1 || K < 256 || K % 64 != 0 || N < 64 || N % 64 != 0 || N > 65536)
+        return SFFN_ERR_SHAPE;
+    if (M == 0) return SFFN_OK;
+    if (!ell_val || !ell_col || !row_nnz || !row_loc || !W || !Y) return SFFN_ERR_INVALID_ARG;
+    if (D > 0 && (!dense_map || !d_dense_count || !dense || !workspace)) return SFFN_ERR_INVALID_ARG;
+    if (!aligned16(W) || !aligned16(Y)) return SFFN_ERR_INVALID_ARG;
+    if (D > 0 && ws_bytes < sffn_hybrid_mm_workspace_bytes(D, K, N)) return SFFN_ERR_SHAPE;
+    int r = check_device();
+    if (r != SFFN_OK) return r;
+    cudaStream_t st = S(stream);
+    { hybrid_spmm_ell_kernel<<<static_cast<unsigned>(M), 128, 0, st>>>(
+        static_cast<const uint16_t*>(ell_val), ell_col, row_nnz, row_loc, ell_w, static_cast<const uint4*>(W),
+        (int)(K / 8), static_cast<uint4*>(Y)); note_launch(); }
+    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    if (D == 0) return SFFN_OK;
+    // dense tail: tcgen05 GEMM of the tail rows with W (read MN-major by TMA), rows scattered to Y[dense_map[s]]
+    const int64_t Dp = ((D + 127) / 128) * 128;
+    void* Yd = workspace;
+    CUtensorMap th, tw, ty;
+    if (!tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dense, N, D, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W, K, N, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Yd, K, Dp, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return SFFN_ERR_CUDA;
+    GemmArgs ga{};
+    ga.M = (int)Dp;
+    ga.N = (int)K;
+    ga.K = (int)N;
+    ga.m_dev = d_dense_count;
+    if ((r = launch_gemm<EPI_BF16_MN, 1>(th, tw, tw, ty, ga, GEMM_BN, st)) != SFFN_OK) return r;
+    const unsigned g = static_cast<unsigned>((Dp * 32 + 255) / 256);
+    { move_rows_kernel<false><<<g, 256, 0, st>>>(static_cast<const uint4*>(Yd), static_cast<uint4*>(Y), dense_map,
+                                               d_dense_count, (int)D, (int)(K / 8)); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 

@@ -63,6 +63,11 @@ _SIGS = {
     "sffn_allreduce_sym_bf16": (_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "sffn_sharded_forward_sym": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
                                         _int, _vp]),
+    "sffn_hybrid_mm_workspace_bytes": (_sz, [_i64, _i64, _i64]),
+    "sffn_hybrid_sddmm": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _int, _vp,
+                                 _vp, _vp, _sz, _vp]),
+    "sffn_hybrid_spmm": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _sz,
+                                _vp]),
     "sffn_launch_count": (_i64, []),
     "sffn_union_block_rows": (_int, []),
     "sffn_forward_host": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _sz, _vp, _int,
@@ -272,6 +277,41 @@ def twell_to_hybrid(tw, N: int, T: int = 256, C: int = 8, ell_w: int = 128, dens
                                     _p(out["row_nnz"]), _p(out["row_loc"]), D, _p(out["dense_rows"]),
                                     _p(out["dense_map"]), _p(out["dense_count"]), _p(out["l0l1"]), _stream(stream)),
          "sffn_twell_to_hybrid")
+    return out
+
+
+def hybrid_sddmm(a, b, hyb: dict, gate: bool = True, workspace=None, stream=None) -> dict:
+    """Training forward, dense -> hybrid (Listing 5 + Alg.3): h = g (.) a b^T on the pattern of `hyb` (a dict from
+    twell_to_hybrid), g = the pattern values (gate=True) or its 0/1 mask.  Returns a hybrid dict with the same
+    pattern arrays and new "ell_val" / "dense_rows"."""
+    M, K = a.shape
+    N = b.shape[0]
+    ell_w = hyb["ell_col"].shape[1]
+    D = hyb["dense_map"].shape[0]
+    out = dict(hyb)
+    out["ell_val"] = torch.zeros_like(hyb["ell_val"])
+    out["dense_rows"] = torch.zeros_like(hyb["dense_rows"])
+    workspace = _ws(int(lib().sffn_hybrid_mm_workspace_bytes(D, K, N)), a.device, workspace)
+    _chk(lib().sffn_hybrid_sddmm(_bf16(a, "a"), _bf16(b, "b"), M, K, N, ell_w, _p(hyb["ell_col"]), _p(hyb["row_nnz"]),
+                                 _p(hyb["row_loc"]), _p(hyb["ell_val"]), D, _p(hyb["dense_map"]),
+                                 _p(hyb["dense_count"]), _p(hyb["dense_rows"]), 1 if gate else 0, _p(out["ell_val"]),
+                                 _p(out["dense_rows"]), _p(workspace), workspace.numel() * workspace.element_size(),
+                                 _stream(stream)), "sffn_hybrid_sddmm")
+    return out
+
+
+def hybrid_spmm(hyb: dict, w, out=None, workspace=None, stream=None) -> torch.Tensor:
+    """Training forward, hybrid -> dense (Listing 6 + Alg.3): Y = h W for the hybrid h and W [N, K] (hidden-major)."""
+    M, ell_w = hyb["ell_col"].shape
+    N, K = w.shape
+    D = hyb["dense_map"].shape[0]
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=w.device)
+    workspace = _ws(int(lib().sffn_hybrid_mm_workspace_bytes(D, K, N)), w.device, workspace)
+    _chk(lib().sffn_hybrid_spmm(_p(hyb["ell_val"]), _p(hyb["ell_col"]), _p(hyb["row_nnz"]), _p(hyb["row_loc"]), M,
+                                ell_w, D, _p(hyb["dense_map"]), _p(hyb["dense_count"]), _p(hyb["dense_rows"]),
+                                _bf16(w, "w"), N, K, _bf16(out, "out"), _p(workspace),
+                                workspace.numel() * workspace.element_size(), _stream(stream)), "sffn_hybrid_spmm")
     return out
 
 

@@ -599,3 +599,47 @@ def test_launch_count(sffn, algo, expected):
     sffn.forward(X, Wg, Wu, Wd, 256, 8, algo=algo)
     torch.cuda.synchronize()
     assert sffn.launch_count() - c0 == expected
+
+
+# ----------------------------------------------------------------- training forward on the hybrid format (NEXT-4)
+@pytest.mark.parametrize("dense_cap", [256, 4])
+def test_hybrid_training_forward(sffn, dense_cap):
+    """pack -> twell_to_hybrid -> SDDMM h = h_g (.) x W_u on the pattern (Listing 5 + masked tcgen05 tail) -> SpMM
+    y = h W_d (Listing 6 + tcgen05 tail scattered to the tail rows): SDDMM element-wise within one bf16 rounding of
+    the oracle, SpMM within 1e-2 of the oracle on the same hybrid input, the chain within 1e-2 of Eq.3 (stored
+    gate) on every non-dropped row; dropped rows (tail full) are zero."""
+    cfg = synth.CONFIGS["1B"].replace(M=900, K=512, N=2048, Kb=16, sparsity=0.97)
+    X, Wg, Wu, Wd = inputs(cfg)
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    tw = sffn.pack(to_dev(X), to_dev(Wg), cfg.T, cfg.C)
+    ell_w = 24
+    hyb = sffn.twell_to_hybrid(tw, cfg.N, cfg.T, cfg.C, ell_w=ell_w, dense_cap=dense_cap)
+    h = sffn.hybrid_sddmm(to_dev(X), to_dev(Wu), hyb, gate=True)
+    Y = sffn.hybrid_spmm(h, to_dev(Wd))
+    torch.cuda.synchronize()
+    col = hyb["ell_col"].cpu().numpy()
+    nnz = hyb["row_nnz"].cpu().numpy()
+    loc = hyb["row_loc"].cpu().numpy()
+    nd = min(int(hyb["dense_count"].item()), dense_cap)
+    dmap = hyb["dense_map"].cpu().numpy()[:nd]
+    assert nd > 0 and (loc == -1).sum() > 0
+    if dense_cap == 4:
+        assert (loc == -2).any()
+    P_ell = hyb["ell_val"].cpu().view(torch.int16).numpy().view(np.uint16)
+    P_dense = hyb["dense_rows"].cpu().view(torch.int16).numpy().view(np.uint16)[:nd]
+    ref_ell, ref_dense = oracle.hybrid_sddmm(X, Wu, col, nnz, loc, P_ell, dmap, P_dense, True)
+    g_ell = h["ell_val"].float().cpu().numpy().astype(np.float64)
+    g_dense = h["dense_rows"].float().cpu().numpy().astype(np.float64)[:nd]
+    for m in np.flatnonzero(loc == -1):
+        z = min(nnz[m], ell_w)
+        assert (np.abs(g_ell[m, :z] - ref_ell[m, :z]) <= 2.0 ** -8 * np.abs(ref_ell[m, :z]) + 1e-30).all(), m
+    assert (np.abs(g_dense - ref_dense) <= 2.0 ** -8 * np.abs(ref_dense) + 1e-30).all()
+    y = bf16_np(Y)
+    # SpMM against the oracle on the GPU's own bf16 SDDMM output, and the whole chain against the fp64 oracle chain
+    assert rel_fro(y, oracle.hybrid_spmm(g_ell, col, nnz, loc, dmap, g_dense, Wd)) < Y_TOL
+    chain = oracle.hybrid_spmm(ref_ell, col, nnz, loc, dmap, ref_dense, Wd)
+    assert rel_fro(y, chain) < Y_TOL
+    keep = loc != -2
+    eq3 = oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)
+    assert rel_fro(y[keep], eq3[keep]) < Y_TOL
+    assert (y[~keep] == 0).all()

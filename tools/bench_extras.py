@@ -42,10 +42,18 @@ res["hybrid_forward_ms"] = t(lambda: sffn.forward_hybrid(X, Wg, Wu, Wd, T, C, ba
                                                          backup_count=cnt))
 res["hybrid_backup_rows_used"] = int(cnt.item())
 tw = sffn.pack(X, Wg, T, C)
-res["twell_to_hybrid_ms"] = t(lambda: sffn.twell_to_hybrid(tw, N, T, C, ell_w=128, dense_cap=M // 8))
-h = sffn.twell_to_hybrid(tw, N, T, C, ell_w=128, dense_cap=M // 8)
+ELL_W = 384  # ~2.7x the mean row occupancy: the heavy-tailed rows beyond it fit the M/8 dense tail (P:1611 sizing)
+res["hybrid_ell_w"] = ELL_W
+res["twell_to_hybrid_ms"] = t(lambda: sffn.twell_to_hybrid(tw, N, T, C, ell_w=ELL_W, dense_cap=M // 8))
+h = sffn.twell_to_hybrid(tw, N, T, C, ell_w=ELL_W, dense_cap=M // 8)
 res["twell_to_hybrid_l0_l1"] = h["l0l1"].cpu().tolist()
 res["twell_to_hybrid_dense_rows"] = int(h["dense_count"].item())
+# training forward on the hybrid format (NEXT-4): SDDMM h = h_g (.) x W_u on the pattern, SpMM y = h W_d
+hws2 = torch.empty(int(sffn.sffn.lib().sffn_hybrid_mm_workspace_bytes(M // 8, K, N)), dtype=torch.uint8, device="cuda")
+hh = sffn.hybrid_sddmm(X, Wu, h, gate=True, workspace=hws2)
+res["hybrid_sddmm_ms"] = t(lambda: sffn.hybrid_sddmm(X, Wu, h, gate=True, workspace=hws2))
+res["hybrid_spmm_ms"] = t(lambda: sffn.hybrid_spmm(hh, Wd, out=Y, workspace=hws2))
+res["hybrid_train_fwd_ms"] = res["twell_to_hybrid_ms"] + res["hybrid_sddmm_ms"] + res["hybrid_spmm_ms"]
 # fp32 mode (correctness mode; SIMT fp32 GEMM) on a row slice to bound the time
 Mf = min(M, 4096)
 Xf = torch.from_numpy(synth.gen_x(cfg, 0, Mf, dtype="f32", p=p)).cuda()

@@ -18,7 +18,9 @@ for algo in ("gather", "union"):
     sffn.forward_hybrid(X, Wg, Wu, Wd, 256, 8, backup_rows=128, algo=algo)
 sffn.dense_forward(X, Wg, Wu, sffn.transpose(Wd))
 sffn.gate_gemm_f32(X, Wg)
-sffn.twell_to_hybrid(tw, cfg.N, 256, 8, ell_w=16, dense_cap=64)
+hyb = sffn.twell_to_hybrid(tw, cfg.N, 256, 8, ell_w=16, dense_cap=64)
+hh = sffn.hybrid_sddmm(X, Wu, hyb, gate=True)
+sffn.hybrid_spmm(hh, Wd)
 f = lambda a: a.float().contiguous()
 sffn.forward_f32(f(X), f(Wg), f(Wu), f(Wd), 256, 8)
 xh = X.cpu().pin_memory()
