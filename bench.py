@@ -368,7 +368,8 @@ def main():
         Xh = torch.from_numpy(X_host.view(np.int16)).view(torch.bfloat16).pin_memory()
         Yh = torch.empty((M, K), dtype=torch.bfloat16).pin_memory()
         rows = min(args.e2e_chunk, M)
-        ws_h = torch.empty(sffn.workspace_bytes(rows, K, Nl, T, C, args.algo), dtype=torch.uint8, device=dev)
+        wsz = sffn.workspace_bytes(rows, K, Nl, T, C, args.algo)  # two: chunks alternate two compute streams
+        ws_h = torch.empty((wsz + 1023) // 1024 * 1024 + wsz, dtype=torch.uint8, device=dev)
         stage = torch.empty(int(sffn.sffn.lib().sffn_forward_host_stage_bytes(K, ((rows + 127) // 128) * 128)),
                             dtype=torch.uint8, device=dev)
 

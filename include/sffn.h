@@ -177,7 +177,9 @@ int sffn_forward_nongated(const void* X, const void* Wu, const void* Wd, int64_t
  * streams (created once per device, event-ordered; no host synchronization).  The call is
  * stream-ordered on `stream`: Y_host is complete when `stream` reaches this point.
  *   stage: device buffer >= sffn_forward_host_stage_bytes(K, chunk_rows) (2 X + 2 Y chunk slots)
- *   workspace: >= sffn_forward_workspace_bytes(min(chunk_rows, M), K, N, T, C, algo)
+ *   workspace: >= sffn_forward_workspace_bytes(min(chunk_rows, M), K, N, T, C, algo); with twice that (plus 1 KiB
+ *     alignment) consecutive chunks compute on two streams (`stream` and an internal one) so a chunk's kernels
+ *     overlap the previous chunk's tail
  */
 size_t sffn_forward_host_stage_bytes(int64_t K, int64_t chunk_rows);
 /* The chunk schedule sffn_forward_host uses (host only, no device work): writes up to `cap` chunk row

@@ -749,7 +749,7 @@ int sffn_forward_f32(const float* X, const float* Wg, const float* Wu, const flo
 // ---------------------------------------------------------------- host-buffer forward (copy/compute overlap)
 namespace {
 struct CopyStreams {
-    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp = nullptr;  // comp: second compute stream of forward_host
 };
 std::mutex g_cs_mu;
 CopyStreams g_cs[64];
@@ -760,6 +760,7 @@ int copy_streams(int dev, CopyStreams* out) {
     if (!c.h2d) {
         if (cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking) != cudaSuccess) return SFFN_ERR_CUDA;
         if (cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking) != cudaSuccess) return SFFN_ERR_CUDA;
+        if (cudaStreamCreateWithFlags(&c.comp, cudaStreamNonBlocking) != cudaSuccess) return SFFN_ERR_CUDA;
     }
     *out = c;
     return SFFN_OK;
@@ -820,7 +821,8 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     if (M == 0) return SFFN_OK;
     const int64_t rows = chunk_rows < M ? chunk_rows : ((M + 127) / 128) * 128;
     if (stage_bytes < sffn_forward_host_stage_bytes(K, rows)) return SFFN_ERR_SHAPE;
-    if (ws_bytes < sffn_forward_workspace_bytes(rows < M ? rows : M, K, N, T, C, algo)) return SFFN_ERR_SHAPE;
+    const size_t wsz = sffn_forward_workspace_bytes(rows < M ? rows : M, K, N, T, C, algo);
+    if (ws_bytes < wsz) return SFFN_ERR_SHAPE;
     int r = check_device();
     if (r != SFFN_OK) return r;
     int dev = 0;
@@ -828,6 +830,12 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     CopyStreams cs;
     if ((r = copy_streams(dev, &cs)) != SFFN_OK) return r;
     cudaStream_t st = S(stream);
+    // two workspaces -> consecutive chunks compute on two streams (`stream` and an internal one), so the kernels of
+    // chunk i+1 start on the SMs that chunk i's persistent kernels release in their tails
+    const size_t wsz1k = static_cast<size_t>(align1k(static_cast<int64_t>(wsz)));
+    const bool dual = ws_bytes >= wsz1k + wsz;
+    cudaStream_t cst[2] = {st, dual ? cs.comp : st};
+    uint8_t* wss[2] = {static_cast<uint8_t*>(workspace), static_cast<uint8_t*>(workspace) + (dual ? wsz1k : 0)};
     // chunk schedule: ramp up / down in size at the ends (short pipeline fill and drain), full chunks between
     std::vector<int64_t> sizes = host_chunk_plan(M, rows);
     const int64_t nchunks = static_cast<int64_t>(sizes.size());
@@ -843,6 +851,7 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     cudaEventRecord(ev.back(), st);
     cudaStreamWaitEvent(cs.h2d, ev.back(), 0);
     cudaStreamWaitEvent(cs.d2h, ev.back(), 0);
+    if (dual) cudaStreamWaitEvent(cs.comp, ev.back(), 0);
     int64_t r0 = 0;
     for (int64_t i = 0; i < nchunks && r == SFFN_OK; r0 += sizes[static_cast<size_t>(i)], ++i) {
         const int64_t mr = sizes[static_cast<size_t>(i)];
@@ -852,11 +861,12 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
         if (cudaMemcpyAsync(xs[sl], static_cast<const uint8_t*>(X_host) + r0 * K * 2, bytes, cudaMemcpyHostToDevice,
                             cs.h2d) != cudaSuccess) { r = SFFN_ERR_CUDA; break; }
         cudaEventRecord(E(0, i), cs.h2d);
-        cudaStreamWaitEvent(st, E(0, i), 0);
-        if (i >= 2) cudaStreamWaitEvent(st, E(2, i - 2), 0);  // Y slot free once chunk i-2 copied out
-        r = sffn_forward(xs[sl], Wg, Wu, Wd, mr, K, N, T, C, ys[sl], workspace, ws_bytes, d_overflow, algo, stream);
+        cudaStream_t cs_i = cst[sl];  // chunk i-2 used the same stream and workspace half: ordered
+        cudaStreamWaitEvent(cs_i, E(0, i), 0);
+        if (i >= 2) cudaStreamWaitEvent(cs_i, E(2, i - 2), 0);  // Y slot free once chunk i-2 copied out
+        r = sffn_forward(xs[sl], Wg, Wu, Wd, mr, K, N, T, C, ys[sl], wss[sl], wsz, d_overflow, algo, cs_i);
         if (r != SFFN_OK) break;
-        cudaEventRecord(E(1, i), st);
+        cudaEventRecord(E(1, i), cs_i);
         cudaStreamWaitEvent(cs.d2h, E(1, i), 0);
         if (cudaMemcpyAsync(static_cast<uint8_t*>(Y_host) + r0 * K * 2, ys[sl], bytes, cudaMemcpyDeviceToHost,
                             cs.d2h) != cudaSuccess) { r = SFFN_ERR_CUDA; break; }

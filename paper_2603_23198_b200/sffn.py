@@ -233,7 +233,9 @@ def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspa
         out = torch.empty((M, K), dtype=torch.bfloat16, pin_memory=True)
     a = _algo(algo)
     rows = min(chunk_rows, ((M + 127) // 128) * 128)
-    workspace = _ws(workspace_bytes(min(rows, M), K, N, T, C, a), wg.device, workspace)
+    wsz = workspace_bytes(min(rows, M), K, N, T, C, a)
+    # two workspaces: consecutive chunks compute on two streams (sffn_forward_host)
+    workspace = _ws((wsz + 1023) // 1024 * 1024 + wsz, wg.device, workspace)
     stage = _ws(int(lib().sffn_forward_host_stage_bytes(K, rows)), wg.device, stage)
     _chk(lib().sffn_forward_host(ctypes.c_void_p(x_host.data_ptr()), _bf16(wg, "wg"), _bf16(wu, "wu"),
                                  _bf16(wd, "wd"), M, K, N, T, C, ctypes.c_void_p(out.data_ptr()), _p(workspace),

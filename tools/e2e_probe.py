@@ -40,7 +40,14 @@ for rows in (2048, 4096, 8192):
     xr, yr = X[:rows], Yd[:rows]
     t = tim(lambda: sffn.forward(xr, Wg, Wu, Wd, T, C, out=yr, workspace=ws, algo="union"))
     print(f"forward M={rows}: {t:.3f} ms  (x{M//rows} = {t*M/rows:.2f} ms)")
-for rows in (4096, 8192, 16384):
-    wsh = None
-    t = tim(lambda: sffn.forward_host(Xh, Wg, Wu, Wd, T, C, out=Yh, algo="union", chunk_rows=rows), n=5)
-    print(f"forward_host chunk={rows}: {t:.3f} ms = {M/t/1e3:.3f} M tok/s")
+rows = 4096
+wsz = sffn.workspace_bytes(rows, K, N, T, C, "union")
+wsd = {False: torch.empty(wsz, dtype=torch.uint8, device="cuda"),
+       True: torch.empty((wsz + 1023) // 1024 * 1024 + wsz, dtype=torch.uint8, device="cuda")}
+res = {False: [], True: []}
+for rnd in range(6):
+    for dual in ((False, True) if rnd % 2 == 0 else (True, False)):
+        res[dual].append(tim(lambda: sffn.forward_host(Xh, Wg, Wu, Wd, T, C, out=Yh, workspace=wsd[dual], algo="union",
+                                                       chunk_rows=rows), n=3))
+for dual in (False, True):
+    print(f"forward_host chunk={rows} dual={dual}: median {np.median(res[dual]):.3f} ms  {[round(x, 3) for x in res[dual]]}")
