@@ -383,6 +383,32 @@ def main():
                "d2h_bytes_per_step": int(Yh.numel() * 2), "ms_per_step": t_e / len(ms_e) * 1e3,
                "api": f"sffn_forward_host (pinned host X/Y, chunks of {args.e2e_chunk} rows, copy/compute overlap)"}
         del ws_h, stage
+    elif not args.no_e2e and world > 1:
+        # N > 1: every rank copies X from pinned host memory, runs the sharded forward through the public API
+        # (Comm.sharded_forward / sharded_forward_sym), and copies Y back; copies inside the timed region (serial,
+        # no overlap); max over ranks as for `value`
+        Xh = torch.from_numpy(X_host.view(np.int16)).view(torch.bfloat16).pin_memory()
+        Yh = torch.empty((M, K), dtype=torch.bfloat16).pin_memory()
+        Xd = torch.empty_like(X)
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            if allreduce.startswith("sym"):
+                comm.sharded_forward_sym(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
+            else:
+                comm.sharded_forward(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo,
+                                     n_chunks=args.chunks)
+            Yh.copy_(Y, non_blocking=True)
+
+        ms_e = timed(e2e_step, max(3, args.steps // 3), 3)
+        t_e = float(np.sum(ms_e)) / 1e3
+        tt = torch.tensor([t_e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e = float(tt.item())
+        e2e = {"value": M * len(ms_e) / t_e, "unit": "tokens/s", "h2d_bytes_per_step": int(Xh.numel() * 2),
+               "d2h_bytes_per_step": int(Yh.numel() * 2), "ms_per_step": t_e / len(ms_e) * 1e3,
+               "api": "Comm.sharded_forward on every rank with X copied in from pinned host memory and Y copied out "
+                      "(serial copies; per-rank bytes)"}
 
     # ------------------------------------------------------------------ CPU oracle baseline
     cpu = None
