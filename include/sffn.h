@@ -326,6 +326,12 @@ int sffn_comm_symmetric_init(sffn_comm* comm, int64_t max_rows, int64_t K);
 /* multimem = 1 when the NVLS (multicast) reduction is used, 0 for P2P loads / stores. */
 int sffn_comm_symmetric_info(const sffn_comm* comm, int* multimem, int64_t* max_rows, int64_t* K);
 int sffn_allreduce_sym_bf16(sffn_comm* comm, const void* src, void* Y, int64_t rows, int64_t K, void* stream);
+/* Reduce-scatter variant (sequence-parallel consumers): rank r receives the sum over ranks of rows
+ * [rows*r/G, rows*(r+1)/G) of the partials (src copied into the window first unless NULL) in Y_slice
+ * [*nrows, K] bf16; *row0 / *nrows (may be NULL) report the slice.  Same kernel structure as the all-reduce
+ * without the broadcast store. */
+int sffn_reduce_scatter_sym_bf16(sffn_comm* comm, const void* src, int64_t rows, int64_t K, void* Y_slice,
+                                 int64_t* row0, int64_t* nrows, void* stream);
 int sffn_sharded_forward_sym(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
                              int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
                              size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream);

@@ -53,6 +53,38 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Reduce-scatter variant (sequence-parallel consumers): rank r reduces its 1/G slice of rows
+// [row0, row1) from every window (multimem.ld_reduce, or P2P loads) and writes it only to its own output; one LSA
+// barrier before (partials complete everywhere) and one after (no rank overwrites its window, i.e. starts the next
+// forward, while a peer may still be reading it).
+__global__ void __launch_bounds__(SYM_THREADS) sym_reduce_scatter_kernel(ncclDevComm dc, ncclWindow_t win, int64_t q0,
+                                                                        int64_t q1, int nranks, int multimem,
+                                                                        uint4* Yr) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    if (multimem) {
+        const uint4* mc = static_cast<const uint4*>(ncclGetLsaMultimemPointer(win, 0, dc));
+        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
+            uint4 v;
+            asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "l"(mc + q)
+                         : "memory");
+            Yr[q - q0] = v;
+        }
+    } else {
+        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
+            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int p = 0; p < nranks; ++p)
+                bf16x8_acc(a, __ldcg(static_cast<const uint4*>(ncclGetLsaPointer(win, 0, p)) + q));
+            Yr[q - q0] = make_uint4(bf16x2_rn(a[0], a[1]), bf16x2_rn(a[2], a[3]), bf16x2_rn(a[4], a[5]),
+                                    bf16x2_rn(a[6], a[7]));
+        }
+    }
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
 __global__ void __launch_bounds__(SYM_THREADS) sym_allreduce_kernel(ncclDevComm dc, ncclWindow_t win, int64_t n16,
                                                                    int rank, int nranks, int multimem, uint4* Y) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
@@ -215,6 +247,27 @@ int sffn_allreduce_sym_bf16(sffn_comm* c, const void* src, void* Y, int64_t rows
         return SFFN_ERR_CUDA;
     sym_allreduce_kernel<<<SYM_CTAS, SYM_THREADS, 0, st>>>(c->dev, c->win, static_cast<int64_t>(bytes / 16), c->rank,
                                                            c->nranks, c->multimem ? 1 : 0, static_cast<uint4*>(Y));
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_reduce_scatter_sym_bf16(sffn_comm* c, const void* src, int64_t rows, int64_t K, void* Y_slice,
+                                  int64_t* row0, int64_t* nrows, void* stream) {
+    if (!c || rows < 0 || K < 8 || K % 8 != 0) return SFFN_ERR_INVALID_ARG;
+    if (!c->has_dev) return SFFN_ERR_UNSUPPORTED;
+    if (rows > c->sym_rows || K != c->sym_K) return SFFN_ERR_SHAPE;
+    // rank r owns rows [rows * r / G, rows * (r + 1) / G)
+    const int64_t r0 = rows * c->rank / c->nranks, r1 = rows * (c->rank + 1) / c->nranks;
+    if (row0) *row0 = r0;
+    if (nrows) *nrows = r1 - r0;
+    if (rows == 0) return SFFN_OK;
+    if (!Y_slice && r1 > r0) return SFFN_ERR_INVALID_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (src && src != c->sym_buf &&
+        cudaMemcpyAsync(c->sym_buf, src, static_cast<size_t>(rows) * K * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return SFFN_ERR_CUDA;
+    const int64_t k16 = K / 8;  // 16-byte chunks per row
+    sym_reduce_scatter_kernel<<<SYM_CTAS, SYM_THREADS, 0, st>>>(c->dev, c->win, r0 * k16, r1 * k16, c->nranks,
+                                                                c->multimem ? 1 : 0, static_cast<uint4*>(Y_slice));
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 

@@ -61,6 +61,7 @@ _SIGS = {
     "sffn_comm_symmetric_init": (_int, [_vp, _i64, _i64]),
     "sffn_comm_symmetric_info": (_int, [_vp, _vp, _vp, _vp]),
     "sffn_allreduce_sym_bf16": (_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "sffn_reduce_scatter_sym_bf16": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "sffn_sharded_forward_sym": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
                                         _int, _vp]),
     "sffn_hybrid_mm_workspace_bytes": (_sz, [_i64, _i64, _i64]),
@@ -488,6 +489,17 @@ class Comm:
         _chk(lib().sffn_allreduce_sym_bf16(self.h, _bf16(src, "src"), _bf16(out, "out"), rows, K, _stream(stream)),
              "sffn_allreduce_sym_bf16")
         return out
+
+    def reduce_scatter_sym(self, src, stream=None):
+        """This rank's row slice of the sum over ranks of `src` [rows, K] (NEXT-3 reduce-scatter variant)."""
+        rows, K = src.shape
+        r0, nr = ctypes.c_int64(), ctypes.c_int64()
+        n = rows * (self.rank + 1) // self.world - rows * self.rank // self.world
+        out = torch.empty((n, K), dtype=torch.bfloat16, device=src.device)
+        _chk(lib().sffn_reduce_scatter_sym_bf16(self.h, _bf16(src, "src"), rows, K, _p(out) if n else None,
+                                                ctypes.byref(r0), ctypes.byref(nr), _stream(stream)),
+             "sffn_reduce_scatter_sym_bf16")
+        return out, r0.value
 
     def sharded_forward_sym(self, x, wg_s, wu_s, wd_s, T=256, C=8, out=None, workspace=None, overflow=None,
                             algo="auto", stream=None):

@@ -320,6 +320,9 @@ def test_sharded_forward_symmetric_single_rank(sffn, algo):
         out = comm.allreduce_sym(src)
         torch.cuda.synchronize()
         assert torch.equal(out.view(torch.int16), src.view(torch.int16))
+        rs, r0 = comm.reduce_scatter_sym(src)  # G = 1: the whole buffer is this rank's slice
+        torch.cuda.synchronize()
+        assert r0 == 0 and torch.equal(rs.view(torch.int16), src.view(torch.int16))
         with pytest.raises(sffn.SffnError):
             comm.allreduce_sym(torch.zeros(2048, cfg.K, dtype=torch.bfloat16, device="cuda"))
     finally:
