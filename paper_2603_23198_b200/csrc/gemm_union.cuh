@@ -8,7 +8,7 @@
 // with G = 0 add exact zeros.  Both kernels are persistent warp-specialized tcgen05 GEMMs like
 // gemm_tc.cuh; the dense A operand comes by TMA, the weight rows of U_b are gathered by four producer
 // warps with 16-byte cp.async.cg into the 128-byte-swizzled UMMA layout (TMA tile::gather4 measured
-// ~70 SM cycles per instruction on B200 — 8x too slow to feed the tensor cores, profiles/r01):
+// ~70 SM cycles per instruction on B200 — 8x too slow to feed the tensor cores, tools/exp_gather4.cu):
 //   UP   B operand: W_u[U_b[256c + r], k0:k0+64]       K-major
 //   DOWN B operand: W_d[U_b[k0 + r], 256j:256j+256]     MN-major (4 x 64-column atoms)
 // cp.async completion is signalled with cp.async.mbarrier.arrive.noinc on the stage's full barrier.
@@ -33,29 +33,9 @@ struct UnionArgs {
     bf16_t* Y;            // DOWN: output [M, K]
 };
 
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t col, int32_t r0,
-                                            int32_t r1, int32_t r2, int32_t r3) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-        : "memory");
-}
-
-#ifndef UG_WPOL
-#define UG_WPOL 0
-#endif
-// gathered weight rows: optional L2 evict_last hint (UG_WPOL=1)
+// 16-byte cp.async of a gathered weight-row segment (L2 only: .cg); src_bytes < 16 zero-fills the rest
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-#if UG_WPOL
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
-                 "r"(src_bytes), "l"(pol)
-                 : "memory");
-#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-#endif
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -95,9 +75,6 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
 
 constexpr int UG_STAGES = 4;
 constexpr int UG_GPRE = 8;  // UP epilogue: gate entries per row prefetched before the accumulator wait
-#ifndef FENCE_CPASYNC
-#define FENCE_CPASYNC 1
-#endif
 #ifndef UG_NGW
 #define UG_NGW 8
 #endif
@@ -221,7 +198,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], dense ? GEMM_STAGE_BYTES : GEMM_A_BYTES);
                     tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
-                                UG_WPOL ? policy_evict_first() : policy_evict_last());
+                                policy_evict_last());
                     if (dense) {
                         uint8_t* bdst = stB + stage * GEMM_B_BYTES;
                         if (UP) {  // W_u rows [256 cj, 256 cj + 256), k-slice kb: K-major box {64, 256}
@@ -354,7 +331,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     // relaxed per-stage wait (an acquire wait invalidates the SM's L1 every k-block, hurting the
                     // gather warps' index loads); the cp.async data is complete when the stage's barrier flips
                     mbar_wait_relaxed(&full[stage], phase);
-                    if (FENCE_CPASYNC) fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+                    fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads (async proxy)
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
                     const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);

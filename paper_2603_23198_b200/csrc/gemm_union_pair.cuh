@@ -25,15 +25,6 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 
-#ifndef UGP_RELAY_FENCE
-#define UGP_RELAY_FENCE 1
-#endif
-#ifndef UGP_FULL_CLUSTER_WAIT
-#define UGP_FULL_CLUSTER_WAIT 0
-#endif
-#ifndef UGP_EXP
-#define UGP_EXP 0  // experiments only (wrong results): 1 = no B gathers, 2 = no epilogue work
-#endif
 constexpr int UGP_B_BYTES = GEMM_B_BYTES / 2;                 // this CTA's half of the B tile (16 KB)
 constexpr int UGP_STAGE = GEMM_A_BYTES + UGP_B_BYTES;         // 32 KB
 constexpr int UGP_STAGES = 6;
@@ -183,7 +174,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 const int nk = UP ? nk_up : len / GEMM_BK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait_relaxed(&gfull[stage], phase);  // per stage: no L1 invalidation
-                    if (UGP_RELAY_FENCE) fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+                    fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads (async proxy)
                     mbar_arrive_remote(full_leader + 8u * static_cast<uint32_t>(stage));
                     if (++stage == S) {
                         stage = 0;
@@ -224,7 +215,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
                         const int rr = 4 * UG_GW * i + 4 * gw + sub;
-                        if (nidx[i] >= 0 && UGP_EXP != 1)
+                        if (nidx[i] >= 0)
                             cp_async16(dst + rr * 128 + ((c8 ^ (rr & 7)) << 4),
                                        args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * GEMM_BK + 8 * c8, 16);
                     }
@@ -258,7 +249,6 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
                         const int r = 2 * UG_GW * i + 2 * gw + rsub;
-                        if (UGP_EXP != 1)
                         cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
                                    args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + (in ? col : 0), in ? 16 : 0);
                     }
@@ -295,8 +285,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
                 for (int kb = 0; kb < nk; ++kb) {
-                    if (UGP_FULL_CLUSTER_WAIT) mbar_wait_cluster(&full[stage], phase);
-                    else mbar_wait_relaxed(&full[stage], phase);  // per stage: no L1 invalidation
+                    mbar_wait_relaxed(&full[stage], phase);  // per stage: no L1 invalidation
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
                     const uint32_t b0 = smem_u32(stB + stage * UGP_B_BYTES);
@@ -349,11 +338,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             tc_fence_after();
             const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
             const uint32_t release = tempty_leader + 8u * static_cast<uint32_t>(acc);
-            if (UGP_EXP == 2) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_remote(release);
-            } else if constexpr (UP) {
+            if constexpr (UP) {
                 const int p0 = 256 * cj;
 #pragma unroll 1
                 for (int h = 0; h < 2 && 128 * h < len; ++h) {
