@@ -263,6 +263,17 @@ int sffn_forward_f32(const float* X, const float* Wg, const float* Wu, const flo
  *   rows are zero.  Requires K % 64 == 0, K >= 256, N % 64 == 0; workspace as above when D > 0.
  * Caller-owned device memory, stream-ordered, no host synchronization. */
 size_t sffn_hybrid_mm_workspace_bytes(int64_t D, int64_t K, int64_t N);
+/* sffn_forward_train — the training forward through the union tensor-core path: sffn_forward (algo UNION) gives
+ * Y, then the TwELL is converted to the hybrid format (as sffn_twell_to_hybrid: pattern, h_g values in
+ * ell_g / dense_g, dense_map, *d_dense_count zeroed by the caller, L0/L1) and h = h_g (.) x W_u — the values the
+ * SDDMM computes on that pattern, already in the union GEMM's H_c buffer — is copied out in the same hybrid
+ * layout (ell_h [M, ell_w], dense_h [dense_cap, N], bf16) for the backward pass.  One call instead of
+ * pack + SDDMM + SpMM; workspace >= sffn_forward_workspace_bytes(M, K, N, T, C, SFFN_ALGO_UNION); N % 64 == 0. */
+int sffn_forward_train(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                       int T, int C, void* Y, int ell_w, void* ell_g, void* ell_h, int16_t* ell_col, int32_t* row_nnz,
+                       int32_t* row_loc, int64_t dense_cap, void* dense_g, void* dense_h, int32_t* dense_map,
+                       int* d_dense_count, double* d_l0l1, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
+                       void* stream);
 int sffn_hybrid_sddmm(const void* A, const void* B, int64_t M, int64_t K, int64_t N, int ell_w, const int16_t* ell_col,
                       const int32_t* row_nnz, const int32_t* row_loc, const void* P_ell, int64_t D,
                       const int32_t* dense_map, const int* d_dense_count, const void* P_dense, int gate, void* out_ell,

@@ -120,4 +120,40 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// Training forward through the union tensor-core path (sffn_forward_train): after the union up/down, H_c holds
+// h = h_g (.) x W_u (bf16) for every stored (row, unit) at the row's union positions.  Warp per pi position p
+// (token row m = perm[p]): the row's compact gate list (ascending units = ascending union positions = the ELL
+// order of sffn_twell_to_hybrid) gives the positions; ELL rows: ell_h[m, j] = H_c[p, pos_j] for j < min(nnz, ell_w);
+// dense-tail rows (row_loc = s >= 0): dense_h[s, :] = 0, then dense_h[s, unit_j] = H_c[p, pos_j] (unit from the
+// block's union list).  Dropped rows (-2) are skipped.
+__global__ void union_h_to_hybrid_kernel(const uint16_t* __restrict__ hc, int M, int N, int brows,
+                                         const int32_t* __restrict__ perm, const uint32_t* __restrict__ glist,
+                                         const uint16_t* __restrict__ coff, int lmax, int nchunk,
+                                         const int32_t* __restrict__ ulist, const int32_t* __restrict__ row_nnz,
+                                         const int32_t* __restrict__ row_loc, int ell_w, uint16_t* __restrict__ ell_h,
+                                         uint16_t* __restrict__ dense_h) {
+    const int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= M) return;
+    const int64_t m = __ldg(perm + p);
+    const int loc = __ldg(row_loc + m);
+    if (loc == -2) return;
+    const uint32_t* gl = glist + p * lmax;
+    const uint16_t* hrow = hc + p * N;
+    if (loc == -1) {
+        const int z = min(__ldg(row_nnz + m), ell_w);
+        for (int j = lane; j < z; j += 32) ell_h[m * ell_w + j] = __ldg(hrow + (__ldg(gl + j) >> 16));
+        return;
+    }
+    uint16_t* d = dense_h + static_cast<int64_t>(loc) * N;
+    for (int c = lane; c < N / 8; c += 32) reinterpret_cast<uint4*>(d)[c] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    const int e = __ldg(coff + p * (nchunk + 1) + nchunk);  // stored entries of the row
+    const int32_t* ul = ulist + (p / brows) * static_cast<int64_t>(N);
+    for (int j = lane; j < e; j += 32) {
+        const int pos = static_cast<int>(__ldg(gl + j) >> 16);
+        d[__ldg(ul + pos)] = __ldg(hrow + pos);
+    }
+}
+
 }  // namespace sffn

@@ -975,6 +975,31 @@ int sffn_twell_to_hybrid(const uint32_t* twell, int64_t M, int64_t N, int T, int
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
+// ---------------------------------------------------------------- training forward via the union path (NEXT-4)
+int sffn_forward_train(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                       int T, int C, void* Y, int ell_w, void* ell_g, void* ell_h, int16_t* ell_col, int32_t* row_nnz,
+                       int32_t* row_loc, int64_t dense_cap, void* dense_g, void* dense_h, int32_t* dense_map,
+                       int* d_dense_count, double* d_l0l1, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
+                       void* stream) {
+    if (!union_applicable(N)) return SFFN_ERR_SHAPE;
+    if (M > 0 && (!ell_g || !ell_h || (dense_cap > 0 && !dense_h))) return SFFN_ERR_INVALID_ARG;
+    int r = sffn_forward(X, Wg, Wu, Wd, M, K, N, T, C, Y, workspace, ws_bytes, d_overflow, SFFN_ALGO_UNION, stream);
+    if (r != SFFN_OK || M == 0) return r;
+    const uint32_t* tw = static_cast<const uint32_t*>(workspace);
+    if ((r = sffn_twell_to_hybrid(tw, M, N, T, C, ell_w, ell_g, ell_col, row_nnz, row_loc, dense_cap, dense_g,
+                                  dense_map, d_dense_count, d_l0l1, stream)) != SFFN_OK)
+        return r;
+    const int64_t tw_bytes = align1k(sffn_twell_words(M, N, T, C) * 4);
+    uint8_t* base = static_cast<uint8_t*>(workspace) + tw_bytes;
+    UnionWs L = union_ws_layout(M, N, K, T, C);
+    { union_h_to_hybrid_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, S(stream)>>>(
+        reinterpret_cast<const uint16_t*>(base + L.hc), (int)M, (int)N, union_brows(),
+        reinterpret_cast<const int32_t*>(base + L.perm), reinterpret_cast<const uint32_t*>(base + L.glist),
+        reinterpret_cast<const uint16_t*>(base + L.coff), L.lmax, L.nchunk, reinterpret_cast<const int32_t*>(base + L.ulist),
+        row_nnz, row_loc, ell_w, static_cast<uint16_t*>(ell_h), static_cast<uint16_t*>(dense_h)); note_launch(); }
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
 // ---------------------------------------------------------------- training forward on the hybrid format (NEXT-4)
 size_t sffn_hybrid_mm_workspace_bytes(int64_t D, int64_t K, int64_t N) {
     if (D < 0 || K <= 0 || N <= 0) return 0;

@@ -69,6 +69,8 @@ _SIGS = {
                                  _vp, _vp, _sz, _vp]),
     "sffn_hybrid_spmm": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _sz,
                                 _vp]),
+    "sffn_forward_train": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _int, _vp, _vp, _vp, _vp, _vp,
+                                  _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "sffn_launch_count": (_i64, []),
     "sffn_union_block_rows": (_int, []),
     "sffn_forward_host": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _sz, _vp, _int,
@@ -281,6 +283,37 @@ def twell_to_hybrid(tw, N: int, T: int = 256, C: int = 8, ell_w: int = 128, dens
                                     _p(out["dense_map"]), _p(out["dense_count"]), _p(out["l0l1"]), _stream(stream)),
          "sffn_twell_to_hybrid")
     return out
+
+
+def forward_train(x, wg, wu, wd, T: int = 256, C: int = 8, ell_w: int = 128, dense_cap: int | None = None, out=None,
+                  workspace=None, overflow=None, stream=None):
+    """Training forward through the union path: (Y, hyb_g, hyb_h) — hyb_g the hybrid form of h_g (as twell_to_hybrid),
+    hyb_h the same pattern holding h = h_g (.) x W_u (what hybrid_sddmm computes), both dicts."""
+    M, K = x.shape
+    N = wg.shape[0]
+    dev = x.device
+    D = max(1, M // 8) if dense_cap is None else dense_cap
+    if out is None:
+        out = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+    g = {"ell_val": torch.empty((M, ell_w), dtype=torch.bfloat16, device=dev),
+         "ell_col": torch.empty((M, ell_w), dtype=torch.int16, device=dev),
+         "row_nnz": torch.empty(M, dtype=torch.int32, device=dev),
+         "row_loc": torch.empty(M, dtype=torch.int32, device=dev),
+         "dense_rows": torch.empty((max(D, 1), N), dtype=torch.bfloat16, device=dev),
+         "dense_map": torch.empty(max(D, 1), dtype=torch.int32, device=dev),
+         "dense_count": torch.zeros(1, dtype=torch.int32, device=dev),
+         "l0l1": torch.zeros(2, dtype=torch.float64, device=dev)}
+    h = dict(g)
+    h["ell_val"] = torch.zeros_like(g["ell_val"])
+    h["dense_rows"] = torch.zeros_like(g["dense_rows"])
+    workspace = _ws(workspace_bytes(M, K, N, T, C, "union"), dev, workspace)
+    _chk(lib().sffn_forward_train(_bf16(x, "x"), _bf16(wg, "wg"), _bf16(wu, "wu"), _bf16(wd, "wd"), M, K, N, T, C,
+                                  _bf16(out, "out"), ell_w, _p(g["ell_val"]), _p(h["ell_val"]), _p(g["ell_col"]),
+                                  _p(g["row_nnz"]), _p(g["row_loc"]), D, _p(g["dense_rows"]), _p(h["dense_rows"]),
+                                  _p(g["dense_map"]), _p(g["dense_count"]), _p(g["l0l1"]), _p(workspace),
+                                  workspace.numel() * workspace.element_size(), _p(overflow), _stream(stream)),
+         "sffn_forward_train")
+    return out, g, h
 
 
 def hybrid_sddmm(a, b, hyb: dict, gate: bool = True, workspace=None, stream=None) -> dict:

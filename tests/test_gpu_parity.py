@@ -646,3 +646,47 @@ def test_hybrid_training_forward(sffn, dense_cap):
     eq3 = oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)
     assert rel_fro(y[keep], eq3[keep]) < Y_TOL
     assert (y[~keep] == 0).all()
+
+
+def test_forward_train_union_path(sffn):
+    """sffn_forward_train: Y bit-identical to sffn_forward (union); the h_g hybrid identical to sffn_twell_to_hybrid
+    (up to the atomic order of dense-tail slots); the stored h = h_g (.) x W_u (copied out of the union GEMM's H_c)
+    equals the paper-design SDDMM on the same pattern bit for bit on dyadic-grid inputs (both exact fp32 dot products
+    times the same bf16 gate, one rounding), and the oracle SDDMM within one bf16 rounding."""
+    cfg = synth.CONFIGS["1B"].replace(M=900, K=512, N=2048, Kb=16, sparsity=0.97)
+    X, Wg, Wu, Wd = inputs(cfg)
+    Xd, Wgd, Wud, Wdd = (to_dev(a) for a in (X, Wg, Wu, Wd))
+    ell_w, cap = 48, 900  # no dropped rows: per-row comparison independent of the tail slot order
+    ref = sffn.forward(Xd, Wgd, Wud, Wdd, cfg.T, cfg.C, algo="union")
+    Y, g, h = sffn.forward_train(Xd, Wgd, Wud, Wdd, cfg.T, cfg.C, ell_w=ell_w, dense_cap=cap)
+    torch.cuda.synchronize()
+    assert torch.equal(Y.view(torch.int16), ref.view(torch.int16))
+    tw = sffn.pack(Xd, Wgd, cfg.T, cfg.C)
+    g2 = sffn.twell_to_hybrid(tw, cfg.N, cfg.T, cfg.C, ell_w=ell_w, dense_cap=cap)
+    s2 = sffn.hybrid_sddmm(Xd, Wud, g2, gate=True)
+    torch.cuda.synchronize()
+    loc, loc2 = g["row_loc"].cpu().numpy(), g2["row_loc"].cpu().numpy()
+    nnz = g["row_nnz"].cpu().numpy()
+    assert np.array_equal(nnz, g2["row_nnz"].cpu().numpy())
+    assert (loc >= 0).sum() > 0 and not (loc == -2).any() and np.array_equal(loc >= 0, loc2 >= 0)
+    I16 = lambda t: t.view(torch.int16).cpu().numpy()
+    he, se, ge, g2e = I16(h["ell_val"]), I16(s2["ell_val"]), I16(g["ell_val"]), I16(g2["ell_val"])
+    hd, sd, gd, g2d = I16(h["dense_rows"]), I16(s2["dense_rows"]), I16(g["dense_rows"]), I16(g2["dense_rows"])
+    for m in range(cfg.M):
+        if loc[m] == -1:
+            z = nnz[m]
+            assert np.array_equal(he[m, :z], se[m, :z]) and np.array_equal(ge[m, :z], g2e[m, :z]), m
+        else:
+            assert np.array_equal(hd[loc[m]], sd[loc2[m]]) and np.array_equal(gd[loc[m]], g2d[loc2[m]]), m
+    col = g["ell_col"].cpu().numpy()
+    nd = int(g["dense_count"].item())
+    dmap = g["dense_map"].cpu().numpy()[:nd]
+    P_ell = ge.view(np.uint16)
+    P_dense = gd.view(np.uint16)[:nd]
+    ref_ell, ref_dense = oracle.hybrid_sddmm(X, Wu, col, nnz, loc, P_ell, dmap, P_dense, True)
+    hv = h["ell_val"].float().cpu().numpy().astype(np.float64)
+    for m in np.flatnonzero(loc == -1):
+        z = nnz[m]
+        assert (np.abs(hv[m, :z] - ref_ell[m, :z]) <= 2.0 ** -8 * np.abs(ref_ell[m, :z]) + 1e-30).all()
+    hdv = h["dense_rows"].float().cpu().numpy().astype(np.float64)[:nd]
+    assert (np.abs(hdv - ref_dense) <= 2.0 ** -8 * np.abs(ref_dense) + 1e-30).all()

@@ -54,6 +54,11 @@ hh = sffn.hybrid_sddmm(X, Wu, h, gate=True, workspace=hws2)
 res["hybrid_sddmm_ms"] = t(lambda: sffn.hybrid_sddmm(X, Wu, h, gate=True, workspace=hws2))
 res["hybrid_spmm_ms"] = t(lambda: sffn.hybrid_spmm(hh, Wd, out=Y, workspace=hws2))
 res["hybrid_train_fwd_ms"] = res["twell_to_hybrid_ms"] + res["hybrid_sddmm_ms"] + res["hybrid_spmm_ms"]
+res["pack_ms"] = t(lambda: sffn.pack(X, Wg, T, C, out=tw))
+res["paper_design_train_fwd_ms"] = res["pack_ms"] + res["hybrid_train_fwd_ms"]
+# the same outputs (Y, h_g and h in the hybrid format) through the union tensor-core path in one call
+res["forward_train_union_ms"] = t(lambda: sffn.forward_train(X, Wg, Wu, Wd, T, C, ell_w=ELL_W, dense_cap=M // 8,
+                                                             out=Y, workspace=ws))
 # fp32 mode (correctness mode; SIMT fp32 GEMM) on a row slice to bound the time
 Mf = min(M, 4096)
 Xf = torch.from_numpy(synth.gen_x(cfg, 0, Mf, dtype="f32", p=p)).cuda()
