@@ -162,6 +162,9 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunks", type=int, default=4, help="M chunks overlapping compute and all-reduce (N>1)")
+    ap.add_argument("--shard", choices=["hidden", "tokens"], default="hidden",
+                    help="N>1: hidden-dim sharding + all-reduce (north_star (5), strong scaling) or independent "
+                         "token-parallel replicas with full weights and no collective (SURVEY 8(e) control, weak scaling)")
     ap.add_argument("--allreduce", choices=["nccl", "sym"], default="nccl",
                     help="N>1: NCCL all-reduce (chunked overlap) or the library's symmetric-memory reduction kernel "
                          "(NEXT-3: NVLS multimem / P2P over an NCCL symmetric window; falls back to nccl if unsupported)")
@@ -194,7 +197,8 @@ def main():
 
     M, K, N, T, C = cfg.M, cfg.K, cfg.N, cfg.T, cfg.C
     from paper_2603_23198_b200.sharding import shard_range
-    n0, Nl = shard_range(N, world, rank, T)
+    replicas = world > 1 and args.shard == "tokens"
+    n0, Nl = (0, N) if replicas else shard_range(N, world, rank, T)
 
     def to_dev(a):
         return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).to(dev)
@@ -210,7 +214,7 @@ def main():
     ov = torch.zeros(1, dtype=torch.int32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
-    comm = sffn.Comm(rank, world, local) if world > 1 else None
+    comm = sffn.Comm(rank, world, local) if world > 1 and not replicas else None
     allreduce = "none"
     if comm is not None:
         allreduce = "nccl"
@@ -277,7 +281,8 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     ms_per_step = t_max / args.steps * 1e3
-    value = M * args.steps / t_max  # tokens/s, whole job (all ranks jointly process the M tokens)
+    # tokens/s, whole job: hidden-dim sharding -> all ranks jointly process the M tokens; replicas -> M each
+    value = (world if replicas else 1) * M * args.steps / t_max
 
     # ------------------------------------------------------------------ per-kernel timing (roofline)
     peaks = load_peaks()
@@ -393,7 +398,9 @@ def main():
 
         def e2e_step():
             Xd.copy_(Xh, non_blocking=True)
-            if allreduce.startswith("sym"):
+            if replicas:
+                sffn.forward(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
+            elif allreduce.startswith("sym"):
                 comm.sharded_forward_sym(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
             else:
                 comm.sharded_forward(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo,
@@ -405,9 +412,10 @@ def main():
         tt = torch.tensor([t_e], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e = float(tt.item())
-        e2e = {"value": M * len(ms_e) / t_e, "unit": "tokens/s", "h2d_bytes_per_step": int(Xh.numel() * 2),
+        e2e = {"value": (world if replicas else 1) * M * len(ms_e) / t_e, "unit": "tokens/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 2),
                "d2h_bytes_per_step": int(Yh.numel() * 2), "ms_per_step": t_e / len(ms_e) * 1e3,
-               "api": "Comm.sharded_forward on every rank with X copied in from pinned host memory and Y copied out "
+               "api": ("sffn.forward" if replicas else "Comm.sharded_forward") + " on every rank with X copied in from pinned host memory and Y copied out "
                       "(serial copies; per-rank bytes)"}
 
     # ------------------------------------------------------------------ CPU oracle baseline
@@ -424,11 +432,12 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-               "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+               "scaling": "strong" if world > 1 and not replicas else "weak", "vs_baseline": None, "dtype": "bf16",
                "data": "synthetic (seeded dyadic-grid generator: 99% sparsity, lognormal per-token nnz, "
                        "30% dead neurons)",
                "config": {"workload": cfg.name, "M": M, "K": K, "N": N, "T": T, "C": C, "sparsity": cfg.sparsity,
-                          "parallelism": f"hidden-dim x{world}" if world > 1 else "single", "allreduce": allreduce,
+                          "parallelism": (f"token replicas x{world}" if replicas else f"hidden-dim x{world}")
+                          if world > 1 else "single", "allreduce": allreduce,
                           "l2": "flushed (512 MiB write) between timed steps", "seed": cfg.seed,
                           "launch": "cuda_graph" if graph is not None else "eager"},
                "tokens_per_s_per_gpu": value / world,
