@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     constexpr int GROUP = GEMM_GROUP_M / PAIR;
     static_assert(S >= 2, "not enough shared memory for a 2-stage ring");
     static_assert(PAIR == 1 || PAIR == 2, "PAIR is 1 or 2");
-    static_assert(PAIR == 1 || EPI == EPI_TWELL || EPI == EPI_F32 || EPI == EPI_BF16, "pair mode: K-major B only");
+    static_assert(PAIR == 1 || EPI == EPI_TWELL || EPI == EPI_F32 || EPI == EPI_BF16 || EPI == EPI_GLU,
+                  "pair mode: K-major B only");
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -172,8 +173,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
                         tma_load_2d_pair(stA + stage * GEMM_A_BYTES, &tmA, fb, kb * GEMM_BK,
                                          mb * PM + static_cast<int>(rank) * GEMM_BM, pol);
-                        tma_load_2d_pair(stB + stage * B_BYTES, &tmB, fb, kb * GEMM_BK,
-                                         nb * GEMM_BN + static_cast<int>(rank) * (GEMM_BN / 2), pol);
+                        if (EPI == EPI_GLU)  // B tile [W_g rows; W_u rows] of 128 hidden units: one half per CTA
+                            tma_load_2d_pair(stB + stage * B_BYTES, rank == 0 ? &tmB : &tmB2, fb, kb * GEMM_BK,
+                                             nb * 128, pol);
+                        else
+                            tma_load_2d_pair(stB + stage * B_BYTES, &tmB, fb, kb * GEMM_BK,
+                                             nb * GEMM_BN + static_cast<int>(rank) * (GEMM_BN / 2), pol);
                     } else {
                     mbar_arrive_expect_tx(&full[stage], GEMM_STAGE_BYTES);
                     tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, pol);

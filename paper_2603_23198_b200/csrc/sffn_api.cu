@@ -612,24 +612,32 @@ int sffn_dense_forward(const void* X, const void* Wg, const void* Wu, const void
     int r = check_device();
     if (r != SFFN_OK) return r;
     if (M == 0) return SFFN_OK;
+    static const bool pair = env_flag("SFFN_GATE_PAIR", true);
     CUtensorMap tx, tg, tu, th_out, th_in, twd, ty;
     if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&tg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&tu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&th_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, H, N, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !tmap_2d(&th_in, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, H, N, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, WdT, N, K, GEMM_BK, GEMM_BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, WdT, N, K, GEMM_BK, pair ? GEMM_BN / 2 : GEMM_BN,
+                 CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, K, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
         return SFFN_ERR_CUDA;
     GemmArgs a1{};
     a1.M = (int)M;
     a1.N = (int)N;
     a1.K = (int)K;
-    if ((r = launch_gemm<EPI_GLU, 1>(tx, tg, tu, th_out, a1, 128, S(stream))) != SFFN_OK) return r;
     GemmArgs a2{};
     a2.M = (int)M;
     a2.N = (int)K;
     a2.K = (int)N;
+    // CTA pairs like the gate GEMM (the GLU tile's W_g half on one CTA, its W_u half on the other): the
+    // speedup denominator uses the same tcgen05 machinery as the sparse path
+    if (pair) {
+        if ((r = launch_gemm<EPI_GLU, 1, 2>(tx, tg, tu, th_out, a1, 128, S(stream))) != SFFN_OK) return r;
+        return launch_gemm<EPI_BF16, 1, 2>(th_in, twd, twd, ty, a2, GEMM_BN, S(stream));
+    }
+    if ((r = launch_gemm<EPI_GLU, 1>(tx, tg, tu, th_out, a1, 128, S(stream))) != SFFN_OK) return r;
     return launch_gemm<EPI_BF16, 1>(th_in, twd, twd, ty, a2, GEMM_BN, S(stream));
 }
 
