@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 tile_info(tile, b, cj, len);
                 const int nk = UP ? nk_up : len / GEMM_BK;
                 // dense block (union forced to all N units, union_meta_kernel): B by TMA tiles, no gathers
-                const bool dense = __ldg(args.um.utot + b) == N;
+                const bool dense = __ldg(args.um.udense + b) != 0;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], dense ? GEMM_STAGE_BYTES : GEMM_A_BYTES);
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             int b, cj, len;
             tile_info(tile, b, cj, len);
             const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
-            if (__ldg(args.um.utot + b) == N) {
+            if (__ldg(args.um.udense + b) != 0) {
                 // dense block: B comes by TMA (warp 0); keep the per-stage arrivals of the full barrier
                 const int nk = UP ? nk_up : len / GEMM_BK;
                 for (int kb = 0; kb < nk; ++kb) {
@@ -371,14 +371,22 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             int e0 = 0, e1 = 0;
             const uint32_t* gl = nullptr;
             uint32_t gpre[UG_GPRE];
+            // dense block (identity union, position = unit): the gates come straight from the row's TwELL tiles of
+            // this chunk (no gate list is built for dense blocks)
+            const bool dense_blk = UP && __ldg(args.um.udense + b) != 0;
+            const uint32_t* twrow = nullptr;
             if constexpr (UP) {
                 const int64_t prow = static_cast<int64_t>(row0) + lane;  // pi-ordered row (H_c row)
-                gl = args.um.glist + prow * args.um.lmax;
-                const uint16_t* co = args.um.coff + prow * (args.um.nchunk + 1);
-                e0 = __ldg(co + cj);
-                e1 = __ldg(co + cj + 1);
+                if (dense_blk) {
+                    if (prow < args.M) twrow = args.tw + static_cast<int64_t>(__ldg(args.perm + prow)) * (N / args.C);
+                } else {
+                    gl = args.um.glist + prow * args.um.lmax;
+                    const uint16_t* co = args.um.coff + prow * (args.um.nchunk + 1);
+                    e0 = __ldg(co + cj);
+                    e1 = __ldg(co + cj + 1);
 #pragma unroll
-                for (int i = 0; i < UG_GPRE; ++i) gpre[i] = e0 + i < e1 ? __ldg(gl + e0 + i) : 0u;
+                    for (int i = 0; i < UG_GPRE; ++i) gpre[i] = e0 + i < e1 ? __ldg(gl + e0 + i) : 0u;
+                }
             }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -404,10 +412,25 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                             *reinterpret_cast<uint16_t*>(stg + (j >> 6) * 4096 + sw128_off(lane, j & 63)) =
                                 static_cast<uint16_t>(w & 0xFFFFu);
                     };
+                    if (dense_blk) {
+                        if (twrow) {  // TwELL tiles covering units [p0 + 128 h, p0 + 128 h + 128)
+                            const int WPT = args.T / args.C, cap = WPT - 1;
+                            const int t0 = (p0 + 128 * h) / args.T, t1 = min(N, p0 + 128 * h + 128 + args.T - 1) / args.T;
+                            for (int t = t0; t < t1 && t < N / args.T; ++t) {
+                                const uint32_t* blk = twrow + static_cast<int64_t>(t) * WPT;
+                                const int cnt = min(static_cast<int>(__ldg(blk)), cap);
+                                for (int e = 1; e <= cnt; ++e) {
+                                    const uint32_t w = __ldg(blk + e);
+                                    put_g(((w & 0xFFFFu) << 16) | (w >> 16));  // gate-list word: unit = position
+                                }
+                            }
+                        }
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < UG_GPRE; ++i)
-                        if (e0 + i < e1) put_g(gpre[i]);
-                    for (int e = e0 + UG_GPRE; e < e1; ++e) put_g(__ldg(gl + e));
+                        for (int i = 0; i < UG_GPRE; ++i)
+                            if (e0 + i < e1) put_g(gpre[i]);
+                        for (int e = e0 + UG_GPRE; e < e1; ++e) put_g(__ldg(gl + e));
+                    }
 #pragma unroll 1
                     for (int q32 = 0; q32 < 2 * nbox; ++q32) {
                         uint32_t v[32];

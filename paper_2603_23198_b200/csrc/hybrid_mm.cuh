@@ -131,7 +131,8 @@ __global__ void union_h_to_hybrid_kernel(const uint16_t* __restrict__ hc, int M,
                                          const uint16_t* __restrict__ coff, int lmax, int nchunk,
                                          const int32_t* __restrict__ ulist, const int32_t* __restrict__ row_nnz,
                                          const int32_t* __restrict__ row_loc, int ell_w, uint16_t* __restrict__ ell_h,
-                                         uint16_t* __restrict__ dense_h) {
+                                         uint16_t* __restrict__ dense_h, const uint32_t* __restrict__ tw, int T, int C,
+                                         const int32_t* __restrict__ udense) {
     const int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (p >= M) return;
@@ -140,6 +141,36 @@ __global__ void union_h_to_hybrid_kernel(const uint16_t* __restrict__ hc, int M,
     if (loc == -2) return;
     const uint32_t* gl = glist + p * lmax;
     const uint16_t* hrow = hc + p * N;
+    if (__ldg(udense + p / brows) != 0) {
+        // dense block (identity union, no gate list): walk the row's TwELL tiles in order (lane per tile, warp
+        // prefix of the counts = the ELL slot order of sffn_twell_to_hybrid); position = unit
+        const int NT = N / T, WPT = T / C, cap = WPT - 1;
+        const uint32_t* row = tw + m * (N / C);
+        uint16_t* d = loc >= 0 ? dense_h + static_cast<int64_t>(loc) * N : nullptr;
+        if (d) {
+            for (int c = lane; c < N / 8; c += 32) reinterpret_cast<uint4*>(d)[c] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+        }
+        int base = 0;
+        for (int t0 = 0; t0 < NT; t0 += 32) {
+            const int t = t0 + lane;
+            const int cnt = t < NT ? min(static_cast<int>(__ldg(row + static_cast<int64_t>(t) * WPT)), cap) : 0;
+            int inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
+            }
+            const int start = base + inc - cnt;
+            for (int e = 0; e < cnt; ++e) {
+                const int n = static_cast<int>(__ldg(row + static_cast<int64_t>(t) * WPT + 1 + e) & 0xFFFFu);
+                if (d) d[n] = __ldg(hrow + n);
+                else if (start + e < ell_w) ell_h[m * ell_w + start + e] = __ldg(hrow + n);
+            }
+            base += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        return;
+    }
     if (loc == -1) {
         const int z = min(__ldg(row_nnz + m), ell_w);
         for (int j = lane; j < z; j += 32) ell_h[m * ell_w + j] = __ldg(hrow + (__ldg(gl + j) >> 16));

@@ -224,7 +224,7 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, glist, coff, bctr, total;
+    int64_t hc, ulist, ulen, utot, udense, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, glist, coff, bctr, total;
     int lmax, nchunk;
 };
 // Token rows per union block: 128 (single-CTA union GEMMs) or 256 (CTA-pair union GEMMs, SFFN_UNION_PAIR=1).
@@ -242,6 +242,7 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8)
     w.ulist = o; o = align1k(o + NB * N * 4);
     w.ulen = o;  o = align1k(o + NB * 4);
     w.utot = o;  o = align1k(o + NB * 4);
+    w.udense = o; o = align1k(o + NB * 4);
     w.umask = o; o = align1k(o + NB * (N / 32) * 4);
     w.uwoff = o; o = align1k(o + NB * (N / 32) * 4);
     w.chunk = o; o = align1k(o + (NB + 1) * 4);
@@ -313,6 +314,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     um.ulist = reinterpret_cast<int32_t*>(base + L.ulist);
     um.ulen = reinterpret_cast<int32_t*>(base + L.ulen);
     um.utot = reinterpret_cast<int32_t*>(base + L.utot);
+    um.udense = reinterpret_cast<int32_t*>(base + L.udense);
     um.umask = reinterpret_cast<uint32_t*>(base + L.umask);
     um.uwoff = reinterpret_cast<int32_t*>(base + L.uwoff);
     um.chunk_off = reinterpret_cast<int32_t*>(base + L.chunk);
@@ -1004,7 +1006,8 @@ int sffn_forward_train(const void* X, const void* Wg, const void* Wu, const void
         reinterpret_cast<const uint16_t*>(base + L.hc), (int)M, (int)N, union_brows(),
         reinterpret_cast<const int32_t*>(base + L.perm), reinterpret_cast<const uint32_t*>(base + L.glist),
         reinterpret_cast<const uint16_t*>(base + L.coff), L.lmax, L.nchunk, reinterpret_cast<const int32_t*>(base + L.ulist),
-        row_nnz, row_loc, ell_w, static_cast<uint16_t*>(ell_h), static_cast<uint16_t*>(dense_h)); note_launch(); }
+        row_nnz, row_loc, ell_w, static_cast<uint16_t*>(ell_h), static_cast<uint16_t*>(dense_h), tw, T, C,
+        reinterpret_cast<const int32_t*>(base + L.udense)); note_launch(); }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 

@@ -22,6 +22,7 @@ struct UnionMeta {
     int32_t* uwoff;
     int32_t* chunk_off;  // [1]: number of UP tiles
     int32_t* utot;       // [NB] un-padded union sizes
+    int32_t* udense;     // [NB] 1: dense block (identity union; weight tiles by TMA, gates read from the TwELL)
     int32_t* tiles;      // [NB * ceil(N/256)]: UP work list, (b << 8) | chunk, grouped raster
     int* counters;       // [2] dynamic tile-scheduler counters of the UP and DOWN GEMMs
     uint32_t* glist;     // [NB*128, lmax] per (pi-ordered) row: (union position << 16) | bf16 gate, ascending
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
     if (threadIdx.x == 0) {
         um.ulen[b] = padded;
         um.utot[b] = total;
+        um.udense[b] = (dense_units <= N && total == N) ? 1 : 0;  // only when the dense (TMA) path is enabled
     }
 
     // the last CTA builds the UP work list from every block's ulen
@@ -337,7 +339,8 @@ __global__ void __launch_bounds__(256) union_gate_list_kernel(const uint32_t* __
     const uint32_t* msk = um.umask + static_cast<int64_t>(b) * NW;
     const int32_t* wof = um.uwoff + static_cast<int64_t>(b) * NW;
     uint32_t* gl = um.glist + i * um.lmax;
-    const bool dense = __ldg(um.utot + b) == N;  // identity union: position = unit
+    const bool dense = __ldg(um.udense + b) != 0;  // identity union: the UP epilogue reads the TwELL directly
+    if (dense) return;
     auto emit = [&](uint32_t w, int idx) {
         const int n = static_cast<int>(w & 0xFFFFu);
         const int j = dense ? n : __ldg(wof + (n >> 5)) + __popc(__ldg(msk + (n >> 5)) & ((1u << (n & 31)) - 1u));

@@ -692,11 +692,13 @@ def test_forward_train_union_path(sffn):
     assert (np.abs(hdv - ref_dense) <= 2.0 ** -8 * np.abs(ref_dense) + 1e-30).all()
 
 
-@pytest.mark.parametrize("N,T,C,K,M", [(64, 32, 2, 64, 300), (128, 64, 4, 128, 129), (192, 64, 2, 64, 1)])
-def test_union_small_shapes(sffn, N, T, C, K, M):
+@pytest.mark.parametrize("N,T,C,K,M,sp", [(64, 32, 2, 64, 300, 0.9), (128, 64, 4, 128, 129, 0.9), (192, 64, 2, 64, 1, 0.9),
+                                          (128, 64, 1, 128, 300, 0.5), (256, 256, 1, 128, 300, 0.5)])
+def test_union_small_shapes(sffn, N, T, C, K, M, sp):
     """Union path at its smallest legal shapes (N = 64 .. 192, one or two 256-position chunks, K = 64, M = 1 and
-    ragged M): Y within 1e-2 of Eq.3."""
-    cfg = synth.CONFIGS["tiny"].replace(M=M, K=K, N=N, T=T, C=C, Kb=8, sparsity=0.9)
+    ragged M), and at 50% density where the unions are naturally full (N < 256: no TMA path, the identity list
+    is gathered; N = 256: dense blocks): Y within 1e-2 of Eq.3."""
+    cfg = synth.CONFIGS["tiny"].replace(M=M, K=K, N=N, T=T, C=C, Kb=8, sparsity=sp)
     X, Wg, Wu, Wd = inputs(cfg)
     Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), T, C, algo="union")
     words, counts, ov, A = oracle.pack_from_inputs(X, Wg, T, C)
