@@ -704,3 +704,18 @@ def test_union_small_shapes(sffn, N, T, C, K, M, sp):
     words, counts, ov, A = oracle.pack_from_inputs(X, Wg, T, C)
     y = bf16_np(Y)
     assert rel_fro(y, oracle.ffn_twell(X, words, Wu, Wd, N, T, C)) < Y_TOL
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+@pytest.mark.parametrize("name,M", [("1B", 512), ("7B", 256)])
+def test_forward_other_seeds(sffn, name, M, seed):
+    """the configs are generated with seeds 0/1/2 — the union forward and the pack on seeds 1 and 2
+    (TwELL bit-exact on the rows, Y within 1e-2 of Eq.3)."""
+    cfg = synth.CONFIGS[name].replace(M=M, seed=seed)
+    X, Wg, Wu, Wd = inputs(cfg)
+    tw = sffn.pack(to_dev(X), to_dev(Wg), cfg.T, cfg.C)
+    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo="union")
+    words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    got = tw.cpu().numpy().view(np.uint32)
+    assert oracle.valid_prefix_equal(got, words, cfg.T, cfg.C).all()
+    assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
