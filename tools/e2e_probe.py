@@ -40,14 +40,16 @@ for rows in (2048, 4096, 8192):
     xr, yr = X[:rows], Yd[:rows]
     t = tim(lambda: sffn.forward(xr, Wg, Wu, Wd, T, C, out=yr, workspace=ws, algo="union"))
     print(f"forward M={rows}: {t:.3f} ms  (x{M//rows} = {t*M/rows:.2f} ms)")
-rows = 4096
-wsz = sffn.workspace_bytes(rows, K, N, T, C, "union")
-wsd = {False: torch.empty(wsz, dtype=torch.uint8, device="cuda"),
-       True: torch.empty((wsz + 1023) // 1024 * 1024 + wsz, dtype=torch.uint8, device="cuda")}
-res = {False: [], True: []}
-for rnd in range(6):
-    for dual in ((False, True) if rnd % 2 == 0 else (True, False)):
-        res[dual].append(tim(lambda: sffn.forward_host(Xh, Wg, Wu, Wd, T, C, out=Yh, workspace=wsd[dual], algo="union",
-                                                       chunk_rows=rows), n=3))
-for dual in (False, True):
-    print(f"forward_host chunk={rows} dual={dual}: median {np.median(res[dual]):.3f} ms  {[round(x, 3) for x in res[dual]]}")
+res = {}
+wsz = sffn.workspace_bytes(16384, K, N, T, C, "union")
+wsd = torch.empty((wsz + 1023) // 1024 * 1024 + wsz, dtype=torch.uint8, device="cuda")
+chunks = [int(c) for c in os.environ.get("CHUNKS", "4096,8192,16384").split(",")]
+for c in chunks:
+    res[c] = []
+for rnd in range(4):
+    for c in (chunks if rnd % 2 == 0 else chunks[::-1]):
+        res[c].append(tim(lambda: sffn.forward_host(Xh, Wg, Wu, Wd, T, C, out=Yh, workspace=wsd, algo="union",
+                                                    chunk_rows=c), n=3))
+for c in chunks:
+    print(f"forward_host chunk={c} {sffn.forward_host_chunks(M, c)}: median {np.median(res[c]):.3f} ms  "
+          f"{[round(x, 3) for x in res[c]]}")
