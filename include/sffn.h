@@ -343,6 +343,19 @@ int sffn_allreduce_sym_bf16(sffn_comm* comm, const void* src, void* Y, int64_t r
  * without the broadcast store. */
 int sffn_reduce_scatter_sym_bf16(sffn_comm* comm, const void* src, int64_t rows, int64_t K, void* Y_slice,
                                  int64_t* row0, int64_t* nrows, void* stream);
+/* sffn_sharded_forward_fused — the all-reduce fused into the DOWN GEMM at 2048-row-window granularity (one pi
+ * window = one DOWN raster group): after each output tile the DOWN epilogue warps count their rows at the window's
+ * owner rank (w % G; system-scope atomic on the owner's window counter through the LSA mapping), and an otherwise
+ * idle warp of every DOWN CTA waits for the owned windows in raster order and reduces its slice of each across the
+ * ranks' windows (NVLS multimem.ld_reduce / multimem.st, else P2P) while later windows still compute; a final LSA
+ * barrier and the local copy window -> Y end the call.  Union path only (single-CTA union GEMMs); needs
+ * sffn_comm_symmetric_init with max_rows >= M; two counter sets alternate by call parity and each call zeroes its
+ * own set after the closing barrier, so every rank must make the same sequence of calls (any M <= max_rows).
+ * A counter that does not reach its target within about a minute (a rank gone) traps the kernel: the call's
+ * stream reports a launch failure instead of hanging. */
+int sffn_sharded_forward_fused(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
+                               int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
+                               size_t ws_bytes, uint32_t* d_overflow, void* stream);
 int sffn_sharded_forward_sym(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
                              int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
                              size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream);

@@ -31,7 +31,28 @@ struct UnionArgs {
     const int32_t* perm;  // DOWN: output row of permuted row i
     int* counter;         // dynamic tile scheduler (zeroed by union_scan_kernel)
     bf16_t* Y;            // DOWN: output [M, K]
+    // DOWN with the fused window-granular all-reduce (NEXT-3, sffn_sharded_forward_fused); Y = this rank's
+    // symmetric window.  ptrs[p] = rank p's window base (LSA, P2P-mapped), ptrs[G] = its multicast address or 0.
+    const uint64_t* ptrs;
+    int G, rank;
+    int64_t flags_off;    // byte offset of the per-2048-row-window arrival counters in every window
 };
+
+// ---------------------------------------------------------------- fused all-reduce helpers (NEXT-3)
+constexpr int FUSE_WIN = 2048;  // rows per reduction window (= the pi window: a DOWN raster group of 16 blocks)
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fuse_bf16x8_acc(float (&a)[8], const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        a[2 * i] += __uint_as_float(w[i] << 16);
+        a[2 * i + 1] += __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+}
 
 // 16-byte cp.async of a gathered weight-row segment (L2 only: .cg); src_bytes < 16 zero-fills the rest
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
@@ -86,7 +107,7 @@ constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 1024;
 constexpr int UG_RING = 8;       // tile-scheduler ring depth
 constexpr int UG_READERS = UG_GW + 5;  // gather warps + MMA thread + 4 epilogue warps
 
-template <bool UP>
+template <bool UP, bool FUSED = false>
 __global__ void __launch_bounds__(UG_THREADS, 1)
     union_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmOut, const UnionArgs args) {
@@ -353,6 +374,58 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 }
             }
         }
+    } else if (FUSED && !UP && warp == 3) {
+        // ------------------------------------------------------------ fused all-reduce (window granular)
+        // Windows owned by this rank (w % G == rank), in raster order: wait until every rank's epilogue warps have
+        // counted all their tiles of the window (4 per block and column tile), then this CTA reduces its slice of
+        // the window's rows across the ranks' windows (multimem.ld_reduce + multimem.st through the switch, else
+        // P2P loads, fp32 sum, P2P stores into every window) — while later windows are still being computed.
+        const int nwin = (args.M + FUSE_WIN - 1) / FUSE_WIN;
+        const int64_t K8 = args.K / 8;
+        const int rpc = (FUSE_WIN + gridDim.x - 1) / gridDim.x;  // rows of a window per CTA
+        const uint32_t* flags = reinterpret_cast<const uint32_t*>(args.ptrs[args.rank] + args.flags_off);
+        const uint64_t mc = args.ptrs[args.G];
+        for (int w = args.rank; w < nwin; w += args.G) {
+            const int rows_w = min(FUSE_WIN, args.M - w * FUSE_WIN);
+            const int blocks = (rows_w + GEMM_BM - 1) / GEMM_BM;
+            const uint32_t target = static_cast<uint32_t>(4 * blocks * args.NJ * args.G);
+            if (lane == 0) {
+                long long spins = 0;
+                uint32_t v;
+                while (static_cast<int32_t>((v = ld_acquire_sys_u32(flags + w)) - target) < 0) {
+                    __nanosleep(200);
+                    if (++spins == (1ll << 28)) {  // > 1 min: a rank is gone; fail the launch instead of hanging
+                        printf("sffn fused: cta %d window %d counter %u target %u\n", blockIdx.x, w, v, target);
+                        __trap();
+                    }
+                }
+            }
+            __syncwarp();
+            const int r0 = w * FUSE_WIN + blockIdx.x * rpc;
+            const int r1 = min(w * FUSE_WIN + rows_w, r0 + rpc);
+            if (r1 <= r0) continue;
+            const int64_t q0 = static_cast<int64_t>(r0) * K8, q1 = static_cast<int64_t>(r1) * K8;
+            for (int64_t q = q0 + lane; q < q1; q += 32) {
+                if (mc) {
+                    uint4 v;
+                    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                 : "l"(reinterpret_cast<uint4*>(mc) + q)
+                                 : "memory");
+                    asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(
+                                     reinterpret_cast<uint4*>(mc) + q),
+                                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                                 : "memory");
+                } else {
+                    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                    for (int p = 0; p < args.G; ++p)
+                        fuse_bf16x8_acc(a, __ldcv(reinterpret_cast<const uint4*>(args.ptrs[p]) + q));
+                    const uint4 o = make_uint4(pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]), pack_bf16x2(a[4], a[5]),
+                                               pack_bf16x2(a[6], a[7]));
+                    for (int p = 0; p < args.G; ++p) reinterpret_cast<uint4*>(args.ptrs[p])[q] = o;
+                }
+            }
+        }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue
         const int ew = warp - 4;
@@ -498,6 +571,16 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                             *reinterpret_cast<uint4*>(args.Y + yrow * args.K + c0 + chunk * 8) = val;
                     }
                     __syncwarp();  // staging rows read before the next half overwrites them
+                }
+                if constexpr (FUSED) {
+                    // this warp's 32 rows x 256 columns are in the local window: count them at the window's owner
+                    __threadfence_system();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int w = b * GEMM_BM / FUSE_WIN;
+                        uint32_t* f = reinterpret_cast<uint32_t*>(args.ptrs[w % args.G] + args.flags_off) + w;
+                        atomicAdd_system(f, 1u);
+                    }
                 }
             }
             if (++acc == 2) {

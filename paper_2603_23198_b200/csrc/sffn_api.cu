@@ -303,9 +303,16 @@ int64_t union_dense_nnz(int64_t N, bool has_tma_path) {
     return static_cast<int64_t>(f * static_cast<double>(N));
 }
 
+// NEXT-3 fused all-reduce parameters of the DOWN kernel (sffn_sharded_forward_fused; null: plain DOWN)
+struct FuseParams {
+    const uint64_t* ptrs;  // device: G window bases + multicast base (0 if none)
+    int G, rank;
+    int64_t flags_off;
+};
+
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true,
-                      bool nnz_ready = false) {
+                      bool nnz_ready = false, const FuseParams* fuse = nullptr) {
     const int BR = union_brows();
     const int64_t NB = (M + BR - 1) / BR;
     UnionWs L = union_ws_layout(M, N, K, T, C);
@@ -401,6 +408,9 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         if (attr == cudaSuccess)
             attr = cudaFuncSetAttribute(union_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UG_SMEM);
         if (attr == cudaSuccess)
+            attr = cudaFuncSetAttribute(union_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        UG_SMEM);
+        if (attr == cudaSuccess)
             attr = cudaFuncSetAttribute(union_gemm_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         UGP_SMEM);
         if (attr == cudaSuccess)
@@ -444,7 +454,15 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
     const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
-    { union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
+    if (fuse) {
+        ud.ptrs = fuse->ptrs;
+        ud.G = fuse->G;
+        ud.rank = fuse->rank;
+        ud.flags_off = fuse->flags_off;
+        { union_gemm_kernel<false, true><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
+    } else {
+        { union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
+    }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
@@ -561,6 +579,28 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
     return updown_dispatch(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, ws_bytes - static_cast<size_t>(tw_bytes), algo,
                            S(stream));
+}
+
+// Internal (not in include/sffn.h): sffn_forward (UNION) whose DOWN GEMM writes the partial Y into this rank's
+// symmetric window (Y) and reduces 2048-row windows across the ranks as they complete (sffn_comm.cu).
+int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
+                        int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
+                        const uint64_t* ptrs, int G, int rank, int64_t flags_off, void* stream) {
+    int r = pack_checks(X, Wg, M, K, N, T, C, workspace);
+    if (r != SFFN_OK) return r;
+    if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
+    if (!union_applicable(N) || union_brows() != 128) return SFFN_ERR_UNSUPPORTED;
+    if (ws_bytes < sffn_forward_workspace_bytes(M, K, N, T, C, SFFN_ALGO_UNION)) return SFFN_ERR_SHAPE;
+    if ((r = check_device()) != SFFN_OK) return r;
+    if (M == 0) return SFFN_OK;
+    uint32_t* tw = static_cast<uint32_t*>(workspace);
+    const int64_t tw_bytes = align1k(sffn_twell_words(M, N, T, C) * 4);
+    uint8_t* udws = static_cast<uint8_t*>(workspace) + tw_bytes;
+    int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
+    if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+    if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz)) != SFFN_OK) return r;
+    FuseParams fp{ptrs, G, rank, flags_off};
+    return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
 }
 
 int sffn_down(const uint32_t* twell, const void* Wd, int64_t M, int64_t K, int64_t N, int T, int C, void* Y,

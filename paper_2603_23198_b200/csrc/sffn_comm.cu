@@ -24,7 +24,25 @@ struct sffn_comm {
     ncclWindow_t win = nullptr;
     ncclDevComm dev{};
     bool has_dev = false, multimem = false;
+    // fused window-granular all-reduce (sffn_sharded_forward_fused): peer window bases + multicast base on the device;
+    // two sets of per-window arrival counters after the partial-Y region (call parity alternates them; each call
+    // zeroes its set after its closing barrier, when no rank can still touch it and before any rank's call + 2)
+    uint64_t* d_ptrs = nullptr;
+    int64_t flags_off = 0, nwin = 0;
+    uint32_t fuse_calls = 0;
 };
+
+extern "C" int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
+                                   int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes,
+                                   uint32_t* d_overflow, const uint64_t* ptrs, int G, int rank,
+                                   int64_t flags_off, void* stream);
+
+// device: ptrs[p] = rank p's window base through the LSA mapping, ptrs[G] = the window's multicast address (or 0)
+__global__ void sym_ptrs_kernel(ncclDevComm dc, ncclWindow_t win, int G, int multimem, uint64_t* ptrs) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int p = 0; p < G; ++p) ptrs[p] = reinterpret_cast<uint64_t>(ncclGetLsaPointer(win, 0, p));
+    ptrs[G] = multimem ? reinterpret_cast<uint64_t>(ncclGetLsaMultimemPointer(win, 0, dc)) : 0ull;
+}
 
 // ---------------------------------------------------------------- NEXT-3: symmetric-memory all-reduce kernel
 // One launch after the DOWN GEMM (whose epilogue wrote this rank's partial Y straight into the registered
@@ -83,6 +101,20 @@ __global__ void __launch_bounds__(SYM_THREADS) sym_reduce_scatter_kernel(ncclDev
         }
     }
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
+// After the fused DOWN: every rank's reducers are done (LSA barrier), then the local copy window -> Y.
+__global__ void __launch_bounds__(SYM_THREADS) sym_finish_kernel(ncclDevComm dc, ncclWindow_t win, int64_t n16,
+                                                                int multimem, uint4* Y, int64_t flag0, int64_t nwin) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    const uint4* loc = static_cast<const uint4*>(ncclGetLocalPointer(win, 0));
+    if (blockIdx.x == 0) {  // this call's counter set: every rank's increments and this rank's waits are done
+        uint32_t* flags = static_cast<uint32_t*>(ncclGetLocalPointer(win, 0)) + flag0;
+        for (int64_t w = threadIdx.x; w < nwin; w += blockDim.x) flags[w] = 0;
+    }
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n16; q += stride) Y[q] = loc[q];
 }
 
 __global__ void __launch_bounds__(SYM_THREADS) sym_allreduce_kernel(ncclDevComm dc, ncclWindow_t win, int64_t n16,
@@ -170,6 +202,7 @@ int sffn_comm_destroy(sffn_comm* c) {
         if (ncclDevCommDestroy(c->nccl, &c->dev) != ncclSuccess) r = SFFN_ERR_NCCL;
         if (c->win && ncclCommWindowDeregister(c->nccl, c->win) != ncclSuccess) r = SFFN_ERR_NCCL;
         if (c->sym_buf && ncclMemFree(c->sym_buf) != ncclSuccess) r = SFFN_ERR_NCCL;
+        if (c->d_ptrs) cudaFree(c->d_ptrs);
     }
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -192,7 +225,10 @@ int sffn_allreduce_bf16(sffn_comm* c, void* buf, int64_t count, void* stream) {
 int sffn_comm_symmetric_init(sffn_comm* c, int64_t max_rows, int64_t K) {
     if (!c || max_rows < 1 || K < 8 || K % 8 != 0) return SFFN_ERR_INVALID_ARG;
     if (c->sym_buf) return SFFN_ERR_INVALID_ARG;  // once per communicator
-    const size_t bytes = (static_cast<size_t>(max_rows) * K * 2 + NCCL_WIN_REQUIRED_ALIGNMENT - 1) /
+    // [partial Y: max_rows x K bf16][arrival counters: one uint32 per 2048-row window]
+    const int64_t flags_off = (static_cast<int64_t>(max_rows) * K * 2 + 255) / 256 * 256;
+    const int64_t nwin = (max_rows + 2047) / 2048;
+    const size_t bytes = (static_cast<size_t>(flags_off + 8 * nwin) + NCCL_WIN_REQUIRED_ALIGNMENT - 1) /
                          NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
     if (ncclMemAlloc(&c->sym_buf, bytes) != ncclSuccess) {
         c->sym_buf = nullptr;
@@ -219,6 +255,19 @@ int sffn_comm_symmetric_init(sffn_comm* c, int64_t max_rows, int64_t K) {
         c->win = nullptr;
         return SFFN_ERR_UNSUPPORTED;
     }
+    if (cudaMemset(static_cast<uint8_t*>(c->sym_buf) + flags_off, 0, static_cast<size_t>(8 * nwin)) != cudaSuccess ||
+        cudaMalloc(&c->d_ptrs, static_cast<size_t>(c->nranks + 1) * 8) != cudaSuccess) {
+        ncclDevCommDestroy(c->nccl, &c->dev);
+        ncclCommWindowDeregister(c->nccl, c->win);
+        ncclMemFree(c->sym_buf);
+        c->sym_buf = nullptr;
+        c->win = nullptr;
+        return SFFN_ERR_CUDA;
+    }
+    sym_ptrs_kernel<<<1, 32>>>(c->dev, c->win, c->nranks, req.lsaMultimem ? 1 : 0, c->d_ptrs);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return SFFN_ERR_CUDA;
+    c->flags_off = flags_off;
+    c->nwin = nwin;
     c->has_dev = true;
     c->multimem = req.lsaMultimem;
     c->sym_bytes = bytes;
@@ -268,6 +317,27 @@ int sffn_reduce_scatter_sym_bf16(sffn_comm* c, const void* src, int64_t rows, in
     const int64_t k16 = K / 8;  // 16-byte chunks per row
     sym_reduce_scatter_kernel<<<SYM_CTAS, SYM_THREADS, 0, st>>>(c->dev, c->win, r0 * k16, r1 * k16, c->nranks,
                                                                 c->multimem ? 1 : 0, static_cast<uint4*>(Y_slice));
+    return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
+}
+
+int sffn_sharded_forward_fused(sffn_comm* c, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,
+                               int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
+                               size_t ws_bytes, uint32_t* d_overflow, void* stream) {
+    if (!c) return SFFN_ERR_INVALID_ARG;
+    if (!c->has_dev) return SFFN_ERR_UNSUPPORTED;
+    if (M < 0 || M > c->sym_rows || K != c->sym_K) return SFFN_ERR_SHAPE;
+    if (!Y) return SFFN_ERR_INVALID_ARG;
+    if (M == 0) return SFFN_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // the DOWN GEMM writes the partial Y into the window and reduces each 2048-row window across the ranks as soon as
+    // every rank has counted it; then one barrier (all windows reduced everywhere) and the local copy window -> Y
+    const int64_t foff = c->flags_off + 4 * c->nwin * (c->fuse_calls & 1);
+    int r = sffn__forward_fused(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, c->sym_buf, workspace, ws_bytes,
+                                d_overflow, c->d_ptrs, c->nranks, c->rank, foff, stream);
+    if (r != SFFN_OK) return r;
+    ++c->fuse_calls;
+    sym_finish_kernel<<<SYM_CTAS, SYM_THREADS, 0, st>>>(c->dev, c->win, M * K / 8, c->multimem ? 1 : 0,
+                                                       static_cast<uint4*>(Y), foff / 4, (M + 2047) / 2048);
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 

@@ -64,6 +64,8 @@ _SIGS = {
     "sffn_reduce_scatter_sym_bf16": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "sffn_sharded_forward_sym": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
                                         _int, _vp]),
+    "sffn_sharded_forward_fused": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
+                                          _vp]),
     "sffn_hybrid_mm_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "sffn_hybrid_sddmm": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _int, _vp,
                                  _vp, _vp, _sz, _vp]),
@@ -546,6 +548,21 @@ class Comm:
                                             _bf16(wd_s, "wd"), M, K, N_local, T, C, _bf16(out, "out"), _p(workspace),
                                             workspace.numel() * workspace.element_size(), _p(overflow), a,
                                             _stream(stream)), "sffn_sharded_forward_sym")
+        return out
+
+    def sharded_forward_fused(self, x, wg_s, wu_s, wd_s, T=256, C=8, out=None, workspace=None, overflow=None,
+                              stream=None):
+        """Union forward with the all-reduce fused into the DOWN GEMM (2048-row windows reduced as they finish);
+        needs symmetric_init(max_rows >= M, K)."""
+        M, K = x.shape
+        N_local = wg_s.shape[0]
+        if out is None:
+            out = torch.empty((M, K), dtype=torch.bfloat16, device=x.device)
+        workspace = _ws(workspace_bytes(M, K, N_local, T, C, ALGO_UNION), x.device, workspace)
+        _chk(lib().sffn_sharded_forward_fused(self.h, _bf16(x, "x"), _bf16(wg_s, "wg"), _bf16(wu_s, "wu"),
+                                              _bf16(wd_s, "wd"), M, K, N_local, T, C, _bf16(out, "out"),
+                                              _p(workspace), workspace.numel() * workspace.element_size(),
+                                              _p(overflow), _stream(stream)), "sffn_sharded_forward_fused")
         return out
 
     def allreduce(self, buf, stream=None):

@@ -329,6 +329,24 @@ def test_sharded_forward_symmetric_single_rank(sffn, algo):
         comm.close()
 
 
+def test_sharded_forward_fused_single_rank(sffn):
+    """NEXT-3, all-reduce fused into the DOWN GEMM (window counters + in-kernel reducer warp) on a 1-rank
+    communicator: bit-identical to sffn_forward over three windows (ragged), repeated calls (epochs) and
+    smaller M.  Run in a child process under a timeout so a counter bug fails instead of hanging."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.dirname(here), here, os.environ.get("PYTHONPATH", "")]))
+    try:
+        out = subprocess.run([sys.executable, os.path.join(here, "fused_case.py")], capture_output=True, text=True,
+                             timeout=240, env=env)
+    except subprocess.TimeoutExpired:
+        pytest.fail("fused forward did not finish within 240 s (window counter never reached its target)")
+    if "SKIP" in out.stdout:
+        pytest.skip(out.stdout.strip())
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
+
+
 # ----------------------------------------------------------------- fp32 mode (R19): Y within 1e-5
 F32_TOL = 1e-5
 
