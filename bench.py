@@ -165,9 +165,10 @@ def main():
     ap.add_argument("--shard", choices=["hidden", "tokens"], default="hidden",
                     help="N>1: hidden-dim sharding + all-reduce (north_star (5), strong scaling) or independent "
                          "token-parallel replicas with full weights and no collective (SURVEY 8(e) control, weak scaling)")
-    ap.add_argument("--allreduce", choices=["nccl", "sym"], default="nccl",
-                    help="N>1: NCCL all-reduce (chunked overlap) or the library's symmetric-memory reduction kernel "
-                         "(NEXT-3: NVLS multimem / P2P over an NCCL symmetric window; falls back to nccl if unsupported)")
+    ap.add_argument("--allreduce", choices=["nccl", "sym", "fused"], default="nccl",
+                    help="N>1: NCCL all-reduce (chunked overlap), the library's symmetric-memory reduction kernel "
+                         "(NEXT-3: NVLS multimem / P2P over an NCCL symmetric window), or that reduction fused into "
+                         "the DOWN GEMM per 2048-row window (union path); falls back to nccl if unsupported")
     ap.add_argument("--algo", default="auto", choices=["auto", "gather", "union"], help="fused up/down algorithm")
     ap.add_argument("--e2e-chunk", type=int, default=4096, help="rows per chunk of the host-buffer pipeline")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
@@ -218,8 +219,9 @@ def main():
     allreduce = "none"
     if comm is not None:
         allreduce = "nccl"
-        if args.allreduce == "sym" and comm.symmetric_init(M, K):
-            allreduce = "sym-nvls" if comm.symmetric_info()["multimem"] else "sym-p2p"
+        if args.allreduce in ("sym", "fused") and comm.symmetric_init(M, K):
+            allreduce = ("sym-" if args.allreduce == "sym" else "fused-") + (
+                "nvls" if comm.symmetric_info()["multimem"] else "p2p")
 
     def step():
         if comm is None:
@@ -227,6 +229,8 @@ def main():
         else:
             if allreduce.startswith("sym"):
                 comm.sharded_forward_sym(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
+            elif allreduce.startswith("fused"):
+                comm.sharded_forward_fused(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov)
             else:
                 comm.sharded_forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo,
                                      n_chunks=args.chunks)
@@ -408,6 +412,8 @@ def main():
                 sffn.forward(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
             elif allreduce.startswith("sym"):
                 comm.sharded_forward_sym(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo)
+            elif allreduce.startswith("fused"):
+                comm.sharded_forward_fused(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov)
             else:
                 comm.sharded_forward(Xd, Wg, Wu, Wd, T, C, out=Y, workspace=ws, overflow=ov, algo=args.algo,
                                      n_chunks=args.chunks)

@@ -349,8 +349,9 @@ int sffn_reduce_scatter_sym_bf16(sffn_comm* comm, const void* src, int64_t rows,
  * idle warp of every DOWN CTA waits for the owned windows in raster order and reduces its slice of each across the
  * ranks' windows (NVLS multimem.ld_reduce / multimem.st, else P2P) while later windows still compute; a final LSA
  * barrier and the local copy window -> Y end the call.  Union path only (single-CTA union GEMMs); needs
- * sffn_comm_symmetric_init with max_rows >= M; two counter sets alternate by call parity and each call zeroes its
- * own set after the closing barrier, so every rank must make the same sequence of calls (any M <= max_rows).
+ * sffn_comm_symmetric_init with max_rows >= M; two counter sets alternate call by call (the closing kernel zeroes
+ * the set it used and selects the other one on the device, so CUDA-graph replays alternate too); every rank must
+ * make the same sequence of calls (any M <= max_rows).
  * A counter that does not reach its target within about a minute (a rank gone) traps the kernel: the call's
  * stream reports a launch failure instead of hanging. */
 int sffn_sharded_forward_fused(sffn_comm* comm, const void* X, const void* Wg_s, const void* Wu_s, const void* Wd_s,

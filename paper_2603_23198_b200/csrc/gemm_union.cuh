@@ -35,14 +35,15 @@ struct UnionArgs {
     // symmetric window.  ptrs[p] = rank p's window base (LSA, P2P-mapped), ptrs[G] = its multicast address or 0.
     const uint64_t* ptrs;
     int G, rank;
-    int64_t flags_off;    // byte offset of the per-2048-row-window arrival counters in every window
 };
 
 // ---------------------------------------------------------------- fused all-reduce helpers (NEXT-3)
-constexpr int FUSE_WIN = 2048;  // rows per reduction window (= the pi window: a DOWN raster group of 16 blocks)
-__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+constexpr int FUSE_WIN = 2048;
+constexpr int FUSE_WARPS = 2;  // reducer warps: 2 (idle after the TMEM allocation) and 3
+constexpr int FUSE_U = 8;      // 16-byte loads in flight per reducer lane  // rows per reduction window (= the pi window: a DOWN raster group of 16 blocks)
+__device__ __forceinline__ uint32_t ld_relaxed_sys_u32(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void fuse_bf16x8_acc(float (&a)[8], const uint4& v) {
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 }
             }
         }
-    } else if (FUSED && !UP && warp == 3) {
+    } else if (FUSED && !UP && warp >= 4 - FUSE_WARPS && warp < 4) {
         // ------------------------------------------------------------ fused all-reduce (window granular)
         // Windows owned by this rank (w % G == rank), in raster order: wait until every rank's epilogue warps have
         // counted all their tiles of the window (4 per block and column tile), then this CTA reduces its slice of
@@ -383,46 +384,83 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         const int nwin = (args.M + FUSE_WIN - 1) / FUSE_WIN;
         const int64_t K8 = args.K / 8;
         const int rpc = (FUSE_WIN + gridDim.x - 1) / gridDim.x;  // rows of a window per CTA
-        const uint32_t* flags = reinterpret_cast<const uint32_t*>(args.ptrs[args.rank] + args.flags_off);
+        const uint32_t* flags = reinterpret_cast<const uint32_t*>(args.ptrs[args.rank] + args.ptrs[args.G + 1]);
         const uint64_t mc = args.ptrs[args.G];
+        const int rl = (warp - (4 - FUSE_WARPS)) * 32 + lane;  // reducer lane
         for (int w = args.rank; w < nwin; w += args.G) {
             const int rows_w = min(FUSE_WIN, args.M - w * FUSE_WIN);
             const int blocks = (rows_w + GEMM_BM - 1) / GEMM_BM;
             const uint32_t target = static_cast<uint32_t>(4 * blocks * args.NJ * args.G);
-            if (lane == 0) {
+            // one poller per CTA (relaxed loads: an acquire load per poll would invalidate L1 each time under the
+            // running GEMM), one acquire fence on success, then a named barrier releases the reducer warps
+            if (rl == 0) {
                 long long spins = 0;
                 uint32_t v;
-                while (static_cast<int32_t>((v = ld_acquire_sys_u32(flags + w)) - target) < 0) {
-                    __nanosleep(200);
-                    if (++spins == (1ll << 28)) {  // > 1 min: a rank is gone; fail the launch instead of hanging
+                while (static_cast<int32_t>((v = ld_relaxed_sys_u32(flags + w)) - target) < 0) {
+                    __nanosleep(500);
+                    if (++spins == (1ll << 27)) {  // > 1 min: a rank is gone; fail the launch instead of hanging
                         printf("sffn fused: cta %d window %d counter %u target %u\n", blockIdx.x, w, v, target);
                         __trap();
                     }
                 }
+                asm volatile("fence.acq_rel.sys;" ::: "memory");
             }
-            __syncwarp();
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * FUSE_WARPS) : "memory");
             const int r0 = w * FUSE_WIN + blockIdx.x * rpc;
             const int r1 = min(w * FUSE_WIN + rows_w, r0 + rpc);
             if (r1 <= r0) continue;
             const int64_t q0 = static_cast<int64_t>(r0) * K8, q1 = static_cast<int64_t>(r1) * K8;
-            for (int64_t q = q0 + lane; q < q1; q += 32) {
+            // FUSE_U independent 16-byte loads in flight per lane before the stores (one or two warps per SM)
+            for (int64_t qb = q0 + rl; qb < q1; qb += FUSE_U * 32 * FUSE_WARPS) {
                 if (mc) {
-                    uint4 v;
-                    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                 : "l"(reinterpret_cast<uint4*>(mc) + q)
-                                 : "memory");
-                    asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(
-                                     reinterpret_cast<uint4*>(mc) + q),
-                                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                                 : "memory");
+                    uint4 v[FUSE_U];
+#pragma unroll
+                    for (int u = 0; u < FUSE_U; ++u) {
+                        const int64_t q = qb + u * 32 * FUSE_WARPS;
+                        if (q < q1)
+                            asm volatile(
+                                "multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                                : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                                : "l"(reinterpret_cast<uint4*>(mc) + q)
+                                : "memory");
+                    }
+#pragma unroll
+                    for (int u = 0; u < FUSE_U; ++u) {
+                        const int64_t q = qb + u * 32 * FUSE_WARPS;
+                        if (q < q1)
+                            asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(
+                                             reinterpret_cast<uint4*>(mc) + q),
+                                         "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                                         : "memory");
+                    }
                 } else {
-                    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                    for (int p = 0; p < args.G; ++p)
-                        fuse_bf16x8_acc(a, __ldcv(reinterpret_cast<const uint4*>(args.ptrs[p]) + q));
-                    const uint4 o = make_uint4(pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]), pack_bf16x2(a[4], a[5]),
-                                               pack_bf16x2(a[6], a[7]));
-                    for (int p = 0; p < args.G; ++p) reinterpret_cast<uint4*>(args.ptrs[p])[q] = o;
+                    float acc8[FUSE_U][8];
+#pragma unroll
+                    for (int u = 0; u < FUSE_U; ++u)
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) acc8[u][i] = 0.f;
+                    for (int p = 0; p < args.G; ++p) {
+                        const uint4* src = reinterpret_cast<const uint4*>(args.ptrs[p]);
+                        uint4 v[FUSE_U];
+#pragma unroll
+                        for (int u = 0; u < FUSE_U; ++u) {
+                            const int64_t q = qb + u * 32 * FUSE_WARPS;
+                            v[u] = q < q1 ? __ldcv(src + q) : make_uint4(0, 0, 0, 0);
+                        }
+#pragma unroll
+                        for (int u = 0; u < FUSE_U; ++u) fuse_bf16x8_acc(acc8[u], v[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < FUSE_U; ++u) {
+                        const int64_t q = qb + u * 32 * FUSE_WARPS;
+                        if (q < q1) {
+                            const uint4 o = make_uint4(pack_bf16x2(acc8[u][0], acc8[u][1]),
+                                                       pack_bf16x2(acc8[u][2], acc8[u][3]),
+                                                       pack_bf16x2(acc8[u][4], acc8[u][5]),
+                                                       pack_bf16x2(acc8[u][6], acc8[u][7]));
+                            for (int p = 0; p < args.G; ++p) reinterpret_cast<uint4*>(args.ptrs[p])[q] = o;
+                        }
+                    }
                 }
             }
         }
@@ -578,7 +616,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     __syncwarp();
                     if (lane == 0) {
                         const int w = b * GEMM_BM / FUSE_WIN;
-                        uint32_t* f = reinterpret_cast<uint32_t*>(args.ptrs[w % args.G] + args.flags_off) + w;
+                        uint32_t* f = reinterpret_cast<uint32_t*>(args.ptrs[w % args.G] + args.ptrs[args.G + 1]) + w;
                         atomicAdd_system(f, 1u);
                     }
                 }

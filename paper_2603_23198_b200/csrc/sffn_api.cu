@@ -307,7 +307,6 @@ int64_t union_dense_nnz(int64_t N, bool has_tma_path) {
 struct FuseParams {
     const uint64_t* ptrs;  // device: G window bases + multicast base (0 if none)
     int G, rank;
-    int64_t flags_off;
 };
 
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
@@ -458,7 +457,6 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         ud.ptrs = fuse->ptrs;
         ud.G = fuse->G;
         ud.rank = fuse->rank;
-        ud.flags_off = fuse->flags_off;
         { union_gemm_kernel<false, true><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
     } else {
         { union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
@@ -585,7 +583,7 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
 // symmetric window (Y) and reduces 2048-row windows across the ranks as they complete (sffn_comm.cu).
 int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
                         int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
-                        const uint64_t* ptrs, int G, int rank, int64_t flags_off, void* stream) {
+                        const uint64_t* ptrs, int G, int rank, void* stream) {
     int r = pack_checks(X, Wg, M, K, N, T, C, workspace);
     if (r != SFFN_OK) return r;
     if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
@@ -599,7 +597,7 @@ int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const voi
     int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
     if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz)) != SFFN_OK) return r;
-    FuseParams fp{ptrs, G, rank, flags_off};
+    FuseParams fp{ptrs, G, rank};
     return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
 }
 

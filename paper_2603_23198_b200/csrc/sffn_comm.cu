@@ -24,24 +24,27 @@ struct sffn_comm {
     ncclWindow_t win = nullptr;
     ncclDevComm dev{};
     bool has_dev = false, multimem = false;
-    // fused window-granular all-reduce (sffn_sharded_forward_fused): peer window bases + multicast base on the device;
-    // two sets of per-window arrival counters after the partial-Y region (call parity alternates them; each call
-    // zeroes its set after its closing barrier, when no rank can still touch it and before any rank's call + 2)
+    // fused window-granular all-reduce (sffn_sharded_forward_fused).  Device table d_ptrs: [0, G) peer window
+    // bases, [G] multicast base (0 if none), [G + 1] byte offset of the counter set the next call uses.  Two sets
+    // of per-window arrival counters follow the partial-Y region; each call's closing kernel zeroes the set it used
+    // (after the barrier: no rank can still touch it) and flips [G + 1] — device-side, so graph replays alternate.
     uint64_t* d_ptrs = nullptr;
     int64_t flags_off = 0, nwin = 0;
-    uint32_t fuse_calls = 0;
 };
 
 extern "C" int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
                                    int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes,
                                    uint32_t* d_overflow, const uint64_t* ptrs, int G, int rank,
-                                   int64_t flags_off, void* stream);
+                                   void* stream);
 
-// device: ptrs[p] = rank p's window base through the LSA mapping, ptrs[G] = the window's multicast address (or 0)
-__global__ void sym_ptrs_kernel(ncclDevComm dc, ncclWindow_t win, int G, int multimem, uint64_t* ptrs) {
+// device: ptrs[p] = rank p's window base through the LSA mapping, ptrs[G] = the window's multicast address (or 0),
+// ptrs[G + 1] = the first counter set's offset
+__global__ void sym_ptrs_kernel(ncclDevComm dc, ncclWindow_t win, int G, int multimem, int64_t flags_off,
+                                uint64_t* ptrs) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int p = 0; p < G; ++p) ptrs[p] = reinterpret_cast<uint64_t>(ncclGetLsaPointer(win, 0, p));
     ptrs[G] = multimem ? reinterpret_cast<uint64_t>(ncclGetLsaMultimemPointer(win, 0, dc)) : 0ull;
+    ptrs[G + 1] = static_cast<uint64_t>(flags_off);
 }
 
 // ---------------------------------------------------------------- NEXT-3: symmetric-memory all-reduce kernel
@@ -71,6 +74,73 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Grid-stride loops over 16-byte elements [q0, q1) with SYM_U independent loads in flight per thread before the
+// stores (one load per iteration leaves the copy latency bound at ~3 TB/s).
+constexpr int SYM_U = 4;
+__device__ __forceinline__ void sym_copy(const uint4* src, uint4* dst, int64_t q0, int64_t q1) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t qb = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; qb < q1; qb += SYM_U * stride) {
+        uint4 v[SYM_U];
+#pragma unroll
+        for (int u = 0; u < SYM_U; ++u)
+            if (qb + u * stride < q1) v[u] = src[qb + u * stride];
+#pragma unroll
+        for (int u = 0; u < SYM_U; ++u)
+            if (qb + u * stride < q1) dst[qb + u * stride] = v[u];
+    }
+}
+// sum over the ranks' windows of [q0, q1): multimem.ld_reduce through the switch (mc != null), else P2P loads with
+// fp32 accumulation; the result goes to every window (bcast: multimem.st / P2P stores) or to out[q - q0]
+__device__ __forceinline__ void sym_reduce(ncclWindow_t win, uint4* mc, int nranks, int64_t q0, int64_t q1, bool bcast,
+                                           uint4* out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t qb = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; qb < q1; qb += SYM_U * stride) {
+        uint4 v[SYM_U];
+        if (mc) {
+#pragma unroll
+            for (int u = 0; u < SYM_U; ++u)
+                if (qb + u * stride < q1)
+                    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                                 : "l"(mc + qb + u * stride)
+                                 : "memory");
+        } else {
+            float a[SYM_U][8];
+#pragma unroll
+            for (int u = 0; u < SYM_U; ++u)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a[u][i] = 0.f;
+            for (int p = 0; p < nranks; ++p) {
+                const uint4* src = static_cast<const uint4*>(ncclGetLsaPointer(win, 0, p));
+                uint4 t[SYM_U];
+#pragma unroll
+                for (int u = 0; u < SYM_U; ++u)
+                    t[u] = qb + u * stride < q1 ? __ldcg(src + qb + u * stride) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < SYM_U; ++u) bf16x8_acc(a[u], t[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < SYM_U; ++u)
+                v[u] = make_uint4(bf16x2_rn(a[u][0], a[u][1]), bf16x2_rn(a[u][2], a[u][3]),
+                                  bf16x2_rn(a[u][4], a[u][5]), bf16x2_rn(a[u][6], a[u][7]));
+        }
+#pragma unroll
+        for (int u = 0; u < SYM_U; ++u) {
+            const int64_t q = qb + u * stride;
+            if (q >= q1) continue;
+            if (!bcast) {
+                out[q - q0] = v[u];
+            } else if (mc) {
+                asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(mc + q),
+                             "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                             : "memory");
+            } else {
+                for (int p = 0; p < nranks; ++p) static_cast<uint4*>(ncclGetLsaPointer(win, 0, p))[q] = v[u];
+            }
+        }
+    }
+}
+
 // Reduce-scatter variant (sequence-parallel consumers): rank r reduces its 1/G slice of rows
 // [row0, row1) from every window (multimem.ld_reduce, or P2P loads) and writes it only to its own output; one LSA
 // barrier before (partials complete everywhere) and one after (no rank overwrites its window, i.e. starts the next
@@ -80,41 +150,26 @@ __global__ void __launch_bounds__(SYM_THREADS) sym_reduce_scatter_kernel(ncclDev
                                                                         uint4* Yr) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    if (multimem) {
-        const uint4* mc = static_cast<const uint4*>(ncclGetLsaMultimemPointer(win, 0, dc));
-        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
-            uint4 v;
-            asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                         : "l"(mc + q)
-                         : "memory");
-            Yr[q - q0] = v;
-        }
-    } else {
-        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
-            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int p = 0; p < nranks; ++p)
-                bf16x8_acc(a, __ldcg(static_cast<const uint4*>(ncclGetLsaPointer(win, 0, p)) + q));
-            Yr[q - q0] = make_uint4(bf16x2_rn(a[0], a[1]), bf16x2_rn(a[2], a[3]), bf16x2_rn(a[4], a[5]),
-                                    bf16x2_rn(a[6], a[7]));
-        }
-    }
+    sym_reduce(win, multimem ? static_cast<uint4*>(ncclGetLsaMultimemPointer(win, 0, dc)) : nullptr, nranks, q0, q1,
+               false, Yr);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
 }
 
 // After the fused DOWN: every rank's reducers are done (LSA barrier), then the local copy window -> Y.
 __global__ void __launch_bounds__(SYM_THREADS) sym_finish_kernel(ncclDevComm dc, ncclWindow_t win, int64_t n16,
-                                                                int multimem, uint4* Y, int64_t flag0, int64_t nwin) {
+                                                                int multimem, uint4* Y, uint64_t* cur_off,
+                                                                int64_t flags_off, int64_t nwin_max, int64_t nwin) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
     const uint4* loc = static_cast<const uint4*>(ncclGetLocalPointer(win, 0));
     if (blockIdx.x == 0) {  // this call's counter set: every rank's increments and this rank's waits are done
-        uint32_t* flags = static_cast<uint32_t*>(ncclGetLocalPointer(win, 0)) + flag0;
+        const int64_t off = static_cast<int64_t>(*cur_off);
+        uint32_t* flags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ncclGetLocalPointer(win, 0)) + off);
         for (int64_t w = threadIdx.x; w < nwin; w += blockDim.x) flags[w] = 0;
+        __syncthreads();
+        if (threadIdx.x == 0) *cur_off = static_cast<uint64_t>(off == flags_off ? flags_off + 4 * nwin_max : flags_off);
     }
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n16; q += stride) Y[q] = loc[q];
+    sym_copy(loc, Y, 0, n16);
 }
 
 __global__ void __launch_bounds__(SYM_THREADS) sym_allreduce_kernel(ncclDevComm dc, ncclWindow_t win, int64_t n16,
@@ -122,32 +177,10 @@ __global__ void __launch_bounds__(SYM_THREADS) sym_allreduce_kernel(ncclDevComm 
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
     const int64_t q0 = n16 * rank / nranks, q1 = n16 * (rank + 1) / nranks;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    if (multimem) {
-        uint4* mc = static_cast<uint4*>(ncclGetLsaMultimemPointer(win, 0, dc));
-        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
-            uint4 v;
-            asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                         : "l"(mc + q)
-                         : "memory");
-            asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(mc + q), "r"(v.x),
-                         "r"(v.y), "r"(v.z), "r"(v.w)
-                         : "memory");
-        }
-    } else {
-        for (int64_t q = q0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < q1; q += stride) {
-            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int p = 0; p < nranks; ++p)
-                bf16x8_acc(a, __ldcg(static_cast<const uint4*>(ncclGetLsaPointer(win, 0, p)) + q));
-            const uint4 o = make_uint4(bf16x2_rn(a[0], a[1]), bf16x2_rn(a[2], a[3]), bf16x2_rn(a[4], a[5]),
-                                       bf16x2_rn(a[6], a[7]));
-            for (int p = 0; p < nranks; ++p) static_cast<uint4*>(ncclGetLsaPointer(win, 0, p))[q] = o;
-        }
-    }
+    sym_reduce(win, multimem ? static_cast<uint4*>(ncclGetLsaMultimemPointer(win, 0, dc)) : nullptr, nranks, q0, q1,
+               true, nullptr);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
-    const uint4* loc = static_cast<const uint4*>(ncclGetLocalPointer(win, 0));
-    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n16; q += stride) Y[q] = loc[q];
+    sym_copy(static_cast<const uint4*>(ncclGetLocalPointer(win, 0)), Y, 0, n16);
 }
 
 static int ensure_events(sffn_comm* c, int n) {
@@ -256,7 +289,7 @@ int sffn_comm_symmetric_init(sffn_comm* c, int64_t max_rows, int64_t K) {
         return SFFN_ERR_UNSUPPORTED;
     }
     if (cudaMemset(static_cast<uint8_t*>(c->sym_buf) + flags_off, 0, static_cast<size_t>(8 * nwin)) != cudaSuccess ||
-        cudaMalloc(&c->d_ptrs, static_cast<size_t>(c->nranks + 1) * 8) != cudaSuccess) {
+        cudaMalloc(&c->d_ptrs, static_cast<size_t>(c->nranks + 2) * 8) != cudaSuccess) {
         ncclDevCommDestroy(c->nccl, &c->dev);
         ncclCommWindowDeregister(c->nccl, c->win);
         ncclMemFree(c->sym_buf);
@@ -264,7 +297,7 @@ int sffn_comm_symmetric_init(sffn_comm* c, int64_t max_rows, int64_t K) {
         c->win = nullptr;
         return SFFN_ERR_CUDA;
     }
-    sym_ptrs_kernel<<<1, 32>>>(c->dev, c->win, c->nranks, req.lsaMultimem ? 1 : 0, c->d_ptrs);
+    sym_ptrs_kernel<<<1, 32>>>(c->dev, c->win, c->nranks, req.lsaMultimem ? 1 : 0, flags_off, c->d_ptrs);
     if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return SFFN_ERR_CUDA;
     c->flags_off = flags_off;
     c->nwin = nwin;
@@ -331,13 +364,12 @@ int sffn_sharded_forward_fused(sffn_comm* c, const void* X, const void* Wg_s, co
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     // the DOWN GEMM writes the partial Y into the window and reduces each 2048-row window across the ranks as soon as
     // every rank has counted it; then one barrier (all windows reduced everywhere) and the local copy window -> Y
-    const int64_t foff = c->flags_off + 4 * c->nwin * (c->fuse_calls & 1);
     int r = sffn__forward_fused(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, c->sym_buf, workspace, ws_bytes,
-                                d_overflow, c->d_ptrs, c->nranks, c->rank, foff, stream);
+                                d_overflow, c->d_ptrs, c->nranks, c->rank, stream);
     if (r != SFFN_OK) return r;
-    ++c->fuse_calls;
     sym_finish_kernel<<<SYM_CTAS, SYM_THREADS, 0, st>>>(c->dev, c->win, M * K / 8, c->multimem ? 1 : 0,
-                                                       static_cast<uint4*>(Y), foff / 4, (M + 2047) / 2048);
+                                                       static_cast<uint4*>(Y), c->d_ptrs + c->nranks + 1,
+                                                       c->flags_off, c->nwin, (M + 2047) / 2048);
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 

@@ -35,6 +35,20 @@ def main():
             Y = comm.sharded_forward_fused(X[:rows].contiguous(), Wg, Wu, Wd, 256, 8)
             torch.cuda.synchronize()
             assert torch.equal(Y.view(torch.int16), ref_r.view(torch.int16)), f"rows {rows}"
+        # captured into a CUDA graph and replayed: the counter set alternates on the device
+        Yg = torch.empty_like(ref)
+        wsg = torch.empty(sffn.workspace_bytes(cfg.M, cfg.K, cfg.N, 256, 8, "union"), dtype=torch.uint8, device="cuda")
+        comm.sharded_forward_fused(X, Wg, Wu, Wd, 256, 8, out=Yg, workspace=wsg)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            comm.sharded_forward_fused(X, Wg, Wu, Wd, 256, 8, out=Yg, workspace=wsg)
+        for it in range(3):
+            Yg.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(Yg.view(torch.int16), ref.view(torch.int16)), f"replay {it}"
+        print("graph replays ok", flush=True)
         try:
             comm.sharded_forward_fused(torch.zeros(9000, cfg.K, dtype=torch.bfloat16, device="cuda"), Wg, Wu, Wd)
             raise AssertionError("M above the window accepted")

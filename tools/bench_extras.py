@@ -59,6 +59,14 @@ res["paper_design_train_fwd_ms"] = res["pack_ms"] + res["hybrid_train_fwd_ms"]
 # the same outputs (Y, h_g and h in the hybrid format) through the union tensor-core path in one call
 res["forward_train_union_ms"] = t(lambda: sffn.forward_train(X, Wg, Wu, Wd, T, C, ell_w=ELL_W, dense_cap=M // 8,
                                                              out=Y, workspace=ws))
+# NEXT-3 on a 1-rank communicator (one GPU): the cost the reduction machinery adds to the forward when there is
+# nothing to reduce — symmetric window + reduction kernel + copy-out vs the same reduction fused into the DOWN GEMM
+comm = sffn.Comm(0, 1, torch.cuda.current_device())
+if comm.symmetric_init(M, K):
+    res["sym_1rank_ms"] = t(lambda: comm.sharded_forward_sym(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, algo="union"))
+    res["fused_1rank_ms"] = t(lambda: comm.sharded_forward_fused(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws))
+    res["forward_union_ms_again"] = t(lambda: sffn.forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws))
+comm.close()
 # fp32 mode (correctness mode; SIMT fp32 GEMM) on a row slice to bound the time
 Mf = min(M, 4096)
 Xf = torch.from_numpy(synth.gen_x(cfg, 0, Mf, dtype="f32", p=p)).cuda()
