@@ -305,8 +305,9 @@ int64_t union_dense_nnz(int64_t N, bool has_tma_path) {
 
 // NEXT-3 fused all-reduce parameters of the DOWN kernel (sffn_sharded_forward_fused; null: plain DOWN)
 struct FuseParams {
-    const uint64_t* ptrs;  // device: G window bases + multicast base (0 if none)
+    const uint64_t* ptrs;  // device: G window bases, multicast base (0 if none), counter-set offset
     int G, rank;
+    int phase;  // 0: the whole up/down; 1: everything before the DOWN kernel; 2: the DOWN kernel only
 };
 
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
@@ -337,38 +338,41 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     // row permutation pi (per 2048-row window, descending stored nnz) and the permuted copy of X
     int* rnnz = reinterpret_cast<int*>(base + L.nnz);
     int* bctr = reinterpret_cast<int*>(base + L.bctr);  // union_meta_kernel counters (zeroed by union_rank_kernel)
-    if (!nnz_ready) {
-        { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
+    const int phase = fuse ? fuse->phase : 0;
+    if (phase != 2) {
+        if (!nnz_ready) {
+            { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
+            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+        }
+        { union_rank_kernel<<<dim3(static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_SPLIT), PERM_W / PERM_SPLIT, 0,
+                            st>>>(rnnz, (int)M, perm, um.umask, NB * (N / 32), bctr, (int)NB + 1); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    }
-    { union_rank_kernel<<<dim3(static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_SPLIT), PERM_W / PERM_SPLIT, 0,
-                        st>>>(rnnz, (int)M, perm, um.umask, NB * (N / 32), bctr, (int)NB + 1); note_launch(); }
-    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    if (gated) {
-        { permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
-            static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp)); note_launch(); }
-        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    }
+        if (gated) {
+            { permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+                static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp)); note_launch(); }
+            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+        }
 
-    // union lists + the UP work list (one launch), then the compact gate lists (gated) or the scattered G (non-gated)
-    const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
-    const int sms_meta = dev_info().sms;
-    // CTAs per union block: a power of two (it must divide the block rows), up to ~1.5 waves of CTAs
-    int split = 1;
-    while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms_meta) split *= 2;
-    { union_meta_kernel<<<static_cast<unsigned>(NB * split), UB_THREADS, ub_smem, st>>>(
-        tw, (int)M, (int)N, T, C, um, perm, bctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split,
-        union_dense_units(N, BR == 128 && N >= 256), rnnz, union_dense_nnz(N, BR == 128 && N >= 256)); note_launch(); }
-    if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    if (gated) {
-        { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
-            tw, (int)M, (int)N, T, C, um, perm); note_launch(); }
+        // union lists + the UP work list (one launch), then the compact gate lists (gated) or the scattered G (non-gated)
+        const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
+        const int sms_meta = dev_info().sms;
+        // CTAs per union block: a power of two (it must divide the block rows), up to ~1.5 waves of CTAs
+        int split = 1;
+        while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms_meta) split *= 2;
+        { union_meta_kernel<<<static_cast<unsigned>(NB * split), UB_THREADS, ub_smem, st>>>(
+            tw, (int)M, (int)N, T, C, um, perm, bctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split,
+            union_dense_units(N, BR == 128 && N >= 256), rnnz, union_dense_nnz(N, BR == 128 && N >= 256)); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    }
-    if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)
-        { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (BR / GS_ROWS)), 256, 0, st>>>(
-            tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm); note_launch(); }
-        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+        if (gated) {
+            { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
+                tw, (int)M, (int)N, T, C, um, perm); note_launch(); }
+            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+        }
+        if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)
+            { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (BR / GS_ROWS)), 256, 0, st>>>(
+                tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm); note_launch(); }
+            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+        }
     }
 
     CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
@@ -446,13 +450,14 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         if ((r = launch_pair(union_gemm_pair_kernel<false>, thc_ld, twd, ty, ud, dtiles)) != SFFN_OK) return r;
         return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
     }
-    if (gated) {
+    if (gated && phase != 2) {
         // UP: the number of (block, chunk) tiles is only known on the device; persistent grid.  For the
         // non-gated variant H_c already holds h = relu(x W_u) (the scattered TwELL values): no UP GEMM.
         { union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
     const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
+    if (phase == 1) return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
     if (fuse) {
         ud.ptrs = fuse->ptrs;
         ud.G = fuse->G;
@@ -583,7 +588,7 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
 // symmetric window (Y) and reduces 2048-row windows across the ranks as they complete (sffn_comm.cu).
 int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
                         int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
-                        const uint64_t* ptrs, int G, int rank, void* stream) {
+                        const uint64_t* ptrs, int G, int rank, int phase, void* stream) {
     int r = pack_checks(X, Wg, M, K, N, T, C, workspace);
     if (r != SFFN_OK) return r;
     if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
@@ -591,13 +596,15 @@ int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const voi
     if (ws_bytes < sffn_forward_workspace_bytes(M, K, N, T, C, SFFN_ALGO_UNION)) return SFFN_ERR_SHAPE;
     if ((r = check_device()) != SFFN_OK) return r;
     if (M == 0) return SFFN_OK;
+    if (phase < 0 || phase > 2) return SFFN_ERR_INVALID_ARG;
     uint32_t* tw = static_cast<uint32_t*>(workspace);
     const int64_t tw_bytes = align1k(sffn_twell_words(M, N, T, C) * 4);
     uint8_t* udws = static_cast<uint8_t*>(workspace) + tw_bytes;
     int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
+    FuseParams fp{ptrs, G, rank, phase};
+    if (phase == 2) return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
     if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz)) != SFFN_OK) return r;
-    FuseParams fp{ptrs, G, rank};
     return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
 }
 

@@ -34,7 +34,7 @@ struct sffn_comm {
 
 extern "C" int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
                                    int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes,
-                                   uint32_t* d_overflow, const uint64_t* ptrs, int G, int rank,
+                                   uint32_t* d_overflow, const uint64_t* ptrs, int G, int rank, int phase,
                                    void* stream);
 
 // device: ptrs[p] = rank p's window base through the LSA mapping, ptrs[G] = the window's multicast address (or 0),
@@ -365,7 +365,7 @@ int sffn_sharded_forward_fused(sffn_comm* c, const void* X, const void* Wg_s, co
     // the DOWN GEMM writes the partial Y into the window and reduces each 2048-row window across the ranks as soon as
     // every rank has counted it; then one barrier (all windows reduced everywhere) and the local copy window -> Y
     int r = sffn__forward_fused(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, c->sym_buf, workspace, ws_bytes,
-                                d_overflow, c->d_ptrs, c->nranks, c->rank, stream);
+                                d_overflow, c->d_ptrs, c->nranks, c->rank, 0, stream);
     if (r != SFFN_OK) return r;
     sym_finish_kernel<<<SYM_CTAS, SYM_THREADS, 0, st>>>(c->dev, c->win, M * K / 8, c->multimem ? 1 : 0,
                                                        static_cast<uint4*>(Y), c->d_ptrs + c->nranks + 1,

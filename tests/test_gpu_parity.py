@@ -347,6 +347,23 @@ def test_sharded_forward_fused_single_rank(sffn):
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_fused_allreduce_emulated(sffn, G):
+    """NEXT-3 fused all-reduce with G emulated ranks on one GPU (no NCCL): G windows, G hidden shards, the G fused
+    DOWN kernels co-resident on 1/G of the SMs each — counters at the window owners, cross-window P2P reduction:
+    every window == bf16(sum of the G partial outputs), counters == 4 x tiles x G at the owner, 0 elsewhere."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.dirname(here), here, os.environ.get("PYTHONPATH", "")]))
+    try:
+        out = subprocess.run([sys.executable, os.path.join(here, "fused_emul_case.py"), str(G)], capture_output=True,
+                             text=True, timeout=240, env=env)
+    except subprocess.TimeoutExpired:
+        pytest.fail("emulated fused all-reduce did not finish within 240 s")
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
+
+
 # ----------------------------------------------------------------- fp32 mode (R19): Y within 1e-5
 F32_TOL = 1e-5
 
