@@ -361,6 +361,20 @@ int sffn_sharded_forward_sym(sffn_comm* comm, const void* X, const void* Wg_s, c
                              int64_t M, int64_t K, int64_t N_local, int T, int C, void* Y, void* workspace,
                              size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream);
 
+/* sffn__forward_fused — INTERNAL (the engine of sffn_sharded_forward_fused, exported for the emulated-rank tests;
+ * not a stable API).  The union forward of one rank's shard whose DOWN GEMM writes the partial Y into Y (= this
+ * rank's window) and runs the window-granular reduction.  ptrs: DEVICE uint64 table of G + 2 entries — the G
+ * window base addresses as this rank can address them, the multicast address of the windows (0: P2P path), and
+ * the byte offset of the counter set to use (each window: Y region, then the per-2048-row-window uint32
+ * counters, zero before the call).  phase 0: the whole forward; 1: pack, metadata and the UP GEMM only; 2: the
+ * fused DOWN GEMM only (after a phase-1 call on the same workspace).  The G ranks' DOWN kernels must be able to
+ * run concurrently (a counter that never completes traps the kernel after about a minute).  No barrier, no
+ * counter reset and no copy-out: the caller does those (sffn_sharded_forward_fused's closing kernel).
+ * Errors: as sffn_forward; SFFN_ERR_UNSUPPORTED when the union path does not apply (N, SFFN_UNION_PAIR). */
+int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K,
+                        int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
+                        const uint64_t* ptrs, int G, int rank, int phase, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,8 @@ _SIGS = {
                                         _int, _vp]),
     "sffn_sharded_forward_fused": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp,
                                           _vp]),
+    "sffn__forward_fused": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp, _vp, _int,
+                                   _int, _int, _vp]),
     "sffn_hybrid_mm_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "sffn_hybrid_sddmm": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _int, _vp,
                                  _vp, _vp, _sz, _vp]),

@@ -4,7 +4,6 @@ pointer table lists the G windows, no multicast.  Phase 1 (pack, metadata, UP) r
 DOWN kernels run concurrently on G streams, each on 1/G of the SMs (SFFN_UNION_GRID), so the window counters, the
 owner mapping (w mod G) and the P2P reduction across G windows run as on G GPUs.  Expected: every window holds
 bf16(sum_r fp32(P_r)) with P_r = sffn_forward of rank r's shard, the reducer's summation order.  Prints OK."""
-import ctypes
 import os
 import sys
 
@@ -21,10 +20,7 @@ def main():
     import paper_2603_23198_b200 as sffn
     from paper_2603_23198_b200.sffn import lib
     L = lib()
-    f = L.sffn__forward_fused
-    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
-    f.restype = i32
-    f.argtypes = [vp, vp, vp, vp, i64, i64, i64, i32, i32, vp, vp, ctypes.c_size_t, vp, vp, i32, i32, i32, vp]
+    f = L.sffn__forward_fused  # signature bound by the package (internal entry, include/sffn.h)
     Nl = 1024
     cfg = synth.CONFIGS["1B"].replace(M=4500, K=640, N=Nl * G, Kb=32, sparsity=0.97)
     M, K, T, C = cfg.M, cfg.K, 256, 8
