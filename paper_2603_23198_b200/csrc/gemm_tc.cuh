@@ -32,6 +32,9 @@ constexpr int GEMM_SMEM_LIMIT = 232448;  // max dynamic shared memory per block 
 #ifndef SFFN_GEMM_POLB
 #define SFFN_GEMM_POLB 0  // L2 policy of the B (weight) tile loads: 0 evict_last (as A), 1 evict_first
 #endif
+#ifndef SFFN_TWELL_STORE_EF
+#define SFFN_TWELL_STORE_EF 1  // TwELL TMA stores hinted L2 evict_first (streaming output; gate GEMM -0.3%, ncu A/B)
+#endif
 #ifndef SFFN_GEMM_GROUP_M
 #define SFFN_GEMM_GROUP_M 32
 #endif
@@ -317,7 +320,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
+#if SFFN_TWELL_STORE_EF
+                    tma_store_2d_hint(&tmOut, stg, nb * ROW_WORDS, row0, policy_evict_first());
+#else
                     tma_store_2d(&tmOut, stg, nb * ROW_WORDS, row0);
+#endif
                     bulk_commit();
                 }
             } else if constexpr (EPI == EPI_F32) {
