@@ -176,7 +176,8 @@ int sffn_forward_nongated(const void* X, const void* Wu, const void* Wd, int64_t
  * chunk i+1 and the device->host copy of chunk i-1 overlap the compute of chunk i on two internal copy
  * streams (created once per device, event-ordered; no host synchronization).  The call is
  * stream-ordered on `stream`: Y_host is complete when `stream` reaches this point.
- *   stage: device buffer >= sffn_forward_host_stage_bytes(K, chunk_rows) (2 X + 2 Y chunk slots)
+ *   stage: device buffer >= sffn_forward_host_stage_bytes(K, chunk_rows) (2 X + 2 Y chunk slots); a larger
+ *     buffer gives more slots (stage_bytes / (2 x slot), up to one per chunk), so fewer copies wait for a slot
  *   workspace: >= sffn_forward_workspace_bytes(min(chunk_rows, M), K, N, T, C, algo); with twice that (plus 1 KiB
  *     alignment) consecutive chunks compute on two streams (`stream` and an internal one) so a chunk's kernels
  *     overlap the previous chunk's tail

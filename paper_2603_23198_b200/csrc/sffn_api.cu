@@ -898,11 +898,13 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     std::vector<int64_t> sizes = host_chunk_plan(M, rows);
     const int64_t nchunks = static_cast<int64_t>(sizes.size());
     const int64_t slot = align1k(rows * K * 2);
-    uint8_t* xs[HOST_SLOTS];
-    uint8_t* ys[HOST_SLOTS];
-    for (int q = 0; q < HOST_SLOTS; ++q) {
-        xs[q] = static_cast<uint8_t*>(stage) + q * slot;
-        ys[q] = static_cast<uint8_t*>(stage) + (HOST_SLOTS + q) * slot;
+    // staging slots: HOST_SLOTS by default; a larger stage buffer buys more (up to one per chunk), so a copy never
+    // waits for a slot still in use by a chunk two places back
+    const int64_t nslots = std::max<int64_t>(HOST_SLOTS, std::min<int64_t>(nchunks, static_cast<int64_t>(stage_bytes) / (2 * slot)));
+    std::vector<uint8_t*> xs(static_cast<size_t>(nslots)), ys(static_cast<size_t>(nslots));
+    for (int64_t q = 0; q < nslots; ++q) {
+        xs[static_cast<size_t>(q)] = static_cast<uint8_t*>(stage) + q * slot;
+        ys[static_cast<size_t>(q)] = static_cast<uint8_t*>(stage) + (nslots + q) * slot;
     }
     // events: per chunk h2d done, compute done, d2h done
     std::vector<cudaEvent_t> ev(static_cast<size_t>(3 * nchunks + 1));
@@ -918,15 +920,15 @@ int sffn_forward_host(const void* X_host, const void* Wg, const void* Wu, const 
     for (int64_t i = 0; i < nchunks && r == SFFN_OK; r0 += sizes[static_cast<size_t>(i)], ++i) {
         const int64_t mr = sizes[static_cast<size_t>(i)];
         const size_t bytes = static_cast<size_t>(mr * K * 2);
-        const int sl = static_cast<int>(i % HOST_SLOTS);
-        if (i >= HOST_SLOTS) cudaStreamWaitEvent(cs.h2d, E(1, i - HOST_SLOTS), 0);  // X slot free: chunk computed
+        const size_t sl = static_cast<size_t>(i % nslots);
+        if (i >= nslots) cudaStreamWaitEvent(cs.h2d, E(1, i - nslots), 0);  // X slot free: chunk computed
         if (cudaMemcpyAsync(xs[sl], static_cast<const uint8_t*>(X_host) + r0 * K * 2, bytes, cudaMemcpyHostToDevice,
                             cs.h2d) != cudaSuccess) { r = SFFN_ERR_CUDA; break; }
         cudaEventRecord(E(0, i), cs.h2d);
         const int cw = static_cast<int>(i & 1);  // compute stream / workspace half: chunk i-2 used it, ordered
         cudaStream_t cs_i = cst[cw];
         cudaStreamWaitEvent(cs_i, E(0, i), 0);
-        if (i >= HOST_SLOTS) cudaStreamWaitEvent(cs_i, E(2, i - HOST_SLOTS), 0);  // Y slot free: chunk copied out
+        if (i >= nslots) cudaStreamWaitEvent(cs_i, E(2, i - nslots), 0);  // Y slot free: chunk copied out
         r = sffn_forward(xs[sl], Wg, Wu, Wd, mr, K, N, T, C, ys[sl], wss[cw], wsz, d_overflow, algo, cs_i);
         if (r != SFFN_OK) break;
         cudaEventRecord(E(1, i), cs_i);

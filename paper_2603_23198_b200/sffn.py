@@ -230,8 +230,9 @@ def forward_host_chunks(M: int, chunk_rows: int = 4096) -> list:
 
 
 def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, stage=None,
-                 overflow=None, algo="auto", chunk_rows: int = 4096, stream=None) -> torch.Tensor:
-    """Sparse forward with X / Y in (pinned) host memory; copies overlap compute (sffn_forward_host)."""
+                 overflow=None, algo="auto", chunk_rows: int = 4096, stream=None, stage_slots: int = 2) -> torch.Tensor:
+    """Sparse forward with X / Y in (pinned) host memory; copies overlap compute (sffn_forward_host).
+    stage_slots: X / Y staging slots on the device (>= 2; more lets copies run further ahead)."""
     M, K = x_host.shape
     N = wg.shape[0]
     if x_host.is_cuda or x_host.dtype != torch.bfloat16 or not x_host.is_contiguous():
@@ -243,7 +244,7 @@ def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspa
     wsz = workspace_bytes(min(rows, M), K, N, T, C, a)
     # two workspaces: consecutive chunks compute on two streams (sffn_forward_host)
     workspace = _ws((wsz + 1023) // 1024 * 1024 + wsz, wg.device, workspace)
-    stage = _ws(int(lib().sffn_forward_host_stage_bytes(K, rows)), wg.device, stage)
+    stage = _ws(int(lib().sffn_forward_host_stage_bytes(K, rows)) * max(2, stage_slots) // 2, wg.device, stage)
     _chk(lib().sffn_forward_host(ctypes.c_void_p(x_host.data_ptr()), _bf16(wg, "wg"), _bf16(wu, "wu"),
                                  _bf16(wd, "wd"), M, K, N, T, C, ctypes.c_void_p(out.data_ptr()), _p(workspace),
                                  workspace.numel() * workspace.element_size(), _p(stage),

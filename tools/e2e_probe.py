@@ -42,14 +42,22 @@ for rows in (2048, 4096, 8192):
     print(f"forward M={rows}: {t:.3f} ms  (x{M//rows} = {t*M/rows:.2f} ms)")
 res = {}
 wsz = sffn.workspace_bytes(16384, K, N, T, C, "union")
-wsd = torch.empty((wsz + 1023) // 1024 * 1024 + wsz, dtype=torch.uint8, device="cuda")
+wsd2 = torch.empty((wsz + 1023) // 1024 * 1024 + wsz, dtype=torch.uint8, device="cuda")
 chunks = [int(c) for c in os.environ.get("CHUNKS", "4096,8192,16384").split(",")]
-for c in chunks:
-    res[c] = []
+slots = [int(c) for c in os.environ.get("SLOTS", "2").split(",")]
+duals = [int(c) for c in os.environ.get("DUAL", "1").split(",")]
+arms = [(c, q, d) for c in chunks for q in slots for d in duals]
+stg = torch.empty(int(sffn.sffn.lib().sffn_forward_host_stage_bytes(K, max(chunks))) * max(slots) // 2,
+                  dtype=torch.uint8, device="cuda")
+for a in arms:
+    res[a] = []
 for rnd in range(4):
-    for c in (chunks if rnd % 2 == 0 else chunks[::-1]):
-        res[c].append(tim(lambda: sffn.forward_host(Xh, Wg, Wu, Wd, T, C, out=Yh, workspace=wsd, algo="union",
-                                                    chunk_rows=c), n=3))
-for c in chunks:
-    print(f"forward_host chunk={c} {sffn.forward_host_chunks(M, c)}: median {np.median(res[c]):.3f} ms  "
-          f"{[round(x, 3) for x in res[c]]}")
+    for c, q, d in (arms if rnd % 2 == 0 else arms[::-1]):
+        st = stg[:int(sffn.sffn.lib().sffn_forward_host_stage_bytes(K, c)) * q // 2]
+        w1 = sffn.workspace_bytes(c, K, N, T, C, "union")
+        wsd = wsd2 if d else wsd2[:w1]  # one workspace: a single compute stream
+        res[(c, q, d)].append(tim(lambda: sffn.forward_host(Xh, Wg, Wu, Wd, T, C, out=Yh, workspace=wsd,
+                                                            algo="union", chunk_rows=c, stage=st), n=3))
+for c, q, d in arms:
+    print(f"forward_host chunk={c} slots={q} dual={d} {sffn.forward_host_chunks(M, c)}: "
+          f"median {np.median(res[(c, q, d)]):.3f} ms  {[round(x, 3) for x in res[(c, q, d)]]}")
