@@ -79,7 +79,10 @@ struct GemmArgs {
     int64_t ld_out;      // EPI_F32 row stride (elements)
     const int* m_dev;    // optional device row count: rows >= min(M, *m_dev) are skipped (dense backup rows)
     int* row_nnz;        // EPI_TWELL, may be null: += stored entries (min(count, cap)) of each row (zeroed by caller)
+    int* tile_ctr;       // optional dynamic tile scheduler: tiles claimed in raster order by atomicAdd on this
+                         // counter (zeroed by the caller); null: static striding (tile += grid)
 };
+constexpr int GT_RING = 4;  // dynamic scheduler: tile ring depth (claims ahead of the slowest reader)
 
 // MN-major 128B-swizzled operand: 64-column atoms 8 KB apart (LBO), 8-row groups 1 KB apart (SBO)
 __device__ __forceinline__ uint64_t umma_desc_sw128_mn_tc(uint32_t smem_addr) {
@@ -127,7 +130,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* sfull = tempty + 2;                           // [GT_RING] dynamic tile ring: slot published
+    uint64_t* sempty = sfull + GT_RING;                     // [GT_RING] slot read by every reader (leader's)
+    int* sched = reinterpret_cast<int*>(sempty + GT_RING);  // [GT_RING]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched + GT_RING);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -150,6 +156,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4 * PAIR);  // every epilogue warp of the pair releases the leader's accumulator
         }
+        for (int i = 0; i < GT_RING; ++i) {
+            mbar_init(&sfull[i], 1);
+            // readers: MMA thread + 4 epilogue warps per CTA (+ the peer's producer in pair mode)
+            mbar_init(&sempty[i], PAIR == 2 ? 10 : 5);
+        }
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -162,6 +173,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    // Tile sequence, identical for every role of both CTAs: static striding, or (args.tile_ctr) claims in raster
+    // order by the (leader's) producer thread, published through a GT_RING-deep ring (pair: into both CTAs'
+    // SMEM, st.shared::cluster + release.cluster arrive; readers release slots on the leader's sempty).  A CTA
+    // (pair) that starts late takes fewer tiles, so the kernel's end is not set by its latest-starting CTA.
+    const bool dyn = args.tile_ctr != nullptr;
+    const uint32_t sempty_leader = PAIR == 2 ? mapa_shared(sempty, 0) : 0u;
+    auto next_tile = [&](int it, int& ridx, uint32_t& rphase, bool arrive) -> int {
+        if (!dyn) {
+            const int t = first_tile + it * tile_step;
+            return t < num_tiles ? t : -1;
+        }
+        if (PAIR == 2) mbar_wait_cluster(&sfull[ridx], rphase);
+        else mbar_wait(&sfull[ridx], rphase);
+        const int t = *reinterpret_cast<volatile int*>(&sched[ridx]);
+        if (arrive) {
+            if (PAIR == 2) mbar_arrive_cluster(sempty_leader + 8u * static_cast<uint32_t>(ridx));
+            else mbar_arrive(&sempty[ridx]);
+        }
+        if (++ridx == GT_RING) {
+            ridx = 0;
+            rphase ^= 1;
+        }
+        return t;
+    };
+
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
@@ -173,7 +209,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #endif
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
+            int ridx = 0, widx = 0;
+            uint32_t rphase = 0, wphase = 0;
+            for (int it = 0;; ++it) {
+                int tile;
+                if (dyn && rank == 0) {  // the claiming thread
+                    if (PAIR == 2) mbar_wait_cluster(&sempty[widx], wphase ^ 1);
+                    else mbar_wait(&sempty[widx], wphase ^ 1);
+                    tile = atomicAdd(args.tile_ctr, 1);
+                    if (tile >= num_tiles) tile = -1;
+                    sched[widx] = tile;
+                    if (PAIR == 2) st_cluster_u32(mapa_shared(&sched[widx], 1), static_cast<uint32_t>(tile));
+                    mbar_arrive(&sfull[widx]);
+                    if (PAIR == 2) mbar_arrive_cluster(mapa_shared(&sfull[widx], 1));
+                    if (++widx == GT_RING) {
+                        widx = 0;
+                        wphase ^= 1;
+                    }
+                } else {
+                    tile = next_tile(it, ridx, rphase, true);
+                }
+                if (tile < 0) break;
                 int mb, nb;
                 gemm_tile_coords<GROUP>(tile, num_m, args.num_n, mb, nb);
                 for (int kb = 0; kb < nk; ++kb) {
@@ -221,7 +277,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
+            int ridx = 0;
+            uint32_t rphase = 0;
+            for (int it = 0;; ++it) {
+                const int tile = next_tile(it, ridx, rphase, true);
+                if (tile < 0) break;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
@@ -268,7 +328,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (PAIR == 2) mbar_arrive_remote(tempty_leader + 8u * static_cast<uint32_t>(a));
             else mbar_arrive(&tempty[a]);
         };
-        for (int tile = first_tile; tile < num_tiles; tile += tile_step) {
+        int ridx = 0;
+        uint32_t rphase = 0;
+        for (int it = 0;; ++it) {
+            const int tile = next_tile(it, ridx, rphase, lane == 0);
+            if (tile < 0) break;
             int mb, nb;
             gemm_tile_coords<GROUP>(tile, num_m, args.num_n, mb, nb);
             const int row0 = mb * PM + static_cast<int>(rank) * GEMM_BM + ew * 32;

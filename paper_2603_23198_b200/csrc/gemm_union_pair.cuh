@@ -21,9 +21,6 @@
 
 namespace sffn {
 
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
-}
 
 constexpr int UGP_B_BYTES = GEMM_B_BYTES / 2;                 // this CTA's half of the B tile (16 KB)
 constexpr int UGP_STAGE = GEMM_A_BYTES + UGP_B_BYTES;         // 32 KB

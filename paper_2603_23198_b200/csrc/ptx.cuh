@@ -185,6 +185,9 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
 // Arrive on an mbarrier given by its shared::cluster address (possibly in the peer CTA), .release at CLUSTER
 // scope: orders this thread's prior shared::cluster stores (e.g. a tile index written into the peer's SMEM)
 // before the arrival.  Compiles to MEMBAR.ALL.GPU + ERRBAR: use only where cross-CTA data is published.
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }

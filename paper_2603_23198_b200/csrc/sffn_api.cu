@@ -142,7 +142,7 @@ int check_device() {
 }
 
 int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
-              uint32_t* d_overflow, cudaStream_t st, int* row_nnz = nullptr) {
+              uint32_t* d_overflow, cudaStream_t st, int* row_nnz = nullptr, int* tile_ctr = nullptr) {
     // CTA-pair gate GEMM by default (SFFN_GATE_PAIR=0 selects the single-CTA kernel)
     static const bool pair = env_flag("SFFN_GATE_PAIR", true);
     CUtensorMap ta, tb, to;
@@ -158,6 +158,7 @@ int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, in
     args.T = T;
     args.overflow = d_overflow;
     args.row_nnz = row_nnz;
+    args.tile_ctr = env_flag("SFFN_GATE_DYN", false) ? tile_ctr : nullptr;  // measured neutral: off
 #define SFFN_PACK_CASE(CC)                                                                              \
     case CC:                                                                                            \
         return pair ? launch_gemm<EPI_TWELL, CC, 2>(ta, tb, tb, to, args, GEMM_BN, st)                  \
@@ -250,7 +251,7 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8)
     w.perm = o;  o = align1k(o + M * 4);
     w.xp = o;    o = align1k(o + M * K * 2);
     w.ctr = o;   o = align1k(o + 64);
-    w.nnz = o;   o = align1k(o + M * 4);
+    w.nnz = o;   o = align1k(o + M * 4 + 16);  // + the gate GEMM's tile counter (nnz[M])
     w.lmax = static_cast<int>((N / T) * (T / C - 1));  // most stored entries a row can have
     w.nchunk = static_cast<int>((N + 255) / 256);
     w.glist = o; o = align1k(o + NB * BR * static_cast<int64_t>(w.lmax) * 4);
@@ -575,8 +576,8 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
     if (resolve_algo(algo, N) == SFFN_ALGO_UNION) {
         // the gate GEMM epilogue also counts each row's stored entries (the union path's row order pi)
         int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
-        if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
-        if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz)) != SFFN_OK) return r;
+        if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M + 1) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+        if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz, nnz + M)) != SFFN_OK) return r;
         return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true);
     }
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
@@ -603,8 +604,8 @@ int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const voi
     int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
     FuseParams fp{ptrs, G, rank, phase};
     if (phase == 2) return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
-    if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
-    if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz)) != SFFN_OK) return r;
+    if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M + 1) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+    if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz, nnz + M)) != SFFN_OK) return r;
     return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
 }
 

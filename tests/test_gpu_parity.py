@@ -626,6 +626,37 @@ def test_union_all_blocks_dense(sffn):
     assert " passed" in r.stdout
 
 
+def test_gate_dynamic_scheduler(sffn, monkeypatch):
+    """The gate GEMM's optional dynamic tile scheduler (SFFN_GATE_DYN=1: atomic claims published through a tile
+    ring, both CTAs of a pair) gives the same TwELL and Y bit for bit as static striding, over repeated calls
+    (the counter lives in the forward's workspace and is zeroed per call)."""
+    cfg = synth.CONFIGS["1B"].replace(M=5000, K=512, N=2048, Kb=32, sparsity=0.97)
+    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    monkeypatch.setenv("SFFN_GATE_DYN", "0")
+    ws = torch.empty(sffn.workspace_bytes(cfg.M, cfg.K, cfg.N, 256, 8, "union"), dtype=torch.uint8, device="cuda")
+    ref = sffn.forward(X, Wg, Wu, Wd, 256, 8, algo="union", workspace=ws)
+    tw_ref = sffn.twell_view(ws, cfg.M, cfg.N, 8).clone()
+    monkeypatch.setenv("SFFN_GATE_DYN", "1")
+    for _ in range(3):
+        Y = sffn.forward(X, Wg, Wu, Wd, 256, 8, algo="union", workspace=ws)
+        torch.cuda.synchronize()
+        # slots past a tile's count are unspecified (staging leftovers): compare counts + valid prefixes
+        tw = sffn.twell_view(ws, cfg.M, cfg.N, 8)
+        assert oracle.valid_prefix_equal(words_np(tw), words_np(tw_ref), 256, 8).all()
+        assert torch.equal(Y.view(torch.int16), ref.view(torch.int16))
+
+
+def test_gate_dynamic_scheduler_single_cta(sffn):
+    """The same with the single-CTA gate GEMM (SFFN_GATE_PAIR=0 is read once per process: child pytest)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, SFFN_GATE_PAIR="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-m", "gpu", "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", "test_gate_dynamic_scheduler and not single_cta"], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("algo,expected", [("union", 7), ("gather", 2)])
 def test_launch_count(sffn, algo, expected):
     """sffn_launch_count (what bench.py reports as gpu_launches): one union forward = gate GEMM + rank + permute
