@@ -29,12 +29,6 @@ constexpr int GEMM_B_BYTES = GEMM_BN * GEMM_BK * 2;  // 32 KB
 constexpr int GEMM_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES;
 constexpr int GEMM_THREADS = 256;
 constexpr int GEMM_SMEM_LIMIT = 232448;  // max dynamic shared memory per block (227 KB)
-#ifndef SFFN_GEMM_POLB
-#define SFFN_GEMM_POLB 0  // L2 policy of the B (weight) tile loads: 0 evict_last (as A), 1 evict_first
-#endif
-#ifndef SFFN_TWELL_STORE_EF
-#define SFFN_TWELL_STORE_EF 1  // TwELL TMA stores hinted L2 evict_first (streaming output; gate GEMM -0.3%, ncu A/B)
-#endif
 #ifndef SFFN_GEMM_GROUP_M
 #define SFFN_GEMM_GROUP_M 32
 #endif
@@ -202,11 +196,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             const uint64_t pol = policy_evict_last();
-#if SFFN_GEMM_POLB == 1
-            const uint64_t polb = policy_evict_first();
-#else
-            const uint64_t polb = pol;
-#endif
             int stage = 0;
             uint32_t phase = 0;
             int ridx = 0, widx = 0;
@@ -245,7 +234,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                              nb * 128, pol);
                         else
                             tma_load_2d_pair(stB + stage * B_BYTES, &tmB, fb, kb * GEMM_BK,
-                                             nb * GEMM_BN + static_cast<int>(rank) * (GEMM_BN / 2), polb);
+                                             nb * GEMM_BN + static_cast<int>(rank) * (GEMM_BN / 2), pol);
                     } else {
                     mbar_arrive_expect_tx(&full[stage], GEMM_STAGE_BYTES);
                     tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, pol);
@@ -259,7 +248,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                             tma_load_2d(stB + stage * GEMM_B_BYTES + q * 8192, &tmB, &full[stage], nb * GEMM_BN + 64 * q,
                                         kb * GEMM_BK, pol);
                     } else {
-                        tma_load_2d(stB + stage * GEMM_B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN, polb);
+                        tma_load_2d(stB + stage * GEMM_B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN, pol);
                     }
                     }
                     if (++stage == S) {
@@ -384,11 +373,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-#if SFFN_TWELL_STORE_EF
+                    // TwELL is a streaming output: L2 evict_first keeps X / W_g resident (gate GEMM -0.3%, ncu A/B)
                     tma_store_2d_hint(&tmOut, stg, nb * ROW_WORDS, row0, policy_evict_first());
-#else
-                    tma_store_2d(&tmOut, stg, nb * ROW_WORDS, row0);
-#endif
                     bulk_commit();
                 }
             } else if constexpr (EPI == EPI_F32) {

@@ -38,17 +38,6 @@ struct UnionArgs {
 };
 
 // ---------------------------------------------------------------- fused all-reduce helpers (NEXT-3)
-#ifndef SFFN_UNION_H_EF
-#define SFFN_UNION_H_EF 0  // UP: H_c TMA stores hinted L2 evict_first
-#endif
-#ifndef SFFN_UNION_Y_EF
-#define SFFN_UNION_Y_EF 0  // DOWN: Y row stores hinted L2 evict_first
-#endif
-__device__ __forceinline__ void st_global_v4_evict_first(void* p, const uint4& v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-                 "r"(v.w), "l"(pol)
-                 : "memory");
-}
 constexpr int FUSE_WIN = 2048;
 constexpr int FUSE_WARPS = 2;  // reducer warps: 2 (idle after the TMEM allocation) and 3
 constexpr int FUSE_U = 8;      // 16-byte loads in flight per reducer lane  // rows per reduction window (= the pi window: a DOWN raster group of 16 blocks)
@@ -579,12 +568,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int q = 0; q < nbox; ++q)
-#if SFFN_UNION_H_EF
-                            tma_store_2d_hint(&tmOut, stg + q * 4096, p0 + 128 * h + 64 * q, row0, policy_evict_first());
-#else
-                            tma_store_2d(&tmOut, stg + q * 4096, p0 + 128 * h + 64 * q, row0);
-#endif
+                        for (int q = 0; q < nbox; ++q) tma_store_2d(&tmOut, stg + q * 4096, p0 + 128 * h + 64 * q, row0);
                         bulk_commit();
                     }
                 }
@@ -596,9 +580,6 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 // warp writes two rows per instruction with coalesced 16-byte global stores (LSU, not per-row
                 // bulk copies: those were 256 small TMA requests per tile competing with the A-tile loads).
                 uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
-#if SFFN_UNION_Y_EF
-                const uint64_t ypol = policy_evict_first();
-#endif
                 const int prow_l = row0 + lane;
                 const int64_t yrow_l = prow_l < args.M ? static_cast<int64_t>(__ldg(args.perm + prow_l)) : -1;
 #pragma unroll 1
@@ -625,11 +606,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                         const int64_t yrow = __shfl_sync(0xffffffffu, yrow_l, r);
                         const uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + chunk * 16);
                         if (yrow >= 0 && chunk * 8 < nc)
-#if SFFN_UNION_Y_EF
-                            st_global_v4_evict_first(args.Y + yrow * args.K + c0 + chunk * 8, val, ypol);
-#else
                             *reinterpret_cast<uint4*>(args.Y + yrow * args.K + c0 + chunk * 8) = val;
-#endif
                     }
                     __syncwarp();  // staging rows read before the next half overwrites them
                 }
