@@ -612,6 +612,8 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 }
                 if constexpr (FUSED) {
                     // this warp's 32 rows x 256 columns are in the local window: count them at the window's owner
+                    // (the owner reads them through the LSA mapping, a virtual alias of the address written here)
+                    asm volatile("fence.proxy.alias;" ::: "memory");
                     __threadfence_system();
                     __syncwarp();
                     if (lane == 0) {
