@@ -345,7 +345,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
             { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
             if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
         }
-        { union_rank_kernel<<<dim3(static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_SPLIT), PERM_W / PERM_SPLIT, 0,
+        { union_rank_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_THREADS, 0,
                             st>>>(rnnz, (int)M, perm, um.umask, NB * (N / 32), bctr, (int)NB + 1); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
         if (gated) {

@@ -429,42 +429,68 @@ __global__ void row_nnz_kernel(const uint32_t* __restrict__ tw, int M, int N, in
     if (lane == 0) nnz[gw] = s;
 }
 
-// pi by ranking (replaces a bitonic sort): row i of a window goes to position
-//   #{ j in window : nnz_j > nnz_i  or  (nnz_j == nnz_i and j < i) }
-// i.e. stable descending order of stored non-zeros.  Grid (windows, PERM_SPLIT); every CTA holds its window's
-// counts in SMEM (padding rows = -1, never counted) and ranks PERM_W / PERM_SPLIT rows (thread per row, four
-// keys per 16-byte SMEM read).  The grid also zeroes union_meta_kernel's merged masks and counters.
-constexpr int PERM_SPLIT = 16;
+// pi: stable descending order of stored non-zeros within each window, i.e. row i of a window goes to position
+//   #{ j in window : nnz_j > nnz_i  or  (nnz_j == nnz_i and j < i) }.
+// One CTA (PERM_THREADS) per window: the window's packed keys (nnz << 11) | (2047 - j) — unique, so the order is
+// total and deterministic — bitonic-sorted descending (66 compare-exchange stages; padding rows get -1 and sort
+// last), then perm[w0 + p] = w0 + (2047 - (key_p & 2047)).  (The former ranking kernel compared every row with
+// all 2048 keys: 4 M comparisons per window.)
+// The grid also zeroes union_meta_kernel's merged masks and counters.
+constexpr int PERM_THREADS = PERM_W / 2;
 static_assert(PERM_W == 2048, "rank keys pack the window index in 11 bits");
-__global__ void __launch_bounds__(PERM_W / PERM_SPLIT) union_rank_kernel(const int* __restrict__ nnz, int M,
-                                                                        int32_t* __restrict__ perm,
-                                                                        uint32_t* __restrict__ zero_a, int64_t na,
-                                                                        int* __restrict__ zero_b, int nb) {
+__global__ void __launch_bounds__(PERM_THREADS) union_rank_kernel(const int* __restrict__ nnz, int M,
+                                                                 int32_t* __restrict__ perm,
+                                                                 uint32_t* __restrict__ zero_a, int64_t na,
+                                                                 int* __restrict__ zero_b, int nb) {
     {  // zero union_meta_kernel's merged masks and counters (it runs after this kernel on the same stream)
-        const int64_t t = (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
-        const int64_t nt = static_cast<int64_t>(gridDim.x) * gridDim.y * blockDim.x;
+        const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
         for (int64_t i = t; i < na; i += nt) zero_a[i] = 0u;
         for (int64_t i = t; i < nb; i += nt) zero_b[i] = 0;
     }
-    // packed key (nnz << 11) | (2047 - j): key_j > key_i  <=>  nnz_j > nnz_i or (nnz_j == nnz_i and j < i)
-    // (stored non-zeros of a row <= N <= 65536 < 2^20); padding rows get -1 and are never counted
-    __shared__ __align__(16) int key[PERM_W];
+    // thread t holds the keys at positions t and t + 1024; a compare-exchange of positions p < q = p ^ j keeps the
+    // larger key at p in descending blocks ((p & k) == 0) and the smaller one otherwise.  Partners within a warp
+    // (j < 32) by shuffle, j = 1024 in registers, the rest through double-buffered SMEM (one barrier per stage).
+    __shared__ int key[2][PERM_W];
     const int w0 = blockIdx.x * PERM_W;
     const int rows = min(PERM_W, M - w0);
-    for (int i = threadIdx.x; i < PERM_W; i += blockDim.x)
-        key[i] = i < rows ? (__ldg(nnz + w0 + i) << 11) | (PERM_W - 1 - i) : -1;
-    __syncthreads();
-    const int i = blockIdx.y * (PERM_W / PERM_SPLIT) + threadIdx.x;
-    if (i >= rows) return;
-    const int ki = key[i];
-    int rank = 0;
-    const int4* k4 = reinterpret_cast<const int4*>(key);
-#pragma unroll 8
-    for (int j4 = 0; j4 < PERM_W / 4; ++j4) {
-        const int4 v = k4[j4];
-        rank += (v.x > ki) + (v.y > ki) + (v.z > ki) + (v.w > ki);
+    const int t = threadIdx.x;
+    int v[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const int i = t + s * PERM_THREADS;
+        v[s] = i < rows ? (__ldg(nnz + w0 + i) << 11) | (PERM_W - 1 - i) : -1;
     }
-    perm[w0 + rank] = w0 + i;
+    auto cx = [](int p, int j, int k, int mine, int other) {
+        const bool desc = (p & k) == 0, lower = (p & j) == 0;
+        return (desc == lower) ? max(mine, other) : min(mine, other);
+    };
+    int buf = 0;
+    for (int k = 2; k <= PERM_W; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == PERM_THREADS) {  // partner: the thread's other key
+                const int a = v[0], c = v[1];
+                v[0] = cx(t, j, k, a, c);
+                v[1] = cx(t + PERM_THREADS, j, k, c, a);
+            } else if (j >= 32) {
+                key[buf][t] = v[0];
+                key[buf][t + PERM_THREADS] = v[1];
+                __syncthreads();
+                const int o0 = key[buf][t ^ j], o1 = key[buf][(t + PERM_THREADS) ^ j];
+                v[0] = cx(t, j, k, v[0], o0);
+                v[1] = cx(t + PERM_THREADS, j, k, v[1], o1);
+                buf ^= 1;
+            } else {
+#pragma unroll
+                for (int s = 0; s < 2; ++s) v[s] = cx(t + s * PERM_THREADS, j, k, v[s], __shfl_xor_sync(0xffffffffu, v[s], j));
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const int p = t + s * PERM_THREADS;
+        if (p < rows) perm[w0 + p] = w0 + (PERM_W - 1 - (v[s] & (PERM_W - 1)));
+    }
 }
 
 // Xp[i, :] = X[perm[i], :]  (warp per row, 16-byte vectors)

@@ -626,6 +626,40 @@ def test_union_all_blocks_dense(sffn):
     assert " passed" in r.stdout
 
 
+def test_union_pi_order(sffn):
+    """The row order pi (descending stored non-zeros per 2048-row window, ties by row index) and the
+    128-row block unions built on it: the union sizes the library reports equal those computed here from the
+    packed TwELL with numpy's stable argsort — a wrong order would change them (Y would not notice: any
+    permutation gives the same Y)."""
+    cfg = synth.CONFIGS["1B"].replace(M=5000, K=256, N=2048, Kb=16, sparsity=0.995)
+    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    M, N, T, C = cfg.M, cfg.N, 256, 8
+    tw = sffn.pack(X, Wg, T, C)
+    ws = torch.empty(max(16, sffn.up_down_workspace_bytes(M, cfg.K, N, T, C, "union")), dtype=torch.uint8,
+                     device="cuda")
+    sffn.up_down(X, tw, Wu, Wd, T, C, workspace=ws, algo="union")
+    st = sffn.union_stats(ws, M, cfg.K, N)
+    w = words_np(tw).reshape(M, N // T, T // C)
+    cnt = np.minimum(w[:, :, 0], T // C - 1).astype(np.int64)  # (uint32 words: negate only as int64)
+    nnz = cnt.sum(axis=1)
+    order = []
+    for w0 in range(0, M, 2048):
+        idx = np.arange(w0, min(M, w0 + 2048))
+        order.extend(idx[np.argsort(-nnz[idx], kind="stable")])
+    units = [set() for _ in range(M)]
+    for m in range(M):
+        for t in range(N // T):
+            for e in range(cnt[m, t]):
+                units[m].add(int(w[m, t, 1 + e]) & 0xFFFF)
+    usum, dense = 0, 0
+    for b0 in range(0, M, 128):
+        u = set().union(*(units[m] for m in order[b0:b0 + 128]))
+        usum += len(u)
+        dense += len(u) >= 0.7 * N
+    assert dense == 0, "test shape meant to stay below the dense-block threshold"
+    assert st["union_sum"] == usum
+
+
 def test_gate_dynamic_scheduler(sffn, monkeypatch):
     """The gate GEMM's optional dynamic tile scheduler (SFFN_GATE_DYN=1: atomic claims published through a tile
     ring, both CTAs of a pair) gives the same TwELL and Y bit for bit as static striding, over repeated calls
