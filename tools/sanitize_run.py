@@ -33,3 +33,10 @@ if os.environ.get("SFFN_UNION_PAIR") != "1":  # NEXT-3 symmetric path on a 1-ran
     comm.close()
 torch.cuda.synchronize()
 print("sanitize run done")
+
+# the gate GEMM's optional dynamic tile scheduler (off by default)
+os.environ["SFFN_GATE_DYN"] = "1"
+sffn.forward(X, Wg, Wu, Wd, 256, 8, algo="union")
+torch.cuda.synchronize()
+os.environ["SFFN_GATE_DYN"] = "0"
+print("dyn scheduler done", flush=True)
