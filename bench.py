@@ -3,13 +3,18 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7B] [--impl ours|reference]
 
+--gpus N > 1 without a torchrun environment re-launches itself through torch.distributed.run (one process per GPU,
+rendezvous on 127.0.0.1); only rank 0 prints.
+
 A step = one pass of the whole hot path (pack: gate GEMM -> TwELL, then the fused sparse up/down; plus
 the NCCL all-reduce of partial outputs when N > 1) over one batch of M synthetic tokens, inputs and
 weights resident in HBM.  The L2 is flushed (a 512 MiB write) between timed steps; every step is timed
 with CUDA events on the launching stream; the reported time is the max over ranks.
 
-N > 1 (torchrun): hidden-dim sharding (north_star (5)) — rank r owns hidden units [r N/G, (r+1) N/G) of
-all three weights; every rank sees all M tokens; value = M / t (strong scaling: total work fixed).
+N > 1 (torchrun): hidden-dim sharding (north_star (5)) — rank r owns N/G hidden units of all three weights
+(contiguous rows, or TwELL tiles dealt round-robin with --shard-mode round_robin); every rank sees all M tokens;
+value = M / t, the whole job's tokens/s (strong scaling: total work fixed); tokens_per_s_per_gpu = value / N is the
+metric's per-GPU figure.
 
 --impl reference: the CPU oracle (oracle/, plain fp64 C) timed on this box's host cores, on a bounded
 row sample of the same workload per step (the only other place bench.py executes oracle/ besides the
@@ -48,6 +53,47 @@ def load_peaks():
     d = dict(PEAKS_FALLBACK)
     d["_source"] = "fallback (B200_PROFILING.md)"
     return d
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(argv, n: int) -> int:
+    """--gpus N > 1 outside torchrun: one process per GPU through torch.distributed.run, rendezvous on 127.0.0.1
+    (the driver's own launch form); rank 0's JSON line reaches our stdout, the exit code is propagated."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ, SFFN_BENCH_LAUNCHED="1")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def bench_config(cfg, args, world: int) -> dict:
+    """The `config` object of the JSON line — a function of the arguments only, so the reference arm and this arm
+    print identical objects for the same command line."""
+    replicas = world > 1 and args.shard == "tokens"
+    par = "single" if world == 1 else (f"token replicas x{world}" if replicas else
+                                       f"hidden-dim x{world} ({args.shard_mode})")
+    return {"workload": cfg.name, "M": cfg.M, "K": cfg.K, "N": cfg.N, "T": cfg.T, "C": cfg.C, "sparsity": cfg.sparsity,
+            "parallelism": par, "allreduce": "none" if world == 1 or replicas else args.allreduce,
+            "l2": "flushed (512 MiB write) between timed steps", "seed": cfg.seed,
+            "launch": "eager" if (args.no_graph or world > 1) else "cuda_graph"}
 
 
 # ----------------------------------------------------------------------------- clocks sampler
@@ -102,33 +148,65 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
-def time_oracle(cfg, rows: int, p=None):
-    """The oracle as it stands (pack_from_inputs + ffn_twell) on `rows` contiguous token rows."""
+def time_oracle(cfg, rows: int, p=None, kind: str = "sparse"):
+    """The oracle as it stands on `rows` contiguous token rows.  kind="sparse": its TwELL-based forward (fp64 gate
+    GEMM + Alg.1 pack + Eq.3 over the stored entries, SPEC's CPU criterion S:728); kind="dense": dense Eq.1 (fp64,
+    3 M K N MACs) + the explicit TwELL pack."""
     import oracle
     X = synth.gen_x(cfg, 0, rows, p=p)
     Wg, Wu, Wd = synth.gen_w(cfg, "g"), synth.gen_w(cfg, "u"), synth.gen_w(cfg, "d")
     t0 = time.perf_counter()
     words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
-    oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)
+    if kind == "sparse":
+        oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)
+    else:
+        oracle.ffn_dense(X, Wg, Wu, Wd)
     return time.perf_counter() - t0
 
 
-def oracle_sample_rows(cfg, target_s: float = 15.0):
-    """Rows of CPU work of about target_s seconds: calibrate on a few rows, then scale (rows are independent)."""
-    ncpu = os.cpu_count() or 1
+def oracle_threads() -> int:
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n and n.isdigit() else (os.cpu_count() or 1)
+
+
+def oracle_sample_rows(cfg, target_s: float = 15.0, kind: str = "sparse"):
+    """Rows of CPU work of about target_s seconds: calibrate on a few rows, then scale (rows are independent).
+    Rows are a multiple of the thread count (OpenMP over rows) so every core has work."""
+    ncpu = oracle_threads()
     r0 = max(1, min(ncpu, 8))
-    t = time_oracle(cfg, r0)
+    t = time_oracle(cfg, r0, kind=kind)
     rows = int(max(r0, min(cfg.M, r0 * target_s / max(t, 1e-3))))
     rows = max(r0, (rows // ncpu) * ncpu) if rows >= ncpu else rows
     return rows, t, r0
 
 
+def cpu_baseline_leg(cfg, p, target_s: float) -> dict:
+    """cpu_baseline: the oracle's sparse forward (the reported value) and its dense Eq.1 + pack,
+    each on a bounded contiguous row sample, on this box's host cores."""
+    ncpu = oracle_threads()
+    rows, _, _ = oracle_sample_rows(cfg, target_s=target_s)
+    t_o = time_oracle(cfg, rows, p)
+    rows_d, _, _ = oracle_sample_rows(cfg, target_s=target_s / 2, kind="dense")
+    t_d = time_oracle(cfg, rows_d, p, kind="dense")
+    return {"value": rows / t_o, "unit": "tokens/s", "cores": min(ncpu, rows), "kind": "oracle",
+            "cpu_model": cpu_model(), "omp_threads": ncpu,
+            "sample": f"{rows} contiguous token rows of {cfg.name} (M={cfg.M}): fp64 gate GEMM + Alg.1 pack + Eq.3 over "
+                      f"the stored entries ({t_o:.1f} s)",
+            "dense_eq1_pack": {"value": rows_d / t_d, "unit": "tokens/s", "cores": min(ncpu, rows_d),
+                               "sample": f"{rows_d} contiguous token rows: fp64 dense Eq.1 (3 M K N MACs) + the "
+                                         f"TwELL pack ({t_d:.1f} s)"}}
+
+
 def run_reference(args, cfg):
-    """--impl reference: the CPU oracle, each step a bounded row sample of the workload."""
+    """--impl reference: the CPU oracle, each step a bounded row sample of the workload (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    ncpu = os.cpu_count() or 1
+    if "LOCAL_RANK" in os.environ:
+        # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 is the only worker here, so it takes every host core
+        # (read by the oracle's OpenMP runtime when oracle/ is first loaded, below)
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+    ncpu = oracle_threads()
     p = synth.token_targets(cfg)
     # one step ~ a few seconds of oracle work so the whole run stays within minutes
     rows, t_cal, r_cal = oracle_sample_rows(cfg, target_s=max(1.0, 60.0 / max(1, args.steps + args.warmup)))
@@ -137,17 +215,84 @@ def run_reference(args, cfg):
     times = [time_oracle(cfg, rows, p) for _ in range(args.steps)]
     t = float(np.mean(times))
     val = rows / t
-    sample = f"{rows} contiguous token rows of {cfg.name} (M={cfg.M}) per step; fp64 gate GEMM + Alg.1 pack + Eq.3"
-    out = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "none",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded dyadic-grid generator)",
-           "config": {"workload": cfg.name, "M": cfg.M, "K": cfg.K, "N": cfg.N, "T": cfg.T, "C": cfg.C,
-                      "sparsity": cfg.sparsity},
-           "impl": "reference",
+    sample = (f"{rows} contiguous token rows of {cfg.name} (M={cfg.M}) per step; fp64 gate GEMM + Alg.1 pack + Eq.3 "
+              f"over the stored entries")
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    out = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "strong" if world > 1 and args.shard == "hidden" else "weak", "vs_baseline": None,
+           "dtype": "f64", "data": DATA, "config": bench_config(cfg, args, world), "impl": "reference",
            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": min(ncpu, rows), "kind": "oracle",
-                            "sample": sample},
+                            "sample": sample, "cpu_model": cpu_model(), "omp_threads": ncpu},
            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+DATA = ("synthetic (seeded dyadic-grid generator: 99% sparsity, lognormal per-token nnz, lognormal per-neuron "
+        "popularity, 30% dead neurons)")
+
+
+def run_dry(args, cfg):
+    """--dry-run (CPU, gloo): the multi-rank skeleton of this script without a GPU — rendezvous, this rank's hidden
+    shard, max-over-ranks of a per-rank number, rank 0 prints one JSON line.  tests/test_bench_launch.py runs it
+    through the self-launcher."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_23198_b200.sharding import shard_perm, shard_range
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    n0, Nl = shard_range(cfg.N, world, rank, cfg.T)
+    units = shard_perm(cfg.N, world, cfg.T, args.shard_mode)[n0:n0 + Nl]
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    u = torch.zeros(cfg.N, dtype=torch.int64)
+    u[torch.from_numpy(units)] = 1
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(u)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "t_max": float(t.item()),
+                          "units_covered_once": bool((u == 1).all()), "config": bench_config(cfg, args, world)}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ncu_step_traffic(config: str, algo: str, launches: int, timeout: int = 300):
+    """DRAM bytes of ONE forward of this build, measured now: ncu (dram__bytes_read/write.sum per kernel, caches
+    not flushed between the step's kernels) on tools/prof_run.py running two forwards of the same config; the last
+    `launches` kernels are the second forward.  Returns (per-kernel list, total bytes) or (None, reason)."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum", "--csv",
+           "--cache-control", "none", "--clock-control", "none", sys.executable,
+           os.path.join(ROOT, "tools", "prof_run.py"), "--config", config, "--iters", "2", "--fwd", "--algo", algo]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    except subprocess.TimeoutExpired:
+        return None, f"ncu timed out after {timeout} s"
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    if r.returncode != 0 or not lines:
+        return None, f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-200:]}"
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines))))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "us": 1e-6,
+             "usecond": 1e-6, "nsecond": 1e-9, "msecond": 1e-3, "ms": 1e-3, "second": 1.0}
+    kern = {}
+    for d in rows:
+        key = (int(d["ID"]), d["Kernel Name"])
+        v = float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1.0)
+        kern.setdefault(key, {})[d["Metric Name"]] = v
+    ks = sorted(kern.items())[-launches:]
+    out = [{"kernel": name.split("(")[0][:80], "dram_bytes": int(m.get("dram__bytes_read.sum", 0) +
+                                                               m.get("dram__bytes_write.sum", 0)),
+            "ncu_ms": m.get("gpu__time_duration.sum", 0.0) * 1e3} for (_, name), m in ks]
+    return out, sum(k["dram_bytes"] for k in out)
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -172,11 +317,20 @@ def main():
     ap.add_argument("--algo", default="auto", choices=["auto", "gather", "union"], help="fused up/down algorithm")
     ap.add_argument("--e2e-chunk", type=int, default=4096, help="rows per chunk of the host-buffer pipeline")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--shard-mode", choices=["contiguous", "round_robin"], default="contiguous",
+                    help="N>1 hidden sharding: contiguous row blocks, or TwELL tiles dealt round-robin (SURVEY 8(e))")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu pass that measures the step's DRAM bytes")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo skeleton of the multi-rank path (tests)")
     ap.add_argument("--json-out", default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = synth.CONFIGS[args.config]
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(sys.argv[1:], args.gpus))
+    if args.dry_run:
+        run_dry(args, cfg)
+        return
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -197,9 +351,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     M, K, N, T, C = cfg.M, cfg.K, cfg.N, cfg.T, cfg.C
-    from paper_2603_23198_b200.sharding import shard_range
+    from paper_2603_23198_b200.sharding import shard_perm, shard_range
     replicas = world > 1 and args.shard == "tokens"
     n0, Nl = (0, N) if replicas else shard_range(N, world, rank, T)
+    units = shard_perm(N, 1 if replicas else world, T, args.shard_mode)[n0:n0 + Nl]  # this rank's hidden units
 
     def to_dev(a):
         return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).to(dev)
@@ -207,7 +362,10 @@ def main():
     p = synth.token_targets(cfg)
     X_host = synth.gen_x(cfg, p=p)
     X = to_dev(X_host)
-    Wg, Wu, Wd = (to_dev(synth.gen_w(cfg, w, n0, Nl)) for w in "gud")
+    if args.shard_mode == "contiguous" or replicas:
+        Wg, Wu, Wd = (to_dev(synth.gen_w(cfg, w, n0, Nl)) for w in "gud")
+    else:  # round-robin tiles: the shard's weight rows gathered once, at load time
+        Wg, Wu, Wd = (to_dev(np.ascontiguousarray(synth.gen_w(cfg, w)[units])) for w in "gud")
     Y = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
     ws = torch.empty(sffn.workspace_bytes(M, K, Nl, T, C, args.algo), dtype=torch.uint8, device=dev)
     tw_view = sffn.twell_view(ws, M, Nl, C)
@@ -300,7 +458,17 @@ def main():
     t_pack = float(np.median(ms_pack)) / 1e3
     t_ud = float(np.median(ms_ud)) / 1e3
     twords = tw.cpu().numpy().view(np.uint32).reshape(M, Nl // T, T // C)
-    nnz_total = int(np.minimum(twords[:, :, 0], T // C - 1).sum())
+    tile_cnt = np.minimum(twords[:, :, 0], T // C - 1).astype(np.int64)
+    nnz_row = tile_cnt.sum(1)
+    nnz_total = int(nnz_row.sum())
+    # realized activation statistics of this run (SURVEY §8d-3 outputs): per-token nnz quantiles and the per-tile
+    # count histogram (counts 0..cap, plus overflowed tiles)
+    hist = np.bincount(np.minimum(twords[:, :, 0], T // C).astype(np.int64).ravel(), minlength=T // C + 1)
+    nnz_stats = {"mean": float(nnz_row.mean()), "p50": float(np.median(nnz_row)),
+                 "p99": float(np.percentile(nnz_row, 99)), "max": int(nnz_row.max()),
+                 "realized_sparsity": 1.0 - nnz_total / (M * Nl),
+                 "tile_count_hist": {"bins": f"count 0..{T // C - 1}, then >= {T // C} (overflow)",
+                                     "counts": [int(v) for v in hist]}}
     gate_flop = 2.0 * M * K * Nl
     ud_flop = 4.0 * K * nnz_total  # useful sparse work of Eq.3
     ud_compulsory = 2 * M * K + 4 * M * Nl // C + 2 * M * K + 4 * Nl * K  # x, TwELL, y, touched weights (<=)
@@ -312,21 +480,27 @@ def main():
                             "algorithmic": "2*M*K*N FLOP"},
     }
     algo_used = args.algo if args.algo != "auto" else ("union" if Nl % 64 == 0 else "gather")
+    # SURVEY §8d-4 floor of the fused up/down (K2'): the method's useful work 4 K nnz FLOP at the FP32-FMA peak vs
+    # its compulsory bytes at the HBM copy bandwidth; frac = floor / measured
+    t_floor_ud = max(ud_flop / (fma_peak * 1e12), ud_compulsory / (peaks["hbm_gbs"] * 1e9))
     if algo_used == "union":
         st = sffn.union_stats(ud_ws, M, K, Nl)
         br = st["block_rows"]
         tc_flop = 4.0 * br * st["padded_sum"] * K  # the two union GEMMs
         kernels["fused_up_down"] = {
-            "ms": t_ud * 1e3, "launches": ud_launches, "algo": "union", "bound": "tensor",
-            "achieved": tc_flop / t_ud / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": tc_flop / t_ud / 1e12 / peaks["bf16_tflops"],
-            "algorithmic": f"4*{br}*sum_b |U_b| * K FLOP (union GEMMs, {br}-row union blocks)",
-            "union_frac_of_N": st["union_sum"] / ((M + br - 1) // br) / Nl, "union_block_rows": br,
-            "useful_tflops": ud_flop / t_ud / 1e12}
+            "ms": t_ud * 1e3, "launches": ud_launches, "algo": "union", "bound": "alu",
+            "achieved": ud_flop / t_ud / 1e12, "peak": fma_peak, "unit": "TFLOP/s",
+            "frac": t_floor_ud / t_ud, "floor_ms": t_floor_ud * 1e3,
+            "algorithmic": "4*K*nnz FLOP (Eq.3 useful work), floor = max(FLOP / FP32-FMA peak, compulsory bytes / HBM)",
+            "tensor_padded": {"achieved": tc_flop / t_ud / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                              "frac": tc_flop / t_ud / 1e12 / peaks["bf16_tflops"],
+                              "work": f"4*{br}*sum_b |U_b| * K FLOP executed by the union GEMMs ({br}-row blocks)",
+                              "redundancy": tc_flop / max(ud_flop, 1.0)},
+            "union_frac_of_N": st["union_sum"] / ((M + br - 1) // br) / Nl, "union_block_rows": br}
     else:
         kernels["fused_up_down"] = {
             "ms": t_ud * 1e3, "launches": ud_launches, "algo": "gather", "bound": "alu", "achieved": ud_flop / t_ud / 1e12,
-            "peak": fma_peak, "unit": "TFLOP/s", "frac": ud_flop / t_ud / 1e12 / fma_peak,
+            "peak": fma_peak, "unit": "TFLOP/s", "frac": t_floor_ud / t_ud, "floor_ms": t_floor_ud * 1e3,
             "algorithmic": "4*K*nnz FLOP", "hbm_compulsory_gbs": ud_compulsory / t_ud / 1e9,
             "gathered_gbs": 4.0 * K * nnz_total / t_ud / 1e9}
     # the dominant single launch: the gate GEMM (the union up/down is several launches, none longer than it;
@@ -334,24 +508,21 @@ def main():
     dom = "gate_gemm_twell" if (algo_used == "union" or t_pack >= t_ud) else "fused_up_down"
     traffic = None
     hbm = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as f:
-                tr = json.load(f)
-            traffic = tr.get(args.config, {}).get(dom)
-            # the metric's "HBM %": DRAM bytes of the step's kernels (one ncu --set full capture of the same
-            # forward, tools/prof_step.sh) over the measured step time, against the measured copy bandwidth
-            step_k = (["gate_gemm_twell", "union_rank", "permute_rows", "union_meta", "union_gate_list",
-                       "union_up_gemm", "union_down_gemm"] if algo_used == "union" else [])
-            tk = tr.get(args.config, {})
-            if world == 1 and step_k and all(k in tk for k in step_k):
-                b = float(sum(tk[k] for k in step_k))
-                hbm = {"step_dram_bytes": b, "achieved_gbs": b / (ms_per_step / 1e3) / 1e9,
-                       "peak_gbs": peaks["hbm_gbs"], "frac": b / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],
-                       "source": "ncu dram__bytes_read+write per kernel (profiles/ncu_traffic.json) / bench step time"}
-        except (OSError, ValueError):
-            traffic = None
+    step_kernels = None
+    if rank == 0 and world == 1 and not args.no_ncu:
+        # the metric's "HBM %": DRAM bytes of one forward of THIS build, measured now by an ncu pass (only DRAM byte
+        # counters are taken from it, never a time), over the step time measured above
+        step_kernels, tot = ncu_step_traffic(args.config, args.algo, launches_per_step)
+        if step_kernels is None:
+            hbm = {"unavailable": tot}
+        else:
+            hbm = {"step_dram_bytes": tot, "achieved_gbs": tot / (ms_per_step / 1e3) / 1e9, "peak_gbs": peaks["hbm_gbs"],
+                   "frac": tot / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],
+                   "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one forward, measured in this run "
+                             "(--cache-control none), / the bench step time", "kernels": step_kernels}
+            gate = [k for k in step_kernels if "gemm_tc_kernel" in k["kernel"]]
+            if dom == "gate_gemm_twell" and gate:
+                traffic = gate[0]["dram_bytes"]
     kd = kernels[dom]
     roofline = {"bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"], "unit": kd["unit"],
                 "frac": kd["frac"], "traffic": traffic, "kernel": dom,
@@ -374,7 +545,16 @@ def main():
         t_d = float(np.median(ms_d)) / 1e3
         dense = {"ms_per_step": t_d * 1e3, "tokens_per_s": M / t_d, "tflops": 6.0 * M * K * Nl / t_d / 1e12,
                  "speedup_sparse_vs_dense": t_d / (ms_per_step / 1e3)}
-        del H, Yd, wdT
+        # sanity line for the denominator's quality: the same three GEMMs through torch.matmul
+        # (cuBLAS), H taken as given (no GLU epilogue)
+        G1 = torch.empty((M, Nl), dtype=torch.bfloat16, device=dev)
+        ms_t = timed(lambda: (torch.matmul(X, Wg.t(), out=G1), torch.matmul(X, Wu.t(), out=H),
+                              torch.matmul(H, Wd, out=Yd)), max(5, args.steps // 2), 3)
+        t_t = float(np.median(ms_t)) / 1e3
+        dense["torch_matmul"] = {"ms_per_step": t_t * 1e3, "tflops": 6.0 * M * K * Nl / t_t / 1e12,
+                                 "what": "torch.matmul (cuBLAS) X W_g^T, X W_u^T, H W_d: the dense FFN's three GEMMs "
+                                         "without the GLU epilogue"}
+        del H, Yd, wdT, G1
 
     # ------------------------------------------------------------------ end to end (host buffers)
     e2e = None
@@ -433,11 +613,7 @@ def main():
     # ------------------------------------------------------------------ CPU oracle baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows, _, _ = oracle_sample_rows(cfg, target_s=12.0)
-        t_o = time_oracle(cfg, rows, p)
-        cpu = {"value": rows / t_o, "unit": "tokens/s", "cores": min(os.cpu_count() or 1, rows), "kind": "oracle",
-               "sample": f"{rows} contiguous token rows of {cfg.name}: fp64 gate GEMM + Alg.1 pack + Eq.3 "
-                         f"({t_o:.1f} s)"}
+        cpu = cpu_baseline_leg(cfg, p, target_s=12.0)
 
     if comm is not None:
         comm.close()
@@ -445,15 +621,11 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                "scaling": "strong" if world > 1 and not replicas else "weak", "vs_baseline": None, "dtype": "bf16",
-               "data": "synthetic (seeded dyadic-grid generator: 99% sparsity, lognormal per-token nnz, "
-                       "30% dead neurons)",
-               "config": {"workload": cfg.name, "M": M, "K": K, "N": N, "T": T, "C": C, "sparsity": cfg.sparsity,
-                          "parallelism": (f"token replicas x{world}" if replicas else f"hidden-dim x{world}")
-                          if world > 1 else "single", "allreduce": allreduce,
-                          "l2": "flushed (512 MiB write) between timed steps", "seed": cfg.seed,
-                          "launch": "cuda_graph" if graph is not None else "eager"},
-               "tokens_per_s_per_gpu": value / world,
-               "roofline": roofline, "kernels": kernels, "nnz_per_token": nnz_total / M,
+               "data": DATA,
+               "config": bench_config(cfg, args, world),
+               "tokens_per_s_per_gpu": value / world, "allreduce_used": allreduce,
+               "launch_used": "cuda_graph" if graph is not None else "eager",
+               "roofline": roofline, "kernels": kernels, "nnz_per_token": nnz_total / M, "nnz": nnz_stats,
                "overflow_tiles": n_ov, "dense": dense, "e2e": e2e, "cpu_baseline": cpu,
                "hbm": hbm,
                "gpu_launches": args.steps * launches_per_step,

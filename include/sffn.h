@@ -301,8 +301,9 @@ int sffn_comm_size(const sffn_comm* comm);
 
 /*
  * sffn_sharded_forward — sffn_forward on the local shard, then one in-place NCCL all-reduce (sum)
- * of Y [M, K] bf16 on `stream`.  With n_chunks > 1 the M dimension is processed in chunks (multiples
- * of 128 rows) and the all-reduce of chunk i overlaps the compute of chunk i+1 (the library orders
+ * of Y [M, K] bf16 on `stream`.  With n_chunks > 1 (and M >= 4096) the M dimension is processed in chunks
+ * (multiples of the 2048-row pi windows, so the result is bit-identical to n_chunks = 1) and the
+ * all-reduce of chunk i overlaps the compute of chunk i+1 (the library orders
  * them with events on an internal communication stream; still no host synchronization).  The
  * workspace (>= sffn_forward_workspace_bytes(M, K, N_local, T, C, algo)) is reused chunk after chunk.
  */

@@ -81,6 +81,23 @@ def gate_preact(X, Wg) -> np.ndarray:
     return A
 
 
+def gate_preact_matmul(X, Wg, rows_per_call: int = 4096) -> np.ndarray:
+    """The same A = X W_g^T with the product taken by ONE library primitive (numpy's fp64 matmul) instead of the
+    k-ascending C loop — the allowed "library primitive as a step" for row samples too large for the loop (the
+    loop streams all of W_g once per row).  On dyadic-grid inputs every product and partial sum is exactly
+    representable (< 2^20 units of 2^-11), so the result equals gate_preact bit for bit whatever
+    the BLAS summation order; tests/test_oracle_pins.py pins that equality.  Off the grid it differs from
+    gate_preact by fp64 rounding only."""
+    X, Wg = _u16(X), _u16(Wg)
+    Wt = ((Wg.astype(np.uint32) << 16).view(np.float32).astype(np.float64)).T
+    M = X.shape[0]
+    A = np.empty((M, Wg.shape[0]), dtype=np.float64)
+    for r0 in range(0, M, rows_per_call):
+        x = (X[r0:r0 + rows_per_call].astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        np.matmul(x, Wt, out=A[r0:r0 + rows_per_call])
+    return A
+
+
 def pack(S, T: int, C: int):
     """Alg.1 lines 7-17 packed as P:869 on fp32 S [M,N] -> (words uint32 [M,N/C], counts [M,N/T], n_overflow).
     Slots beyond each block's count are zero-initialised here (unspecified in the format)."""
@@ -129,9 +146,10 @@ def ffn_twell(X, words, Wu, Wd, N: int, T: int, C: int, A=None) -> np.ndarray:
     return Y
 
 
-def pack_from_inputs(X, Wg, T: int, C: int):
-    """The oracle's TwELL for relu(X W_g^T): fp64 pre-activation -> fp32 (exact on grid inputs) -> Alg.1."""
-    A = gate_preact(X, Wg)
+def pack_from_inputs(X, Wg, T: int, C: int, matmul: bool = False):
+    """The oracle's TwELL for relu(X W_g^T): fp64 pre-activation -> fp32 (exact on grid inputs) -> Alg.1.
+    matmul=True takes the pre-activation from gate_preact_matmul (bit-identical on grid inputs)."""
+    A = gate_preact_matmul(X, Wg) if matmul else gate_preact(X, Wg)
     words, counts, ov = pack(A.astype(np.float32), T, C)
     return words, counts, ov, A
 

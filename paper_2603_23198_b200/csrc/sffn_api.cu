@@ -709,9 +709,12 @@ int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int6
     int r = check_device();
     if (r != SFFN_OK) return r;
     if (M == 0) return SFFN_OK;
+    // the same mainloop as the pack (CTA pairs unless SFFN_GATE_PAIR=0): verifies the production accumulators
+    static const bool pair = env_flag("SFFN_GATE_PAIR", true);
     CUtensorMap ta, tb;
     if (!tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, GEMM_BN, CU_TENSOR_MAP_SWIZZLE_128B))
+        !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, pair ? GEMM_BN / 2 : GEMM_BN,
+                 CU_TENSOR_MAP_SWIZZLE_128B))
         return SFFN_ERR_CUDA;
     GemmArgs args{};
     args.M = (int)M;
@@ -719,7 +722,8 @@ int sffn_gate_gemm_f32(const void* X, const void* Wg, int64_t M, int64_t K, int6
     args.K = (int)K;
     args.out_f32 = Sout;
     args.ld_out = N;
-    return launch_gemm<EPI_F32, 1>(ta, tb, tb, tb, args, GEMM_BN, S(stream));
+    return pair ? launch_gemm<EPI_F32, 1, 2>(ta, tb, tb, tb, args, GEMM_BN, S(stream))
+                : launch_gemm<EPI_F32, 1>(ta, tb, tb, tb, args, GEMM_BN, S(stream));
 }
 
 // ---------------------------------------------------------------- fp32 mode (R19)

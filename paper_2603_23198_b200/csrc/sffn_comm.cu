@@ -395,16 +395,17 @@ int sffn_sharded_forward(sffn_comm* c, const void* X, const void* Wg_s, const vo
     if (M < 0) return SFFN_ERR_SHAPE;
     if (ws_bytes < sffn_forward_workspace_bytes(M, K, N_local, T, C, algo)) return SFFN_ERR_SHAPE;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (n_chunks == 1 || M < 2 * 128) {
+    if (n_chunks == 1 || M < 2 * 2048) {
         int r = sffn_forward(X, Wg_s, Wu_s, Wd_s, M, K, N_local, T, C, Y, workspace, ws_bytes, d_overflow, algo,
                              stream);
         if (r != SFFN_OK) return r;
         return sffn_allreduce_bf16(c, Y, M * K, stream);
     }
     if (ensure_events(c, n_chunks) != SFFN_OK) return SFFN_ERR_CUDA;
-    // chunk rows rounded to the GEMM row tile (128) so every chunk but the last is full
+    // chunk rows rounded to the 2048-row pi windows (P:1078 order per window, reading R21/R24): every chunk starts
+    // on a window boundary, so the chunks build exactly the windows and union blocks of one unchunked call
     int64_t rows = (M + n_chunks - 1) / n_chunks;
-    rows = (rows + 127) / 128 * 128;
+    rows = (rows + 2047) / 2048 * 2048;
     const char* x = static_cast<const char*>(X);
     char* y = static_cast<char*>(Y);
     // the comm stream must not start before earlier work on `stream` that touched Y

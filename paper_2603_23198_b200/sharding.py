@@ -14,6 +14,22 @@ def shard_range(N: int, world: int, rank: int, T: int) -> tuple[int, int]:
     return rank * Nl, Nl
 
 
+def shard_perm(N: int, world: int, T: int, mode: str = "contiguous"):
+    """Hidden-unit order of the G shards: rank r owns units perm[r N/G : (r+1) N/G] (its weight rows, in this order;
+    its TwELL indices are local positions in that slice).  "contiguous": the identity.  "round_robin": TwELL tiles of
+    T units dealt to ranks in turn (tile t -> rank t mod G, SURVEY §8e load balance: hot and dead neurons cluster
+    in contiguous blocks less), each rank keeping its tiles in ascending order.  Any such order is a consistent
+    permutation of hidden units, so sum_r Y_r is unchanged (Eq.1 is a sum over n).  Applied once, at load time."""
+    import numpy as np
+    shard_range(N, world, 0, T)  # validates N % (world * T)
+    if mode == "contiguous":
+        return np.arange(N, dtype=np.int64)
+    if mode != "round_robin":
+        raise ValueError(f"unknown shard mode {mode!r}")
+    tiles = np.arange(N // T).reshape(-1, world).T  # [world, tiles per rank]: rank r gets tiles r, r+G, ...
+    return (tiles[:, :, None] * T + np.arange(T)[None, None, :]).reshape(-1).astype(np.int64)
+
+
 def broadcast_id(id_bytes: bytes | None, rank: int, world: int, group=None) -> bytes:
     """Rank 0's 128-byte id to every rank through torch.distributed (any backend)."""
     if world == 1:

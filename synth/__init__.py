@@ -164,6 +164,12 @@ def neuron_params(cfg: Config):
     return b, d
 
 
+def q_bits(q: int, e: int) -> np.uint16:
+    """bf16 bits of the grid value q * 2^-e (|q| < 16: exact)."""
+    assert abs(q) < 16
+    return np.uint16(np.array([q * 2.0 ** -e], dtype=np.float32).view(np.uint32)[0] >> 16)
+
+
 def bf16_to_f32(a: np.ndarray) -> np.ndarray:
     """Exact widening of bf16 bit patterns (uint16) to float32."""
     return (a.astype(np.uint32) << 16).view(np.float32)

@@ -7,8 +7,11 @@ import sys
 sys.path[:0] = [os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__))]
 import torch  # noqa: E402
 
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
 import synth  # noqa: E402
-from gpu_util import to_dev  # noqa: E402
+from gpu_util import assert_y, to_dev  # noqa: E402
 
 
 def main():
@@ -20,15 +23,18 @@ def main():
         if not comm.symmetric_init(8192, cfg.K):
             print("SKIP symmetric windows unsupported")
             return
-        X, Wg, Wu, Wd = (to_dev(a) for a in (synth.gen_x(cfg), synth.gen_w(cfg, "g"), synth.gen_w(cfg, "u"),
-                                             synth.gen_w(cfg, "d")))
+        Xn, Wgn, Wun, Wdn = synth.gen_x(cfg), synth.gen_w(cfg, "g"), synth.gen_w(cfg, "u"), synth.gen_w(cfg, "d")
+        X, Wg, Wu, Wd = (to_dev(a) for a in (Xn, Wgn, Wun, Wdn))
         ref = sffn.forward(X, Wg, Wu, Wd, 256, 8, algo="union")
+        words, counts, n_ov, A = oracle.pack_from_inputs(Xn, Wgn, 256, 8)
+        Y3 = oracle.ffn_twell(Xn, words, Wun, Wdn, cfg.N, 256, 8)
         print("ref done", flush=True)
         for it in range(3):  # the counters are never reset: each call raises the targets by one epoch
             Y = comm.sharded_forward_fused(X, Wg, Wu, Wd, 256, 8)
             torch.cuda.synchronize()
             print("call", it, "max diff", (Y.float() - ref.float()).abs().max().item(), flush=True)
             assert torch.equal(Y.view(torch.int16), ref.view(torch.int16)), f"call {it}"
+            assert_y(Y.float().cpu().numpy().astype(np.float64), Y3)  # the oracle of the (1-rank) problem
         # a smaller M on the same window (one partial window), then the large one again
         for rows in (1000, 4500, 1):
             ref_r = sffn.forward(X[:rows].contiguous(), Wg, Wu, Wd, 256, 8, algo="union")

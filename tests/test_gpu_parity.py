@@ -12,7 +12,7 @@ import torch
 
 import oracle
 import synth
-from gpu_util import bf16_np, rel_fro, to_dev, twell_invariants, words_np
+from gpu_util import assert_y, bf16_np, rel_fro, to_dev, twell_invariants, words_np
 
 pytestmark = pytest.mark.gpu
 
@@ -37,16 +37,26 @@ def inputs(cfg, rows=None):
 
 
 # ----------------------------------------------------------------- mainloop exactness
-@pytest.mark.parametrize("M,K,N", [(128, 64, 256), (300, 256, 512), (1, 128, 256), (257, 2048, 768), (130, 4096, 272)])
+@pytest.mark.parametrize("M,K,N", [(128, 64, 256), (300, 256, 512), (1, 128, 256), (257, 2048, 768), (130, 4096, 272),
+                                   (384, 4096, 14336), (256, 8192, 28672), (300, 8192, 3584)])
 def test_gate_gemm_exact(sffn, M, K, N):
-    """tcgen05 fp32 accumulators == the oracle's fp64 pre-activation, bitwise, on grid inputs
-    (ragged M, N not a multiple of the 256 tile, K from 64 to 4096)."""
-    cfg = synth.CONFIGS["1B"].replace(M=M, K=K, N=N, Kb=min(64, K // 4))
-    X, Wg = synth.gen_x(cfg), synth.gen_w(cfg, "g")
+    """tcgen05 fp32 accumulators of the production mainloop (CTA pairs, cta_group::2, as the pack runs it) == the
+    oracle's fp64 pre-activation, bitwise, on grid inputs: ragged M, N not a multiple of the 256 tile, K from 64 to
+    8192, the 7B and 70B hidden sizes (N = 14336, 28672 and the 8-way shard 3584).  Row 0 / weight row 0 are set to
+    the worst-case grid magnitudes (|q_x| = 14, |q_w| = 7 on every k: 14*7*K units, 802,816 at K = 8192 < 2^20),
+    the largest partial sums the generator can produce."""
+    name = "70B" if K == 8192 else "1B"
+    cfg = synth.CONFIGS[name].replace(M=M, K=K, N=N, Kb=min(64, K // 4))
+    X, Wg = synth.gen_x(cfg).copy(), synth.gen_w(cfg, "g").copy()
+    X[0, :] = synth.q_bits(14, cfg.x_exp)
+    Wg[0, :] = synth.q_bits(7, cfg.w_exp)
     S = sffn.gate_gemm_f32(to_dev(X), to_dev(Wg))
     torch.cuda.synchronize()
-    A = oracle.gate_preact(X, Wg)
-    assert np.array_equal(S.cpu().numpy().astype(np.float64), A)
+    A = oracle.gate_preact_matmul(X, Wg) if M * K * N > 2e9 else oracle.gate_preact(X, Wg)
+    assert A[0, 0] == 14 * 7 * K * 2.0 ** -(cfg.x_exp + cfg.w_exp)
+    s = S.cpu().numpy().astype(np.float64)
+    bad = np.argwhere(s != A)
+    assert len(bad) == 0, f"{len(bad)} accumulators differ, first {bad[:4].tolist()}"
 
 
 # ----------------------------------------------------------------- pack (Alg.1 epilogue)
@@ -147,7 +157,7 @@ def test_up_down_vs_oracle(sffn, K, algo):
     tw = torch.from_numpy(wo.view(np.int32)).cuda()
     Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo)
     Yref = oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)
-    assert rel_fro(bf16_np(Y), Yref) < Y_TOL
+    assert_y(bf16_np(Y), Yref)
 
 
 @pytest.mark.parametrize("T,C", [(32, 2), (64, 4), (128, 2), (256, 4), (256, 16)])
@@ -158,7 +168,7 @@ def test_up_down_union_tiles(sffn, T, C):
     wo, counts, ov, A = oracle.pack_from_inputs(X, Wg, T, C)
     tw = torch.from_numpy(wo.view(np.int32)).cuda()
     Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), T, C, algo="union")
-    assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, T, C)) < Y_TOL
+    assert_y(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, T, C))
 
 
 def test_up_down_union_dense_rows(sffn):
@@ -177,7 +187,7 @@ def test_up_down_union_dense_rows(sffn):
     for algo in ALGOS:
         Y = sffn.up_down(to_dev(X), tw, to_dev(Wu), to_dev(Wd), 256, 1, algo=algo)
         Yref = oracle.ffn_twell(X, tw1, Wu, Wd, cfg.N, 256, 1)
-        assert rel_fro(bf16_np(Y[:1]), Yref[:1]) < Y_TOL
+        assert_y(bf16_np(Y[:1]), Yref[:1])
         assert not torch.any(Y[1:].float() != 0)
 
 
@@ -195,8 +205,8 @@ def test_forward_vs_oracle(sffn, name, M, algo):
     Y3 = oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)      # Eq.3 with stored h_v
     Y1 = oracle.ffn_dense(X, Wg, Wu, Wd)                           # Eq.1
     y = bf16_np(Y)
-    assert rel_fro(y, Y3) < Y_TOL
-    assert rel_fro(y, Y1) < Y_TOL
+    assert_y(y, Y3)
+    assert_y(y, Y1)
 
 
 def test_forward_empty_pattern_is_zero(sffn):
@@ -232,7 +242,7 @@ def test_forward_single_active_neuron(sffn):
     for algo in ALGOS:
         Y = sffn.up_down(to_dev(Xn), torch.from_numpy(tw.view(np.int32)).cuda(), to_dev(Wu), to_dev(Wd), 256, 8,
                          algo=algo)
-        assert rel_fro(bf16_np(Y), Yref) < 4e-3
+        assert_y(bf16_np(Y), Yref, 4e-3)
 
 
 def test_forward_ragged_and_tiny_M(sffn):
@@ -242,7 +252,7 @@ def test_forward_ragged_and_tiny_M(sffn):
         wo, _, _, _ = oracle.pack_from_inputs(X, Wg, 256, 8)
         for algo in ALGOS:
             Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo)
-            assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8)) < Y_TOL
+            assert_y(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8))
 
 
 # ----------------------------------------------------------------- dense baseline
@@ -256,7 +266,7 @@ def test_dense_forward_vs_oracle(sffn, name, M):
     assert torch.equal(wdT.cpu(), to_dev(Wd).cpu().t().contiguous())
     Y = sffn.dense_forward(to_dev(X), to_dev(Wg), to_dev(Wu), wdT)
     Y1 = oracle.ffn_dense(X, Wg, Wu, Wd)
-    assert rel_fro(bf16_np(Y), Y1) < Y_TOL
+    assert_y(bf16_np(Y), Y1)
 
 
 def test_errors_do_not_launch(sffn):
@@ -278,23 +288,34 @@ def test_sharded_forward_single_rank(sffn, algo):
     """sffn_sharded_forward on a 1-rank communicator: chunked (compute/all-reduce overlap on the comm
     stream) and unchunked results are bit-identical to sffn_forward; hidden shards summed on the host
     reproduce the unsharded output within tolerance (linearity, north_star (5))."""
-    cfg = synth.CONFIGS["1B"].replace(M=700, K=512, N=2048, Kb=32, sparsity=0.97)
-    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    cfg = synth.CONFIGS["1B"].replace(M=5000, K=512, N=2048, Kb=32, sparsity=0.97)
+    Xn, Wgn, Wun, Wdn = inputs(cfg)
+    X, Wg, Wu, Wd = (to_dev(a) for a in (Xn, Wgn, Wun, Wdn))
+    words, counts, n_ov, A = oracle.pack_from_inputs(Xn, Wgn, 256, 8)
+    Y3 = oracle.ffn_twell(Xn, words, Wun, Wdn, cfg.N, 256, 8)  # Eq.3 of the UNSHARDED problem
     ref = sffn.forward(X, Wg, Wu, Wd, 256, 8, algo=algo)
+    assert_y(bf16_np(ref), Y3)
     comm = sffn.Comm(0, 1, torch.cuda.current_device())
     try:
-        for chunks in (1, 3):
+        for chunks in (1, 3):  # 3 chunks: boundaries on the 2048-row pi windows -> bit-identical to one call
             Y = comm.sharded_forward(X, Wg, Wu, Wd, 256, 8, algo=algo, n_chunks=chunks)
             torch.cuda.synchronize()
             assert torch.equal(Y.view(torch.int16), ref.view(torch.int16))
+            assert_y(bf16_np(Y), Y3)
     finally:
         comm.close()
-    from paper_2603_23198_b200.sharding import shard_range
-    parts = torch.zeros(ref.shape, dtype=torch.float32, device="cuda")
-    for r in range(4):
-        n0, Nl = shard_range(cfg.N, 4, r, 256)
-        parts += sffn.forward(X, Wg[n0:n0 + Nl], Wu[n0:n0 + Nl], Wd[n0:n0 + Nl], 256, 8, algo=algo).float()
-    assert rel_fro(parts.cpu().numpy().astype(np.float64), bf16_np(ref)) < Y_TOL
+    from paper_2603_23198_b200.sharding import shard_perm, shard_range
+    # G = 4 hidden shards, contiguous and round-robin-tile (SURVEY §8e load balance), summed in fp32: the reduced Y
+    # equals the unsharded oracle within the bar
+    for mode in ("contiguous", "round_robin"):
+        perm = shard_perm(cfg.N, 4, 256, mode)
+        parts = torch.zeros(ref.shape, dtype=torch.float32, device="cuda")
+        for r in range(4):
+            n0, Nl = shard_range(cfg.N, 4, r, 256)
+            idx = torch.from_numpy(perm[n0:n0 + Nl]).cuda()
+            parts += sffn.forward(X, Wg[idx].contiguous(), Wu[idx].contiguous(), Wd[idx].contiguous(), 256, 8,
+                                  algo=algo).float()
+        assert_y(parts.cpu().numpy().astype(np.float64), Y3)
 
 
 @pytest.mark.parametrize("algo", ALGOS)
@@ -304,8 +325,11 @@ def test_sharded_forward_symmetric_single_rank(sffn, algo):
     barriers, P2P path — NVLS needs >= 2 ranks) and the copy-out: bit-identical to sffn_forward; the
     stand-alone reduction of a random buffer is the identity at G = 1; M above the window is refused."""
     cfg = synth.CONFIGS["1B"].replace(M=700, K=512, N=2048, Kb=32, sparsity=0.97)
-    X, Wg, Wu, Wd = (to_dev(a) for a in inputs(cfg))
+    Xn, Wgn, Wun, Wdn = inputs(cfg)
+    X, Wg, Wu, Wd = (to_dev(a) for a in (Xn, Wgn, Wun, Wdn))
+    words, counts, n_ov, A = oracle.pack_from_inputs(Xn, Wgn, 256, 8)
     ref = sffn.forward(X, Wg, Wu, Wd, 256, 8, algo=algo)
+    assert_y(bf16_np(ref), oracle.ffn_twell(Xn, words, Wun, Wdn, cfg.N, 256, 8))
     comm = sffn.Comm(0, 1, torch.cuda.current_device())
     try:
         if not comm.symmetric_init(1024, cfg.K):
@@ -347,17 +371,19 @@ def test_sharded_forward_fused_single_rank(sffn):
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_fused_allreduce_emulated(sffn, G):
-    """NEXT-3 fused all-reduce with G emulated ranks on one GPU (no NCCL): G windows, G hidden shards, the G fused
-    DOWN kernels co-resident on 1/G of the SMs each — counters at the window owners, cross-window P2P reduction:
-    every window == bf16(sum of the G partial outputs), counters == 4 x tiles x G at the owner, 0 elsewhere."""
+@pytest.mark.parametrize("G,mode", [(2, "contiguous"), (4, "contiguous"), (4, "round_robin")])
+def test_fused_allreduce_emulated(sffn, G, mode):
+    """NEXT-3 fused all-reduce with G emulated ranks on one GPU (no NCCL): G windows, G hidden shards (contiguous or
+    round-robin tiles), the G fused DOWN kernels co-resident on 1/G of the SMs each — counters at the window owners,
+    cross-window P2P reduction: every window == bf16(sum of the G partial outputs), counters == 4 x tiles x G at the
+    owner, 0 elsewhere, the reduced Y within the per-row bar of the UNSHARDED oracle (Eq.3 and Eq.1); run twice so
+    both counter sets are used."""
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.dirname(here), here, os.environ.get("PYTHONPATH", "")]))
     try:
-        out = subprocess.run([sys.executable, os.path.join(here, "fused_emul_case.py"), str(G)], capture_output=True,
+        out = subprocess.run([sys.executable, os.path.join(here, "fused_emul_case.py"), str(G), mode], capture_output=True,
                              text=True, timeout=240, env=env)
     except subprocess.TimeoutExpired:
         pytest.fail("emulated fused all-reduce did not finish within 240 s")
@@ -393,7 +419,7 @@ def test_fp32_forward_grid(sffn, name, M):
     t = lambda a: torch.from_numpy(a).cuda()
     Y = sffn.forward_f32(t(X), t(Wg), t(Wu), t(Wd), cfg.T, cfg.C)
     Y1 = oracle.ffn_dense_f32(X, Wg, Wu, Wd)
-    assert rel_fro(Y.cpu().numpy().astype(np.float64), Y1) < F32_TOL
+    assert_y(Y.cpu().numpy().astype(np.float64), Y1, F32_TOL)
 
 
 def test_fp32_forward_gaussian(sffn):
@@ -408,7 +434,7 @@ def test_fp32_forward_gaussian(sffn):
     t = lambda a: torch.from_numpy(a).cuda()
     Y = sffn.forward_f32(t(X), t(Wg), t(Wu), t(Wd), T, C)
     Y1 = oracle.ffn_dense_f32(X, Wg, Wu, Wd)
-    assert rel_fro(Y.cpu().numpy().astype(np.float64), Y1) < F32_TOL
+    assert_y(Y.cpu().numpy().astype(np.float64), Y1, F32_TOL)
 
 
 @pytest.mark.parametrize("algo", ALGOS)
@@ -440,8 +466,8 @@ def test_nongated_forward(sffn, name, M, algo):
     Y = sffn.forward_nongated(to_dev(X), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo)
     words, counts, ov, A = oracle.pack_from_inputs(X, Wu, cfg.T, cfg.C)
     y = bf16_np(Y)
-    assert rel_fro(y, oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C)) < Y_TOL
-    assert rel_fro(y, oracle.ffn_nongated_dense(X, Wu, Wd)) < Y_TOL
+    assert_y(y, oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C))
+    assert_y(y, oracle.ffn_nongated_dense(X, Wu, Wd))
 
 
 @pytest.mark.parametrize("algo", ALGOS)
@@ -452,48 +478,135 @@ def test_down_from_oracle_twell(sffn, algo):
     words, counts, ov, A = oracle.pack_from_inputs(X, Wu, cfg.T, cfg.C)
     tw = torch.from_numpy(words.view(np.int32)).cuda()
     Y = sffn.down(tw, to_dev(Wd), cfg.K, cfg.T, cfg.C, algo=algo)
-    assert rel_fro(bf16_np(Y), oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C)) < Y_TOL
+    assert_y(bf16_np(Y), oracle.down_twell(words, Wd, cfg.K, cfg.N, cfg.T, cfg.C))
 
 
 # ----------------------------------------------------------------- full-size parity (bench launch configuration)
-def _sample_rows(M, n_random=48, seed=0):
+def survey_rows(cfg, p, n_random=2048, seed=0):
+    """SURVEY §8c-5 row set for the 7B / 70B configs: first 128, last 128, 2048 seeded-random rows and the 64 rows
+    with the highest generator-predicted density (synth.token_targets)."""
+    M = cfg.M
     rng = np.random.default_rng(seed)
-    return np.unique(np.concatenate([np.arange(16), np.arange(M - 16, M), rng.choice(M, n_random, replace=False)]))
+    densest = np.argsort(-p, kind="stable")[:64]
+    rows = np.unique(np.concatenate([np.arange(128), np.arange(M - 128, M), rng.choice(M, n_random, replace=False),
+                                     densest]))
+    return rows, densest
 
 
-@pytest.mark.slow
-def test_7b_full_size_sampled(sffn):
-    """BASELINE configs[2] at full size (M=32768, K=4096, N=14336), the default (union) algorithm exactly as
-    bench.py launches it: TwELL bit-exact and Y within 1e-2 on sampled rows (first/last 16 + 48 random),
-    structural TwELL invariants on all rows, zero overflow."""
-    cfg = synth.CONFIGS["7B"]
+def _full_size_case(sffn, cfg, rows_fn):
+    """The default (union) forward exactly as bench.py launches it (one workspace, CTA-pair gate GEMM), at the
+    config's full size: TwELL bit-exact vs the oracle on the compared rows, structural invariants on ALL rows,
+    overflow count consistent with the counts, Y per-row within 1e-2 of Eq.3 on the compared rows."""
     p = synth.token_targets(cfg)
     X = synth.gen_x(cfg, p=p)
     Wg, Wu, Wd = (synth.gen_w(cfg, w) for w in "gud")
     ws = torch.empty(sffn.workspace_bytes(cfg.M, cfg.K, cfg.N, cfg.T, cfg.C), dtype=torch.uint8, device="cuda")
     ov = torch.zeros(1, dtype=torch.int32, device="cuda")
-    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, workspace=ws, overflow=ov)
-    assert sffn.overflow_check(ov) == 0
+    Xd, Wgd, Wud, Wdd = to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd)
+    Y = sffn.forward(Xd, Wgd, Wud, Wdd, cfg.T, cfg.C, workspace=ws, overflow=ov)
+    n_ov = sffn.overflow_check(ov)
     tw = words_np(sffn.twell_view(ws, cfg.M, cfg.N, cfg.C))
     twell_invariants(tw, cfg.N, cfg.T, cfg.C)
-    rows = _sample_rows(cfg.M)
-    wo, counts, n_ov, A = oracle.pack_from_inputs(X[rows], Wg, cfg.T, cfg.C)
-    assert oracle.valid_prefix_equal(tw[rows], wo, cfg.T, cfg.C).all()
+    cnt = tw.reshape(cfg.M, cfg.N // cfg.T, cfg.T // cfg.C)[:, :, 0]
+    assert n_ov == int((cnt > cfg.T // cfg.C - 1).sum())
+    rows, densest = rows_fn(cfg, p)
+    wo, counts, n_ov_ref, A = oracle.pack_from_inputs(X[rows], Wg, cfg.T, cfg.C, matmul=True)
+    eq = oracle.valid_prefix_equal(tw[rows], wo, cfg.T, cfg.C)
+    assert eq.all(), f"{int((~eq).sum())} (row, tile) blocks differ; first rows {rows[np.flatnonzero(~eq.all(1))[:5]]}"
+    # the densest rows really are the dense ones (the row set covers the tail of the per-token nnz distribution)
+    nnz = np.minimum(cnt, cfg.T // cfg.C - 1).sum(1)
+    print(f"[{cfg.name}] rows compared {len(rows)}; nnz/token mean {nnz.mean():.1f} p50 {np.median(nnz):.0f} "
+          f"p99 {np.percentile(nnz, 99):.0f} max {nnz.max()}; densest-64 mean {nnz[densest].mean():.1f}")
+    assert nnz[densest].mean() > 2 * nnz.mean()
     Yref = oracle.ffn_twell(X[rows], wo, Wu, Wd, cfg.N, cfg.T, cfg.C)
-    assert rel_fro(bf16_np(Y)[rows], Yref) < Y_TOL
+    Ys = Y.index_select(0, torch.from_numpy(rows).cuda())
+    assert_y(bf16_np(Ys), Yref, rows=rows)
+
+
+@pytest.mark.slow
+def test_7b_full_size_sampled(sffn):
+    """BASELINE configs[2] at full size (M=32768, K=4096, N=14336), SURVEY §8c-5 row set (2368 rows)."""
+    _full_size_case(sffn, synth.CONFIGS["7B"], survey_rows)
+
+
+@pytest.mark.slow
+def test_70b_full_size_sampled(sffn):
+    """BASELINE configs[4] at full size on one GPU (M=65536, K=8192, N=28672: the G=1 point of the sharding sweep),
+    SURVEY §8c-5 row set; K=8192 is the worst-case grid sum (860,160 units < 2^20)."""
+    _full_size_case(sffn, synth.CONFIGS["70B"], survey_rows)
+
+
+@pytest.mark.slow
+def test_1b_full_all_rows(sffn):
+    """BASELINE configs[1] (M=16384, K=2048, N=8192, heavy-tailed per-token nnz) compared on ALL rows:
+    every TwELL block bit-exact and every row's Y within 1e-2 of Eq.3."""
+    _full_size_case(sffn, synth.CONFIGS["1B"], lambda cfg, p: (np.arange(cfg.M), np.argsort(-p, kind="stable")[:64]))
 
 
 @pytest.mark.parametrize("algo", ALGOS)
 def test_70b_shapes(sffn, algo):
     """BASELINE configs[4] shapes (K=8192, N=28672 = one GPU's full hidden dim; N=3584 = an 8-way shard) at
-    a reduced M."""
+    a reduced M: TwELL of every row bit-exact, Y per row within 1e-2 of Eq.3."""
     for N in (28672, 3584):
         cfg = synth.CONFIGS["70B"].replace(M=256, N=N)
         X, Wg, Wu, Wd = inputs(cfg)
-        Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo)
-        rows = np.arange(0, 256, 8)
-        wo, counts, n_ov, A = oracle.pack_from_inputs(X[rows], Wg, cfg.T, cfg.C)
-        assert rel_fro(bf16_np(Y)[rows], oracle.ffn_twell(X[rows], wo, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
+        ws = torch.empty(sffn.workspace_bytes(cfg.M, cfg.K, cfg.N, cfg.T, cfg.C, algo), dtype=torch.uint8,
+                         device="cuda")
+        Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo, workspace=ws)
+        wo, counts, n_ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C, matmul=True)
+        assert oracle.valid_prefix_equal(words_np(sffn.twell_view(ws, cfg.M, cfg.N, cfg.C)), wo, cfg.T, cfg.C).all()
+        assert_y(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C))
+
+
+# ----------------------------------------------------------------- continuous (off-grid) mode, SURVEY §8c-3
+def _fp32_sum_bound(X, W):
+    """Worst-case |fp32 sum - exact| of each dot product x_m . w_n of length K under any summation order:
+    gamma_K * sum_k |x_k w_nk|, gamma_K = K u / (1 - K u), u = 2^-24 (plus the products are exact in fp32)."""
+    K = X.shape[1]
+    u = 2.0 ** -24
+    g = K * u / (1 - K * u)
+    xa = np.abs(synth.bf16_to_f32(X).astype(np.float64))
+    wa = np.abs(synth.bf16_to_f32(W).astype(np.float64))
+    return g * (xa @ wa.T)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("M,K,N", [(600, 2048, 2048), (300, 4096, 14336)])
+def test_continuous_bf16(sffn, algo, M, K, N):
+    """Gaussian bf16 inputs off the dyadic grid (full 8-bit mantissas): tensor-core and oracle sums differ by
+    rounding, so a pre-activation within the fp32 summation bound of 0 may land on either side of the threshold.
+    Bar: every (row, unit) where GPU and oracle disagree on "stored" has |a| <= that bound; every unit
+    stored by both holds a value within one bf16 rounding + the bound of a; Y per row within 1e-2 of Eq.1 and of
+    Eq.3 over the oracle's TwELL.  The mismatch count is printed."""
+    rng = np.random.default_rng(11 + K)
+    T, C = 256, 8
+    Xf = rng.standard_normal((M, K)).astype(np.float32)
+    Xf[:, 0] = 4.0  # bias channel: P(a > 0) ~ 2.3% with W_g[:, 0] = -0.5
+    Wgf = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    Wgf[:, 0] = -0.5
+    b16 = lambda a: torch.from_numpy(a).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    X, Wg = b16(Xf), b16(Wgf)
+    Wu = b16((rng.standard_normal((N, K)) * 0.02).astype(np.float32))
+    Wd = b16((rng.standard_normal((N, K)) * 0.02).astype(np.float32))
+    ws = torch.empty(sffn.workspace_bytes(M, K, N, T, C, algo), dtype=torch.uint8, device="cuda")
+    ov = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), T, C, algo=algo, workspace=ws, overflow=ov)
+    assert sffn.overflow_check(ov) == 0
+    tw = words_np(sffn.twell_view(ws, M, N, C))
+    twell_invariants(tw, N, T, C)
+    A = oracle.gate_preact(X, Wg)
+    wo, counts, n_ov, _ = oracle.pack(A.astype(np.float32), T, C)
+    assert n_ov == 0
+    Hg, Hr = oracle.unpack(tw, N, T, C).astype(np.float64), oracle.unpack(wo, N, T, C).astype(np.float64)
+    bound = _fp32_sum_bound(X, Wg)
+    mism = (Hg > 0) != (Hr > 0)
+    print(f"[continuous {M}x{K}x{N}] stored {int((Hr > 0).sum())}, index mismatches {int(mism.sum())}")
+    assert (np.abs(A[mism]) <= bound[mism]).all(), "a stored/unstored mismatch outside the fp32 summation bound"
+    both = (Hg > 0) & (Hr > 0)
+    assert (np.abs(Hg[both] - A[both]) <= 2.0 ** -8 * np.abs(A[both]) + 2 * bound[both]).all()
+    y = bf16_np(Y)
+    assert_y(y, oracle.ffn_twell(X, wo, Wu, Wd, N, T, C))
+    assert_y(y, oracle.ffn_twell(X, wo, Wu, Wd, N, T, C, A=A))  # == Eq.1 (no overflow: skipped terms have a <= 0)
 
 
 @pytest.mark.parametrize("algo", ALGOS)
@@ -507,7 +620,7 @@ def test_forward_with_overflow(sffn, algo):
     n_ov = sffn.overflow_check(ov)
     wo, counts, n_ov_ref, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
     assert n_ov == n_ov_ref > 0
-    assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
+    assert_y(bf16_np(Y), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, cfg.T, cfg.C))
 
 
 # ----------------------------------------------------------------- overflow-exact (hybrid) forward, NEXT-1
@@ -527,9 +640,9 @@ def test_forward_hybrid_exact_on_overflow(sffn, algo):
     assert 0 < len(ov_rows) <= 512 and int(cnt.item()) == len(ov_rows)
     y = bf16_np(Y)
     Y1 = oracle.ffn_dense(X[ov_rows], Wg, Wu, Wd)
-    assert rel_fro(y[ov_rows], Y1) < Y_TOL
+    assert_y(y[ov_rows], Y1)
     Y3 = oracle.ffn_twell(X[ok_rows], wo[ok_rows], Wu, Wd, cfg.N, cfg.T, cfg.C)
-    assert rel_fro(y[ok_rows], Y3) < Y_TOL
+    assert_y(y[ok_rows], Y3)
     # without the backup the overflowed rows are truncated (and measurably off Eq.1)
     Yt = bf16_np(sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo=algo))
     assert rel_fro(Yt[ov_rows], Y1) > 10 * rel_fro(y[ov_rows], Y1)
@@ -605,8 +718,8 @@ def test_union_low_sparsity_dense_blocks(sffn, sparsity):
     Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), cfg.T, cfg.C, algo="union")
     words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
     y = bf16_np(Y)
-    assert rel_fro(y, oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
-    assert rel_fro(y, oracle.ffn_dense(X, Wg, Wu, Wd)) < Y_TOL
+    assert_y(y, oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C))
+    assert_y(y, oracle.ffn_dense(X, Wg, Wu, Wd))
 
 
 @pytest.mark.gpu
@@ -739,12 +852,12 @@ def test_hybrid_training_forward(sffn, dense_cap):
     assert (np.abs(g_dense - ref_dense) <= 2.0 ** -8 * np.abs(ref_dense) + 1e-30).all()
     y = bf16_np(Y)
     # SpMM against the oracle on the GPU's own bf16 SDDMM output, and the whole chain against the fp64 oracle chain
-    assert rel_fro(y, oracle.hybrid_spmm(g_ell, col, nnz, loc, dmap, g_dense, Wd)) < Y_TOL
+    assert_y(y, oracle.hybrid_spmm(g_ell, col, nnz, loc, dmap, g_dense, Wd))
     chain = oracle.hybrid_spmm(ref_ell, col, nnz, loc, dmap, ref_dense, Wd)
-    assert rel_fro(y, chain) < Y_TOL
+    assert_y(y, chain)
     keep = loc != -2
     eq3 = oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)
-    assert rel_fro(y[keep], eq3[keep]) < Y_TOL
+    assert_y(y[keep], eq3[keep])
     assert (y[~keep] == 0).all()
 
 
@@ -803,7 +916,7 @@ def test_union_small_shapes(sffn, N, T, C, K, M, sp):
     Y = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), T, C, algo="union")
     words, counts, ov, A = oracle.pack_from_inputs(X, Wg, T, C)
     y = bf16_np(Y)
-    assert rel_fro(y, oracle.ffn_twell(X, words, Wu, Wd, N, T, C)) < Y_TOL
+    assert_y(y, oracle.ffn_twell(X, words, Wu, Wd, N, T, C))
 
 
 @pytest.mark.parametrize("seed", [1, 2])
@@ -818,4 +931,4 @@ def test_forward_other_seeds(sffn, name, M, seed):
     words, counts, ov, A = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
     got = tw.cpu().numpy().view(np.uint32)
     assert oracle.valid_prefix_equal(got, words, cfg.T, cfg.C).all()
-    assert rel_fro(bf16_np(Y), oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C)) < Y_TOL
+    assert_y(bf16_np(Y), oracle.ffn_twell(X, words, Wu, Wd, cfg.N, cfg.T, cfg.C))

@@ -83,6 +83,29 @@ def test_gate_preact_exact_integer_on_grid():
     assert synth.worst_case_units(synth.CONFIGS["70B"]) < 2 ** 20
 
 
+@pytest.mark.parametrize("name,M,N", [("tiny", 64, 256), ("1B", 40, 512), ("70B", 6, 768)])
+def test_gate_preact_matmul_equals_loop_on_grid(name, M, N):
+    """gate_preact_matmul (one numpy fp64 matmul: the library-primitive step used for large row samples) equals
+    the k-ascending C loop AND the int64 integer matmul of the q's bit for bit on grid inputs — including K=8192
+    with a row and a weight row at the worst-case magnitudes (|q_x| = 14, |q_w| = 7 everywhere: 802,816 units
+    < 2^20), where a lossy summation would show."""
+    cfg = synth.CONFIGS[name].replace(M=M, N=N)
+    X = synth.gen_x(cfg).copy()
+    Wg = synth.gen_w(cfg, "g").copy()
+    X[0, :] = synth_bits(np.full((1, cfg.K), 14 * 2.0 ** -cfg.x_exp, dtype=np.float32))[0]
+    Wg[0, :] = synth_bits(np.full((1, cfg.K), 7 * 2.0 ** -cfg.w_exp, dtype=np.float32))[0]
+    A_mm = oracle.gate_preact_matmul(X, Wg, rows_per_call=M // 2 + 1)
+    A_loop = oracle.gate_preact(X, Wg)
+    qx = np.rint(synth.bf16_to_f32(X) * 2.0 ** cfg.x_exp).astype(np.int64)
+    qw = np.rint(synth.bf16_to_f32(Wg) * 2.0 ** cfg.w_exp).astype(np.int64)
+    ref = (qx @ qw.T).astype(np.float64) * 2.0 ** -(cfg.x_exp + cfg.w_exp)
+    assert A_mm[0, 0] == 14 * 7 * cfg.K * 2.0 ** -(cfg.x_exp + cfg.w_exp)
+    assert np.array_equal(A_mm, ref) and np.array_equal(A_loop, ref)
+    w1, c1, o1, _ = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C, matmul=True)
+    w2, c2, o2, _ = oracle.pack_from_inputs(X, Wg, cfg.T, cfg.C)
+    assert np.array_equal(w1, w2) and np.array_equal(c1, c2) and o1 == o2
+
+
 def test_gate_preact_permutation_matrix():
     """W_g a permutation matrix (hidden-major, W_g[n, pi(n)] = 1): A[:, n] = X[:, pi(n)].
     A transposed W_g (pi^-1) fails for a non-involutive pi."""
