@@ -54,6 +54,8 @@ def _load():
                                 ctypes.c_void_p, ctypes.c_void_p]
         lib.synth_w.argtypes = [P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]
         lib.synth_neuron.argtypes = [P, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        lib.synth_pattern.argtypes = [P, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                      ctypes.c_void_p]
         _lib = lib
     return _lib
 
@@ -152,7 +154,23 @@ def gen_w(cfg: Config, which: str, row0: int = 0, nrows: int | None = None, dtyp
     return out
 
 
+def gen_pattern(cfg: Config, row0: int = 0, nrows: int | None = None, pop_sigma: float = 1.0,
+                p: np.ndarray | None = None) -> np.ndarray:
+    """"Direct TwELL" mode: a dense bf16 [nrows, N] activation matrix with the generator's per-token
+    densities and a LogNormal(., pop_sigma) per-neuron popularity, values q * 2^-4 (q = 1..15), no gate GEMM.
+    Pack it with the oracle (oracle.pack) to feed the fused up/down alone."""
+    lib = _load()
+    nrows = cfg.M - row0 if nrows is None else nrows
+    if p is None:
+        p = token_targets(cfg)
+    out = np.empty((nrows, cfg.N), dtype=np.uint16)
+    c = cfg._c()
+    lib.synth_pattern(ctypes.byref(c), p.ctypes.data, row0, nrows, pop_sigma, out.ctypes.data)
+    return out
+
+
 def neuron_params(cfg: Config):
+    """(beta_n * 64, dead_n) per neuron: the bias coefficient of the lognormal popularity model and the dead flag."""
     lib = _load()
     c = cfg._c()
     b = np.empty(cfg.N, dtype=np.int32)

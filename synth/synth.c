@@ -18,6 +18,14 @@
  *      -> a fraction of noise channels is shared by all tokens of a sequence.
  *   - dead neurons -> a fraction of hidden units whose gate weights
  *     are zero on the noise channels and negative on the bias channels.
+ *   - lognormal per-neuron popularity (hot neurons fire for far more tokens than
+ *     cold ones, Fig 8): neuron n's bias coefficient beta_n = clip(BETA0 - BETA_S z_n,
+ *     BETA_MIN, 7), z_n ~ N(0,1), in steps of 1/64, spread over the K_b bias channels; its
+ *     firing probability Phi_c(beta_n c_m / s_m) is then close to lognormal in z_n (log Phi_c is
+ *     near-linear in beta at the operating point, slope ~ -1.4 per unit of beta); BETA_S = 0.7
+ *     gives a standard deviation of log(popularity) of 1.0 over the live neurons at 7B / 99%
+ *     (measured on a 2048-token window), i.e. LogNormal(., 1) popularity; the hottest neuron
+ *     fires for ~20% of tokens.
  *
  * Exactness: every element is q * 2^-e with |q_x| <= 14, |q_w| <= 7,
  * so X*W products are integer multiples of 2^-11 and every partial sum of a length
@@ -45,11 +53,20 @@ typedef struct {
     int32_t w_exp;     /* W = q * 2^-w_exp */
 } synth_cfg;
 
-enum { S_XTOK = 1, S_XSEQ = 2, S_XI = 3, S_WG = 4, S_WU = 5, S_WD = 6, S_NEU = 7 };
+enum { S_XTOK = 1, S_XSEQ = 2, S_XI = 3, S_WG = 4, S_WU = 5, S_WD = 6, S_NEU = 7, S_PAT = 8, S_PATV = 9 };
 
-/* neuron coefficient classes b in {4,5,6,7} with these cumulative probabilities (x65536) */
-static const uint32_t B_CUM[4] = {6554u, 26214u, 49152u, 65536u}; /* 0.10 0.30 0.35 0.25 */
-static const double B_P[4] = {0.10, 0.30, 0.35, 0.25};
+/* per-neuron popularity: beta = clip(BETA0 - BETA_S * z, BETA_MIN, BETA_MAX), quantised to 1/64 */
+#ifndef BETA0
+#define BETA0 5.0
+#endif
+#ifndef BETA_S
+#define BETA_S 0.7
+#endif
+#ifndef BETA_MIN
+#define BETA_MIN 1.5
+#endif
+#define BETA_MAX 7.0
+#define BETA_Q 64
 #define QX_MAX 14
 #define QW_NOISE_VAR 5.0
 
@@ -87,15 +104,29 @@ static inline void put(void* out, int out_f32, int64_t i, int q, int e) {
         ((uint16_t*)out)[i] = q_to_bf16(q, e);
 }
 
-int synth_neuron(const synth_cfg* c, int64_t n, int32_t* b_out, int32_t* dead_out) {
+static inline int beta_q_of_z(double z) {
+    double b = BETA0 - BETA_S * z;
+    if (b < BETA_MIN) b = BETA_MIN;
+    if (b > BETA_MAX) b = BETA_MAX;
+    return (int)lround(b * BETA_Q);
+}
+
+/* neuron n: bias coefficient beta_n * 64 (integer) and the dead flag */
+int synth_neuron(const synth_cfg* c, int64_t n, int32_t* bq_out, int32_t* dead_out) {
     uint64_t r = rnd(key_of(c->seed, S_NEU), (uint64_t)n);
-    uint32_t u = (uint32_t)(r & 0xFFFF);
-    int b = 4;
-    while (b < 7 && u >= B_CUM[b - 4]) b++;
-    int dead = ((double)((r >> 32) & 0xFFFF) / 65536.0) < c->dead_frac;
-    if (b_out) *b_out = dead ? 7 : b;
+    double u1 = ((double)(r & 0xFFFFFF) + 0.5) / 16777216.0;
+    double u2 = ((double)((r >> 24) & 0xFFFFFF) + 0.5) / 16777216.0;
+    double z = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+    int dead = ((double)((r >> 48) & 0xFFFF) / 65536.0) < c->dead_frac;
+    if (bq_out) *bq_out = dead ? (int32_t)(BETA_MAX * BETA_Q) : beta_q_of_z(z);
     if (dead_out) *dead_out = dead;
     return 0;
+}
+
+/* bias-channel weight magnitudes of a neuron with coefficient bq/64: Bresenham split over the Kb channels
+ * (each channel floor or ceil of beta, prefix sums within 1 of beta * prefix length) */
+static inline int bias_w(int32_t bq, int64_t k) {
+    return (int)(((int64_t)bq * (k + 1)) / BETA_Q - ((int64_t)bq * k) / BETA_Q);
 }
 
 /* Per-token target densities p[0..M): mean (1-sparsity), heavy tail, position decay, clipped. */
@@ -131,11 +162,19 @@ int synth_token_targets(const synth_cfg* c, double* p) {
     return 0;
 }
 
-/* expected density of a token with bias c_units and noise std s (units of 2^-(x_exp+w_exp)) */
+/* expected density of a token with bias c_units and noise std s (units of 2^-(x_exp+w_exp)): the mean over the
+ * live neurons' beta distribution (midpoint rule on z in [-6, 6] weighted by the normal density) */
+#define NZ 121
 static double density_model(const synth_cfg* c, double cu, double s) {
-    double acc = 0;
-    for (int i = 0; i < 4; ++i) acc += B_P[i] * 0.5 * erfc(((double)(4 + i) * cu / s) / 1.4142135623730951);
-    return (1.0 - c->dead_frac) * acc;
+    double acc = 0, wsum = 0;
+    for (int i = 0; i < NZ; ++i) {
+        const double z = -6.0 + 12.0 * (i + 0.5) / NZ;
+        const double w = exp(-0.5 * z * z);
+        const double beta = (double)beta_q_of_z(z) / BETA_Q;
+        acc += w * 0.5 * erfc((beta * cu / s) / 1.4142135623730951);
+        wsum += w;
+    }
+    return (1.0 - c->dead_frac) * acc / wsum;
 }
 
 /* X rows [row0, row0+nrows) -> out (row-major, K per row). p = synth_token_targets output (length M).
@@ -169,10 +208,10 @@ int synth_x(const synth_cfg* c, const double* p, int64_t row0, int64_t nrows, in
         if (cu > 0 && fabs(density_model(c, (double)(cu - 1), s) - target) < fabs(density_model(c, (double)cu, s) - target))
             cu -= 1;
         if (c_out) c_out[i] = cu;
-        int rem = cu;
+        /* cu spread evenly over the Kb bias channels (each <= QX_MAX since cu <= Kb * QX_MAX), so the bias
+         * term sum_k X[m,k] W_g[n,k] is ~ -cu * beta_n for every neuron */
         for (int64_t k = 0; k < Kb; ++k) {
-            int q = rem > QX_MAX ? QX_MAX : rem;
-            rem -= q;
+            int q = (int)(cu / Kb) + (k < cu % Kb ? 1 : 0);
             put(out, out_f32, i * K + k, q, c->x_exp);
         }
     }
@@ -191,12 +230,41 @@ int synth_w(const synth_cfg* c, int which, int64_t row0, int64_t nrows, int out_
         for (int64_t k = 0; k < K; ++k) {
             int q;
             if (which == 0 && k < Kb)
-                q = -b;
+                q = -bias_w(b, k);
             else if (which == 0 && dead)
                 q = 0;
             else
                 q = qw(rnd(key, (uint64_t)(n * K + k)));
             put(out, out_f32, i * K + k, q, c->w_exp);
+        }
+    }
+    return 0;
+}
+
+/* "Direct TwELL" mode: an activation pattern with values, WITHOUT a gate GEMM, for isolating the
+ * fused up/down and for unpack tests.  Rows [row0, row0+nrows) of a dense bf16 [nrows, N] matrix H (zeros off the
+ * pattern; the caller packs it with the oracle).  Unit n of token m is active with probability
+ * min(1, p[m] * w_n), w_n = the neuron's lognormal popularity exp(sigma z_n - sigma^2/2) / (1 - dead_frac) (dead
+ * neurons: 0), sigma = pop_sigma; active values are positive grid values q * 2^-4, q in 1..15. */
+int synth_pattern(const synth_cfg* c, const double* p, int64_t row0, int64_t nrows, double pop_sigma,
+                  uint16_t* out) {
+    const int64_t N = c->N;
+    const uint64_t kn = key_of(c->seed, S_NEU), kp = key_of(c->seed, S_PAT), kv = key_of(c->seed, S_PATV);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < nrows; ++i) {
+        const int64_t m = row0 + i;
+        for (int64_t n = 0; n < N; ++n) {
+            uint64_t r = rnd(kn, (uint64_t)n);
+            double u1 = ((double)(r & 0xFFFFFF) + 0.5) / 16777216.0;
+            double u2 = ((double)((r >> 24) & 0xFFFFFF) + 0.5) / 16777216.0;
+            double z = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+            int dead = ((double)((r >> 48) & 0xFFFF) / 65536.0) < c->dead_frac;
+            double w = dead ? 0.0 : exp(pop_sigma * z - 0.5 * pop_sigma * pop_sigma) / (1.0 - c->dead_frac);
+            double q = p[m] * w;
+            uint64_t ra = rnd(kp, (uint64_t)(m * N + n));
+            double u = ((double)(ra >> 11) + 0.5) / 9007199254740992.0;
+            int qv = 1 + (int)(rnd(kv, (uint64_t)(m * N + n)) % 15);
+            out[i * N + n] = u < q ? q_to_bf16(qv, 4) : (uint16_t)0;
         }
     }
     return 0;

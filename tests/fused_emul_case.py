@@ -20,7 +20,7 @@ import numpy as np  # noqa: E402
 
 import oracle  # noqa: E402
 import synth  # noqa: E402
-from gpu_util import assert_y, to_dev  # noqa: E402
+from gpu_util import ROW_TOL_EQ1, assert_y, to_dev  # noqa: E402
 
 
 def main():
@@ -57,7 +57,9 @@ def main():
     ref = acc.to(torch.bfloat16)
     words, counts, n_ov, A = oracle.pack_from_inputs(Xn, Wgn, T, C)
     Y3 = oracle.ffn_twell(Xn, words, Wun, Wdn, cfg.N, T, C)  # Eq.3 of the unsharded problem
-    Y1 = oracle.ffn_dense(Xn, Wgn, Wun, Wdn)                  # Eq.1
+    ok = ~(counts > T // C - 1).any(1)                         # rows without an overflowed tile (reading R5)
+    assert ok.sum() > M // 2
+    Y1 = oracle.ffn_dense(Xn[ok], Wgn, Wun, Wdn)              # Eq.1 on those rows
     streams = [torch.cuda.Stream() for _ in range(G)]
     for call_i, cset in enumerate((0, 1)):
         off = flags_off + 4 * nwin * cset
@@ -80,7 +82,7 @@ def main():
             assert cnt == want, f"window {r} set {cset} counters {cnt} != {want}"
             y = Y.float().cpu().numpy().astype(np.float64)
             assert_y(y, Y3)
-            assert_y(y, Y1)
+            assert_y(y[ok], Y1, row_tol=ROW_TOL_EQ1)
         # what sym_finish_kernel does after its barrier: zero the set this call used, flip the table's set offset
         for w in wins:
             w[off:off + 4 * nwin].zero_()

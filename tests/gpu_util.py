@@ -31,10 +31,20 @@ def row_rel(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.where(n > 0, d / np.where(n > 0, n, 1.0), np.where(d > 0, np.inf, 0.0))
 
 
-def assert_y(y: np.ndarray, ref: np.ndarray, tol: float = 1e-2, rows=None):
-    """The Y bar: relative Frobenius error over the compared rows AND the worst row's relative error both below
-    `tol` (north_star: 1e-2 bf16 / 1e-5 fp32; the per-row bar catches a dropped term in a single row, which the
-    global norm would dilute).  Logs the worst row and the per-row max-abs error."""
+# bf16 unit roundoff (8 significant bits): every bf16 rounding is within a relative U_BF16 of its argument
+U_BF16 = 2.0 ** -8
+# per-row bar against Eq.1 with the EXACT gate: a row with a single active unit sees three bf16 roundings of its one
+# term (the stored gate h_v, reading A10; h = h_v * u on the union path, R9; the bf16 output) -> 3u + 3u^2
+ROW_TOL_EQ1 = 3 * U_BF16 + 3 * U_BF16 ** 2
+
+
+def assert_y(y: np.ndarray, ref: np.ndarray, tol: float = 1e-2, rows=None, row_tol: float | None = None):
+    """The Y bar: relative Frobenius error over the compared rows below `tol` (north_star: 1e-2 bf16 / 1e-5 fp32)
+    AND the worst row's relative error below `row_tol` (default `tol`; the per-row bar catches a dropped term in a
+    single row, which the global norm would dilute).  Against Eq.3 with the stored gate a row's terms see at most two
+    bf16 roundings (h and the output: 2u + u^2 = 7.8e-3 < 1e-2); against Eq.1 (exact gate) pass
+    row_tol=ROW_TOL_EQ1.  Logs the worst row and the per-row max-abs error."""
+    row_tol = tol if row_tol is None else row_tol
     y = np.asarray(y, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert y.shape == ref.shape, (y.shape, ref.shape)
@@ -48,7 +58,7 @@ def assert_y(y: np.ndarray, ref: np.ndarray, tol: float = 1e-2, rows=None):
     name = f"row {rows[w]}" if rows is not None else f"row {w}"
     print(f"[Y] rows={y.shape[0]} rel_fro={fro:.3e} worst {name} rel={rr[w]:.3e} max_abs={mabs:.3e}")
     assert fro < tol, f"rel_fro {fro:.3e} >= {tol}"
-    assert rr[w] < tol, f"{name}: row-relative error {rr[w]:.3e} >= {tol} (rel_fro {fro:.3e})"
+    assert rr[w] < row_tol, f"{name}: row-relative error {rr[w]:.3e} >= {row_tol:.3e} (rel_fro {fro:.3e})"
     return fro
 
 

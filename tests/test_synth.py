@@ -53,3 +53,37 @@ def test_dead_neurons():
     assert abs(dead.mean() - cfg.dead_frac) < 0.05
     A = oracle.gate_preact(synth.gen_x(cfg), synth.gen_w(cfg, "g"))
     assert not np.any(A[:, dead.astype(bool)] > 0)
+
+
+def test_neuron_popularity_lognormal():
+    """per-neuron popularity (the fraction of tokens a live neuron fires for) is lognormal with
+    sigma ~ 1 (std of log popularity over the live neurons of a 2048-token window of the 7B config), with hot
+    neurons (small beta) firing far more often than cold ones."""
+    cfg = synth.CONFIGS["7B"]
+    p = synth.token_targets(cfg)
+    A = oracle.gate_preact_matmul(synth.gen_x(cfg, 0, 2048, p=p), synth.gen_w(cfg, "g"))
+    pop = (A > 0).mean(0)
+    bq, dead = synth.neuron_params(cfg)
+    alive = pop > 0
+    assert abs(alive.mean() - (1 - cfg.dead_frac)) < 0.05 and not np.any(pop[dead.astype(bool)] > 0)
+    s = np.std(np.log(pop[alive]))
+    assert 0.8 < s < 1.25, s
+    live = ~dead.astype(bool)
+    hot, cold = bq[live] <= np.percentile(bq[live], 10), bq[live] >= np.percentile(bq[live], 90)
+    assert pop[live][hot].mean() > 10 * pop[live][cold].mean()
+
+
+def test_direct_pattern_mode():
+    """Direct mode: per-token density follows the targets, popularity follows the lognormal weights, values are
+    positive grid values; deterministic and row-independent."""
+    cfg = synth.CONFIGS["7B"].replace(M=4096)
+    p = synth.token_targets(cfg)
+    H = synth.gen_pattern(cfg, p=p)
+    assert np.array_equal(synth.gen_pattern(cfg, 100, 7, p=p), H[100:107])
+    act = H != 0
+    assert abs(act.mean() - p.mean()) / p.mean() < 0.03
+    assert np.corrcoef(act.mean(1), p)[0, 1] > 0.9
+    v = synth.bf16_to_f32(H[act]) * 16
+    assert (v >= 1).all() and (v <= 15).all() and np.array_equal(v, np.rint(v))
+    pop = act.mean(0)
+    assert np.std(np.log(pop[pop > 0])) > 0.7
