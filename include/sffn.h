@@ -111,7 +111,7 @@ int sffn_unpack(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int64
  * in fp32; UNION rounds h to bf16 before the down GEMM (as the paper's kernel does, L2 P:994-1002).
  *   X [M, K] bf16, twell [M, N/C] uint32, Wu [N, K] bf16, Wd [N, K] bf16, Y [M, K] bf16 (output)
  *   workspace / ws_bytes: >= sffn_up_down_workspace_bytes(M, N, T, C, algo) (may be NULL for GATHER)
- * Constraints: those of sffn_pack, and K <= 8192 for GATHER.
+ * Constraints: those of sffn_pack, K <= 65536, and K <= 8192 for GATHER (x is held in registers).
  */
 int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const void* Wd, int64_t M, int64_t K,
                  int64_t N, int T, int C, void* Y, void* workspace, size_t ws_bytes, int algo, void* stream);
@@ -119,8 +119,9 @@ int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const voi
 /*
  * sffn_forward — the whole sparse FFN forward: sffn_pack into `workspace` (>= sffn_forward_workspace_bytes)
  * then sffn_up_down with the rest of the workspace.  GATHER = the paper's two launches; UNION
- * adds two small metadata launches (4 total).  The TwELL left at the start of the workspace is valid
- * after the call (stream-ordered).
+ * launches 7 kernels (gate GEMM, row order pi, X in pi order, union metadata, gate lists, UP and DOWN
+ * GEMMs; sffn_launch_count reports them) plus one memset.  The TwELL left at the start of the workspace
+ * is valid after the call (stream-ordered).
  */
 int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
                  int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo,

@@ -208,14 +208,19 @@ int updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* W
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
 
+int resolve_algo(int algo, int64_t N);
+
+// argument / shape checks of the up/down entry points; the GATHER kernel keeps x in registers (K <= 8192), the
+// UNION tensor-core path tiles K (K <= 65536)
 int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
-                  int T, int C, const void* Y) {
+                  int T, int C, const void* Y, int algo) {
     if (M == 0) X = tw = Y = Wu;  // empty batch: X / twell / Y may be NULL
     if (!X || !tw || !Wu || !Wd || !Y) return SFFN_ERR_INVALID_ARG;
     if (!aligned16(X) || !aligned16(tw) || !aligned16(Wu) || !aligned16(Wd) || !aligned16(Y))
         return SFFN_ERR_INVALID_ARG;
     if (!valid_TC(T, C)) return SFFN_ERR_INVALID_ARG;
-    if (M < 0 || K < 64 || K % 64 != 0 || K > 8192 || N <= 0 || N % T != 0 || N > 65536) return SFFN_ERR_SHAPE;
+    if (M < 0 || K < 64 || K % 64 != 0 || K > 65536 || N <= 0 || N % T != 0 || N > 65536) return SFFN_ERR_SHAPE;
+    if (K > 8192 && N > 0 && resolve_algo(algo, N) == SFFN_ALGO_GATHER) return SFFN_ERR_SHAPE;
     if (M > 2147483647) return SFFN_ERR_SHAPE;
     return SFFN_OK;
 }
@@ -549,9 +554,9 @@ int sffn_unpack(const uint32_t* twell, int64_t M, int64_t N, int T, int C, int64
 
 int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
                  int T, int C, void* Y, void* workspace, size_t ws_bytes, int algo, void* stream) {
-    int r = updown_checks(X, twell, Wu, Wd, M, K, N, T, C, Y);
-    if (r != SFFN_OK) return r;
     if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
+    int r = updown_checks(X, twell, Wu, Wd, M, K, N, T, C, Y, algo);
+    if (r != SFFN_OK) return r;
     if (resolve_algo(algo, N) == SFFN_ALGO_UNION && M > 0) {
         if (!union_applicable(N)) return SFFN_ERR_SHAPE;
         if (!workspace || !aligned16(workspace) || ws_bytes < updown_ws_bytes(M, N, K, algo, T, C)) return SFFN_ERR_SHAPE;
@@ -564,8 +569,8 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
                  int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow, int algo, void* stream) {
     int r = pack_checks(X, Wg, M, K, N, T, C, workspace);
     if (r != SFFN_OK) return r;
-    if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
     if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
+    if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y, algo)) != SFFN_OK) return r;
     if (resolve_algo(algo, N) == SFFN_ALGO_UNION && !union_applicable(N)) return SFFN_ERR_SHAPE;
     if (ws_bytes < sffn_forward_workspace_bytes(M, K, N, T, C, algo)) return SFFN_ERR_SHAPE;
     if ((r = check_device()) != SFFN_OK) return r;
@@ -592,7 +597,7 @@ int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const voi
                         const uint64_t* ptrs, int G, int rank, int phase, void* stream) {
     int r = pack_checks(X, Wg, M, K, N, T, C, workspace);
     if (r != SFFN_OK) return r;
-    if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y)) != SFFN_OK) return r;
+    if ((r = updown_checks(X, workspace, Wu, Wd, M, K, N, T, C, Y, SFFN_ALGO_UNION)) != SFFN_OK) return r;
     if (!union_applicable(N) || union_brows() != 128) return SFFN_ERR_UNSUPPORTED;
     if (ws_bytes < sffn_forward_workspace_bytes(M, K, N, T, C, SFFN_ALGO_UNION)) return SFFN_ERR_SHAPE;
     if ((r = check_device()) != SFFN_OK) return r;
@@ -611,9 +616,9 @@ int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const voi
 
 int sffn_down(const uint32_t* twell, const void* Wd, int64_t M, int64_t K, int64_t N, int T, int C, void* Y,
               void* workspace, size_t ws_bytes, int algo, void* stream) {
-    int r = updown_checks(Wd, twell, Wd, Wd, M, K, N, T, C, Y);
-    if (r != SFFN_OK) return r;
     if (algo < SFFN_ALGO_AUTO || algo > SFFN_ALGO_UNION) return SFFN_ERR_INVALID_ARG;
+    int r = updown_checks(Wd, twell, Wd, Wd, M, K, N, T, C, Y, algo);
+    if (r != SFFN_OK) return r;
     const int a = resolve_algo(algo, N);
     if (a == SFFN_ALGO_UNION && M > 0) {
         if (!union_applicable(N)) return SFFN_ERR_SHAPE;

@@ -288,17 +288,22 @@ int sffn_comm_symmetric_init(sffn_comm* c, int64_t max_rows, int64_t K) {
         c->win = nullptr;
         return SFFN_ERR_UNSUPPORTED;
     }
-    if (cudaMemset(static_cast<uint8_t*>(c->sym_buf) + flags_off, 0, static_cast<size_t>(8 * nwin)) != cudaSuccess ||
-        cudaMalloc(&c->d_ptrs, static_cast<size_t>(c->nranks + 2) * 8) != cudaSuccess) {
+    // any failure from here on releases everything acquired above, so a retry starts clean
+    auto release = [&](int status) {
+        if (c->d_ptrs) cudaFree(c->d_ptrs);
+        c->d_ptrs = nullptr;
         ncclDevCommDestroy(c->nccl, &c->dev);
         ncclCommWindowDeregister(c->nccl, c->win);
         ncclMemFree(c->sym_buf);
         c->sym_buf = nullptr;
         c->win = nullptr;
-        return SFFN_ERR_CUDA;
-    }
+        return status;
+    };
+    if (cudaMemset(static_cast<uint8_t*>(c->sym_buf) + flags_off, 0, static_cast<size_t>(8 * nwin)) != cudaSuccess ||
+        cudaMalloc(&c->d_ptrs, static_cast<size_t>(c->nranks + 2) * 8) != cudaSuccess)
+        return release(SFFN_ERR_CUDA);
     sym_ptrs_kernel<<<1, 32>>>(c->dev, c->win, c->nranks, req.lsaMultimem ? 1 : 0, flags_off, c->d_ptrs);
-    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return SFFN_ERR_CUDA;
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return release(SFFN_ERR_CUDA);
     c->flags_off = flags_off;
     c->nwin = nwin;
     c->has_dev = true;

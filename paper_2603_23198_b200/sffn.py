@@ -230,9 +230,13 @@ def forward_host_chunks(M: int, chunk_rows: int = 4096) -> list:
 
 
 def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspace=None, stage=None,
-                 overflow=None, algo="auto", chunk_rows: int = 4096, stream=None, stage_slots: int = 2) -> torch.Tensor:
+                 overflow=None, algo="auto", chunk_rows: int = 4096, stream=None, stage_slots: int = 2,
+                 synchronize: bool = True) -> torch.Tensor:
     """Sparse forward with X / Y in (pinned) host memory; copies overlap compute (sffn_forward_host).
-    stage_slots: X / Y staging slots on the device (>= 2; more lets copies run further ahead)."""
+    stage_slots: X / Y staging slots on the device (>= 2; more lets copies run further ahead).
+    The device-to-host copies into `out` are stream-ordered: with synchronize=True (default) the stream is
+    synchronized before returning, so `out` can be read at once; with synchronize=False the caller must
+    synchronize the stream before reading `out` (reading a host tensor does not wait for CUDA work)."""
     M, K = x_host.shape
     N = wg.shape[0]
     if x_host.is_cuda or x_host.dtype != torch.bfloat16 or not x_host.is_contiguous():
@@ -250,6 +254,8 @@ def forward_host(x_host, wg, wu, wd, T: int = 256, C: int = 8, out=None, workspa
                                  workspace.numel() * workspace.element_size(), _p(stage),
                                  stage.numel() * stage.element_size(), _p(overflow), a, chunk_rows,
                                  _stream(stream)), "sffn_forward_host")
+    if synchronize:
+        (torch.cuda.current_stream() if stream is None else stream).synchronize()
     return out
 
 

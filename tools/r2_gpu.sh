@@ -12,3 +12,7 @@ if [ -z "$NO_BENCH" ]; then
   timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
   echo "bench rc=$?"; tail -c 1500 gpurun_out/bench.err | grep -v Warning; cat gpurun_out/bench.json
 fi
+if [ -n "$TIMELINE" ]; then
+  timeout 300 python tools/timeline.py --config 7B --out gpurun_out/timeline_7B.json > gpurun_out/timeline.log 2>&1
+  echo "timeline rc=$?"; cat gpurun_out/timeline.log | grep -v Warning | tail -20
+fi

@@ -49,6 +49,19 @@ for _ in range(3):
     flush.fill_(1.0)
     fn()
 torch.cuda.synchronize()
+# the same steps timed with CUDA events exactly as bench.py does (flush outside the events), for comparison with
+# the CUPTI span below
+ev_ms = []
+for _ in range(20):
+    flush.fill_(1.0)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    fn()
+    s1.record()
+    ev_ms.append((s0, s1))
+torch.cuda.synchronize()
+ev_ms = [a.elapsed_time(b) for a, b in ev_ms]
+print(f"events: median {np.median(ev_ms) * 1e3:.1f} us, min {min(ev_ms) * 1e3:.1f}, max {max(ev_ms) * 1e3:.1f}")
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
