@@ -334,10 +334,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             if constexpr (EPI == EPI_TWELL) {
                 constexpr int ROW_WORDS = GEMM_BN / C;
+                // staging of the warp's 32 rows x ROW_WORDS packed words: for C <= 8 as ROW_WORDS/32 boxes of
+                // 32 rows x 128 B in the TMA 128-byte-swizzle layout (16-byte chunk index XOR row % 8), so the 32
+                // lanes (= 32 rows) writing the same word index hit 8 different bank groups instead of one bank;
+                // C = 16 (64-byte rows): plain row-major
+                constexpr bool SWZ = ROW_WORDS % 32 == 0;
                 const int T = args.T;
                 const int WPT = T / C;
                 const int cap = WPT - 1;
-                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * ROW_WORDS;
+                uint8_t* sbase = stg;
+                auto sword = [&](int p) -> uint32_t* {
+                    if constexpr (SWZ)
+                        return reinterpret_cast<uint32_t*>(sbase + (p >> 5) * 4096 + lane * 128 +
+                                                           ((((p >> 2) & 7) ^ (lane & 7)) << 4) + ((p & 3) << 2));
+                    else
+                        return reinterpret_cast<uint32_t*>(sbase) + lane * ROW_WORDS + p;
+                };
                 const int col_base = nb * GEMM_BN;
                 const bool row_ok = row0 + lane < args.M;
                 int z = 0, stored = 0;
@@ -348,20 +360,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     tmem_wait_ld();
                     const int tcol = ch * 32;
                     if (tcol % T == 0) z = 0;
-                    uint32_t* blk = srow + (tcol / T) * WPT;
+                    const int tbase = (tcol / T) * WPT;  // word of this tile's count within the row
+                    // Alg.1 line 11 (strict > 0 on the fp32 accumulator) as a 32-bit mask of the chunk's columns;
+                    // lines 12-15 as mask/popc compaction: the slot of column i is the running count z plus the
+                    // positives before it, popc(mask & (2^i - 1)) — ascending column order, no atomics, and the
+                    // (usual, at 99% sparsity) all-zero chunk costs only the compares
+                    uint32_t mask = 0;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float f = __uint_as_float(v[i]);
-                        if (f > 0.0f) {  // Alg.1 line 11 (strict)
-                            if (z < cap) {
-                                const uint32_t bf = __bfloat16_as_ushort(__float2bfloat16_rn(f));
-                                blk[1 + z] = static_cast<uint32_t>(col_base + tcol + i) | (bf << 16);
+                    for (int i = 0; i < 32; ++i) mask |= (__uint_as_float(v[i]) > 0.0f ? 1u : 0u) << i;
+                    if (mask) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int slot = z + __popc(mask & ((1u << i) - 1u));
+                            if (((mask >> i) & 1u) && slot < cap) {
+                                const uint32_t bf = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(v[i])));
+                                *sword(tbase + 1 + slot) = static_cast<uint32_t>(col_base + tcol + i) | (bf << 16);
                             }
-                            ++z;
                         }
+                        z += __popc(mask);
                     }
                     if ((tcol + 32) % T == 0) {
-                        blk[0] = static_cast<uint32_t>(z);  // Alg.1 line 17: true count
+                        *sword(tbase) = static_cast<uint32_t>(z);  // Alg.1 line 17: true count
                         if (z > cap && row_ok && args.overflow) atomicAdd(args.overflow, 1u);
                         stored += min(z, cap);
                     }
@@ -374,7 +393,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 __syncwarp();
                 if (lane == 0) {
                     // TwELL is a streaming output: L2 evict_first keeps X / W_g resident (gate GEMM -0.3%, ncu A/B)
-                    tma_store_2d_hint(&tmOut, stg, nb * ROW_WORDS, row0, policy_evict_first());
+                    if constexpr (SWZ) {
+#pragma unroll
+                        for (int q = 0; q < ROW_WORDS / 32; ++q)
+                            tma_store_2d_hint(&tmOut, stg + q * 4096, nb * ROW_WORDS + 32 * q, row0, policy_evict_first());
+                    } else {
+                        tma_store_2d_hint(&tmOut, stg, nb * ROW_WORDS, row0, policy_evict_first());
+                    }
                     bulk_commit();
                 }
             } else if constexpr (EPI == EPI_F32) {

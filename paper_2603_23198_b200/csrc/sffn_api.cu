@@ -149,7 +149,10 @@ int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, in
     if (!tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, K, M, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wg, K, N, GEMM_BK, pair ? GEMM_BN / 2 : GEMM_BN,
                  CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, twell, N / C, M, GEMM_BN / C, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        // TwELL store boxes: 32 rows x 32 words, 128-byte swizzled, for C <= 8 (gemm_tc.cuh EPI_TWELL staging);
+        // 32 rows x 16 words unswizzled for C = 16
+        !tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, twell, N / C, M, C <= 8 ? 32 : GEMM_BN / C, 32,
+                 C <= 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE))
         return SFFN_ERR_CUDA;
     GemmArgs args{};
     args.M = static_cast<int>(M);
@@ -353,11 +356,6 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         { union_rank_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_THREADS, 0,
                             st>>>(rnnz, (int)M, perm, um.umask, NB * (N / 32), bctr, (int)NB + 1); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-        if (gated) {
-            { permute_rows_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
-                static_cast<const uint4*>(X), perm, (int)M, (int)(K / 8), static_cast<uint4*>(xp)); note_launch(); }
-            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-        }
 
         // union lists + the UP work list (one launch), then the compact gate lists (gated) or the scattered G (non-gated)
         const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
@@ -370,8 +368,10 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
             union_dense_units(N, BR == 128 && N >= 256), rnnz, union_dense_nnz(N, BR == 128 && N >= 256)); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
         if (gated) {
+            // also writes X in pi order (the UP GEMM's A operand)
             { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
-                tw, (int)M, (int)N, T, C, um, perm); note_launch(); }
+                tw, (int)M, (int)N, T, C, um, perm, static_cast<const uint4*>(X), (int)(K / 8),
+                static_cast<uint4*>(xp)); note_launch(); }
             if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
         }
         if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)

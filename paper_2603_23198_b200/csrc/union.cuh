@@ -322,8 +322,13 @@ __global__ void __launch_bounds__(UB_THREADS) union_meta_kernel(const uint32_t* 
 // CTA); the row's stored entries in ascending neuron order = ascending union position (lane per tile, warp prefix
 // of the tile counts); position = uwoff + popc(umask prefix); coff[i][c] = entries with position < 256 c, from
 // per-warp SMEM chunk counters.  Dynamic SMEM: 8 x (nchunk + 1) ints.
+// The same warp also copies its row of X into pi order (Xp[i] = X[perm[i]], the UP GEMM's TMA-loaded A operand;
+// formerly a separate permute_rows_kernel): the HBM-bound copy overlaps the latency-bound gate-list reads.
+constexpr int GL_COPY_U = 4;  // 16-byte X loads in flight per lane
 __global__ void __launch_bounds__(256) union_gate_list_kernel(const uint32_t* __restrict__ tw, int M, int N, int T,
-                                                              int C, UnionMeta um, const int32_t* __restrict__ perm) {
+                                                              int C, UnionMeta um, const int32_t* __restrict__ perm,
+                                                              const uint4* __restrict__ X, int K8,
+                                                              uint4* __restrict__ Xp) {
     extern __shared__ int32_t gl_smem[];
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -339,6 +344,24 @@ __global__ void __launch_bounds__(256) union_gate_list_kernel(const uint32_t* __
     const uint32_t* msk = um.umask + static_cast<int64_t>(b) * NW;
     const int32_t* wof = um.uwoff + static_cast<int64_t>(b) * NW;
     uint32_t* gl = um.glist + i * um.lmax;
+    const int64_t src_row = i < M ? static_cast<int64_t>(__ldg(perm + i)) : -1;
+    if (src_row >= 0 && Xp) {
+        const uint4* src = X + src_row * K8;
+        uint4* dst = Xp + i * K8;
+        for (int c0 = 0; c0 < K8; c0 += 32 * GL_COPY_U) {
+            uint4 v[GL_COPY_U];
+#pragma unroll
+            for (int u = 0; u < GL_COPY_U; ++u) {
+                const int c = c0 + 32 * u + lane;
+                if (c < K8) v[u] = __ldcs(src + c);
+            }
+#pragma unroll
+            for (int u = 0; u < GL_COPY_U; ++u) {
+                const int c = c0 + 32 * u + lane;
+                if (c < K8) dst[c] = v[u];
+            }
+        }
+    }
     const bool dense = __ldg(um.udense + b) != 0;  // identity union: the UP epilogue reads the TwELL directly
     if (dense) return;
     auto emit = [&](uint32_t w, int idx) {
@@ -348,7 +371,7 @@ __global__ void __launch_bounds__(256) union_gate_list_kernel(const uint32_t* __
         atomicAdd(&cc[j >> 8], 1);
     };
     if (i < M) {
-        const uint32_t* row = tw + static_cast<int64_t>(__ldg(perm + i)) * RW;
+        const uint32_t* row = tw + src_row * RW;
         // lane per tile (ascending): measured faster here than coalesced whole-row reads (the row's
         // first-touch DRAM read happened in union_meta_kernel; these sector reads mostly hit L2)
         int base = 0;

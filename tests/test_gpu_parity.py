@@ -822,7 +822,7 @@ def test_gate_dynamic_scheduler_single_cta(sffn):
     assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("algo,expected", [("union", 7), ("gather", 2)])
+@pytest.mark.parametrize("algo,expected", [("union", 6), ("gather", 2)])
 def test_launch_count(sffn, algo, expected):
     """sffn_launch_count (what bench.py reports as gpu_launches): one union forward = gate GEMM + rank + permute
     + union metadata + gate lists + UP + DOWN; one gather forward = gate GEMM + fused up/down kernel."""
