@@ -95,7 +95,35 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
     return static_cast<uint32_t>(r * 128 + ((((c >> 3) ^ r) & 7) << 4) + ((c & 7) << 1));
 }
 
-constexpr int UG_STAGES = 4;
+// k-block of the union GEMMs.  64 (default): 128-byte K-major rows (SWIZZLE_128B), 4 stages of 48 KB.  32: 64-byte
+// rows (SWIZZLE_64B), 8 stages of 24 KB in the same shared memory (more, smaller stages in flight) — measured
+// 1.30x (UP) and 1.67x (DOWN) SLOWER on the 7B step (CUPTI, two alternating rounds): the per-stage costs (barrier
+// round trips, MMA issue, twice the gather instructions per byte) dominate; kept as a compile-time option.
+#ifndef SFFN_UG_BK
+#define SFFN_UG_BK 64
+#endif
+constexpr int UG_BK = SFFN_UG_BK;
+static_assert(UG_BK == 32 || UG_BK == 64, "union k-block is 32 or 64");
+constexpr int UG_A_BYTES = GEMM_BM * UG_BK * 2;           // A tile: 128 rows x UG_BK
+constexpr int UG_B_BYTES = 256 * UG_BK * 2;               // B tile: 256 (UP: rows, DOWN: columns) x UG_BK
+constexpr int UG_STAGE_BYTES = UG_A_BYTES + UG_B_BYTES;
+constexpr int UG_STAGES = UG_BK == 32 ? 8 : 4;
+constexpr int UG_ROWB = UG_BK * 2;                        // bytes of one K-major row segment = the swizzle span
+// K-major operand descriptor for the UG_BK layout: SWIZZLE_64B (8-row atoms of 512 B, layout type 4) or
+// SWIZZLE_128B (8-row atoms of 1 KB, layout type 2); LBO unused for swizzled K-major
+__device__ __forceinline__ uint64_t umma_desc_ug(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>((8 * UG_ROWB) >> 4) << 32;  // SBO: 8 rows
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(UG_BK == 32 ? 4 : 2) << 61;
+    return d;
+}
+// 16-byte chunk c of K-major row r in the UG_BK swizzled layout (TMA SWIZZLE_64B / 128B pattern)
+__device__ __forceinline__ uint32_t ug_kmajor_off(int r, int c) {
+    return static_cast<uint32_t>(r * UG_ROWB + ((c ^ (UG_BK == 32 ? ((r >> 1) & 3) : (r & 7))) << 4));
+}
 constexpr int UG_GPRE = 8;  // UP epilogue: gate entries per row prefetched before the accumulator wait
 #ifndef UG_NGW
 #define UG_NGW 8
@@ -104,7 +132,7 @@ constexpr int UG_GW = UG_NGW;                  // gather producer warps (8..8+UG
 constexpr int UG_THREADS = 256 + 32 * UG_GW;   // warps 0-7 as gemm_tc + gather producer warps
 constexpr int UG_GATHER = 32 * UG_GW;
 constexpr int UG_EWB = 8192;  // epilogue staging per warp
-constexpr int UG_SMEM = 1024 + UG_STAGES * GEMM_STAGE_BYTES + 4 * UG_EWB + 1024;
+constexpr int UG_SMEM = 1024 + UG_STAGES * UG_STAGE_BYTES + 4 * UG_EWB + 1024;
 constexpr int UG_RING = 8;       // tile-scheduler ring depth
 constexpr int UG_READERS = UG_GW + 5;  // gather warps + MMA thread + 4 epilogue warps
 
@@ -116,8 +144,8 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stA = smem;
-    uint8_t* stB = smem + S * GEMM_A_BYTES;
-    uint8_t* epi = stB + S * GEMM_B_BYTES;
+    uint8_t* stB = smem + S * UG_A_BYTES;
+    uint8_t* epi = stB + S * UG_B_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * UG_EWB);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
@@ -133,7 +161,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     const int N = args.N;
     const int NB = args.NB;
     const int num_tiles = UP ? __ldg(args.um.chunk_off) : NB * args.NJ;
-    const int nk_up = (args.K + GEMM_BK - 1) / GEMM_BK;
+    const int nk_up = (args.K + UG_BK - 1) / UG_BK;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmA);
@@ -213,23 +241,23 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 if (tile < 0) break;
                 int b, cj, len;
                 tile_info(tile, b, cj, len);
-                const int nk = UP ? nk_up : len / GEMM_BK;
+                const int nk = UP ? nk_up : len / UG_BK;
                 // dense block (union forced to all N units, union_meta_kernel): B by TMA tiles, no gathers
                 const bool dense = __ldg(args.um.udense + b) != 0;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], dense ? GEMM_STAGE_BYTES : GEMM_A_BYTES);
-                    tma_load_2d(stA + stage * GEMM_A_BYTES, &tmA, &full[stage], kb * GEMM_BK, b * GEMM_BM,
+                    mbar_arrive_expect_tx(&full[stage], dense ? UG_STAGE_BYTES : UG_A_BYTES);
+                    tma_load_2d(stA + stage * UG_A_BYTES, &tmA, &full[stage], kb * UG_BK, b * GEMM_BM,
                                 policy_evict_last());
                     if (dense) {
-                        uint8_t* bdst = stB + stage * GEMM_B_BYTES;
-                        if (UP) {  // W_u rows [256 cj, 256 cj + 256), k-slice kb: K-major box {64, 256}
-                            tma_load_2d(bdst, &tmB, &full[stage], kb * GEMM_BK, 256 * cj, policy_evict_last());
-                        } else {   // W_d rows [64 kb, 64 kb + 64), columns 256 cj + 64 q: four MN-major {64, 64} atoms
+                        uint8_t* bdst = stB + stage * UG_B_BYTES;
+                        if (UP) {  // W_u rows [256 cj, 256 cj + 256), k-slice kb: K-major box {UG_BK, 256}
+                            tma_load_2d(bdst, &tmB, &full[stage], kb * UG_BK, 256 * cj, policy_evict_last());
+                        } else {   // W_d rows [UG_BK kb, +UG_BK), columns 256 cj + 64 q: four MN-major {64, UG_BK} atoms
 #pragma unroll
                             for (int q = 0; q < 4; ++q)
-                                tma_load_2d(bdst + q * 8192, &tmB, &full[stage], 256 * cj + 64 * q, kb * GEMM_BK,
-                                            policy_evict_last());
+                                tma_load_2d(bdst + q * (UG_B_BYTES / 4), &tmB, &full[stage], 256 * cj + 64 * q,
+                                            kb * UG_BK, policy_evict_last());
                         }
                     }
                     if (++stage == S) {
@@ -241,10 +269,10 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         }
     } else if (warp >= 8) {
         // ------------------------------------------------------------ B operand: gathered weight rows
-        // 8 consecutive lanes copy one 128-B row segment (16 B each), so every warp instruction moves whole
-        // 128-B lines: UP 4 rows x 128 B, DOWN one neuron row's 4 adjacent 64-column atoms (512 B).
+        // UP (K-major): LPR consecutive lanes copy one UG_ROWB-byte row segment (16 B each), RPI rows per warp
+        // instruction; DOWN (MN-major, 128-byte swizzle): one neuron row's 4 adjacent 64-column atoms (512 B) per
+        // warp instruction.  Every warp instruction moves whole row segments.
         const int gw = warp - 8;          // 0..UG_GW-1
-        const int c8 = lane & 7, sub = lane >> 3;
         int stage = 0;
         uint32_t phase = 0;
         int ridx = 0;
@@ -257,7 +285,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             const int32_t* ul = args.um.ulist + static_cast<int64_t>(b) * N;
             if (__ldg(args.um.udense + b) != 0) {
                 // dense block: B comes by TMA (warp 0); keep the per-stage arrivals of the full barrier
-                const int nk = UP ? nk_up : len / GEMM_BK;
+                const int nk = UP ? nk_up : len / UG_BK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
                     cp_async_arrive_noinc(&full[stage]);
@@ -267,23 +295,25 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     }
                 }
             } else if (UP) {
-                // pass i covers chunk rows 4 UG_GW i + 4 gw + sub
-                constexpr int NP = 64 / UG_GW;
+                constexpr int LPR = UG_BK / 8;             // lanes per row segment
+                constexpr int RPI = 32 / LPR;              // rows per warp instruction
+                constexpr int NP = 256 / (RPI * UG_GW);    // instructions per warp per stage
+                const int cl = lane % LPR, sub = lane / LPR;
                 int nidx[NP];
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
-                    const int r = 4 * UG_GW * i + 4 * gw + sub;
+                    const int r = RPI * UG_GW * i + RPI * gw + sub;
                     nidx[i] = r < len ? __ldg(ul + 256 * cj + r) : -1;
                 }
                 for (int kb = 0; kb < nk_up; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
-                    const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES);
+                    const uint32_t dst = smem_u32(stB + stage * UG_B_BYTES);
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
-                        const int r = 4 * UG_GW * i + 4 * gw + sub;
+                        const int r = RPI * UG_GW * i + RPI * gw + sub;
                         if (nidx[i] >= 0)
-                            cp_async16(dst + r * 128 + ((c8 ^ (r & 7)) << 4),
-                                       args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * GEMM_BK + 8 * c8, 16);
+                            cp_async16(dst + ug_kmajor_off(r, cl),
+                                       args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * UG_BK + 8 * cl, 16);
                     }
                     cp_async_arrive_noinc(&full[stage]);
                     if (++stage == S) {
@@ -293,24 +323,27 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 }
             } else {
                 // pass i covers k-block row r = UG_GW i + gw, MN atom a = sub (columns 256 cj + 64 a + 8 c8)
-                constexpr int NP = 64 / UG_GW;
-                const int nk = len / GEMM_BK;
+                constexpr int NP = UG_BK / UG_GW;
+                const int c8 = lane & 7, sub = lane >> 3;
+                const int nk = len / UG_BK;
                 const int col = cj * 256 + sub * 64 + 8 * c8;
                 const bool in = col < args.K;
-                // union indices two k-blocks ahead (an L2 round trip is about one k-block of MMA time)
+                // union indices two k-blocks ahead (an L2 round trip is about one k-block of MMA time), issued before
+                // the stage wait so their latency overlaps it.  (A compile-time register ring 2-4 k-blocks ahead,
+                // which never copies a pending load, measured 8% slower: DOWN 1195 vs 1105 us, CUPTI, two rounds.)
                 int nidx[NP], n1[NP];
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
                     nidx[i] = __ldg(ul + UG_GW * i + gw);
-                    n1[i] = __ldg(ul + (nk > 1 ? GEMM_BK : 0) + UG_GW * i + gw);
+                    n1[i] = __ldg(ul + (nk > 1 ? UG_BK : 0) + UG_GW * i + gw);
                 }
                 for (int kb = 0; kb < nk; ++kb) {
                     int nxt[NP];
                     const int kn = kb + 2 < nk ? kb + 2 : nk - 1;
 #pragma unroll
-                    for (int i = 0; i < NP; ++i) nxt[i] = __ldg(ul + kn * GEMM_BK + UG_GW * i + gw);
+                    for (int i = 0; i < NP; ++i) nxt[i] = __ldg(ul + kn * UG_BK + UG_GW * i + gw);
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);
-                    const uint32_t dst = smem_u32(stB + stage * GEMM_B_BYTES) + sub * 8192;
+                    const uint32_t dst = smem_u32(stB + stage * UG_B_BYTES) + sub * (UG_B_BYTES / 4);
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
                         const int r = UG_GW * i + gw;
@@ -344,7 +377,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 if (tile < 0) break;
                 int b, cj, len;
                 tile_info(tile, b, cj, len);
-                const int nk = UP ? nk_up : len / GEMM_BK;
+                const int nk = UP ? nk_up : len / UG_BK;
                 const uint32_t idesc = UP ? umma_idesc_bf16(GEMM_BM, len) : (umma_idesc_bf16(GEMM_BM, 256) | (1u << 16));
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -355,12 +388,14 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                     mbar_wait_relaxed(&full[stage], phase);
                     fence_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads (async proxy)
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(stA + stage * GEMM_A_BYTES);
-                    const uint32_t b0 = smem_u32(stB + stage * GEMM_B_BYTES);
+                    const uint32_t a0 = smem_u32(stA + stage * UG_A_BYTES);
+                    const uint32_t b0 = smem_u32(stB + stage * UG_B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < GEMM_BK / 16; ++k) {
-                        const uint64_t bd = UP ? umma_desc_sw128(b0 + k * 32) : umma_desc_sw128_mn(b0 + k * 2048, 8192, 1024);
-                        umma_f16(d, umma_desc_sw128(a0 + k * 32), bd, idesc, (kb | k) != 0);
+                    for (int k = 0; k < UG_BK / 16; ++k) {
+                        // DOWN B: MN-major atoms of UG_BK k-rows x 128 B (LBO = atom size), 8-row groups 1 KB apart
+                        const uint64_t bd = UP ? umma_desc_ug(b0 + k * 32)
+                                               : umma_desc_sw128_mn(b0 + k * 2048, UG_B_BYTES / 4, 1024);
+                        umma_f16(d, umma_desc_ug(a0 + k * 32), bd, idesc, (kb | k) != 0);
                     }
                     umma_commit(&empty[stage]);
                     if (++stage == S) {

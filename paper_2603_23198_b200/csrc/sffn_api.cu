@@ -381,15 +381,16 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         }
     }
 
+    // operand maps: the single-CTA union GEMMs use k-blocks of UG_BK (SWIZZLE_64B K-major boxes at 32), the CTA-pair
+    // kernels k-blocks of 64 (SWIZZLE_128B)
+    const int kbk = BR == 256 ? GEMM_BK : UG_BK;
+    const CUtensorMapSwizzle ksw = kbk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
     CUtensorMap tx, twu, thc_st, thc_ld, twd, ty;
-    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M > 0 ? M : 1, GEMM_BK, GEMM_BM,
-                 CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, GEMM_BK, N >= 256 ? 256 : 64,
-                 CU_TENSOR_MAP_SWIZZLE_128B) ||
+    if (!tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xp, K, M > 0 ? M : 1, kbk, GEMM_BM, ksw) ||
+        !tmap_2d(&twu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wu, K, N, kbk, N >= 256 ? 256 : 64, ksw) ||
         !tmap_2d(&thc_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * BR, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * BR, GEMM_BK, GEMM_BM,
-                 CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wd, K, N, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&thc_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hc, N, NB * BR, kbk, GEMM_BM, ksw) ||
+        !tmap_2d(&twd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wd, K, N, 64, kbk, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y, K, M, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
         return SFFN_ERR_CUDA;
     UnionArgs ua{};
