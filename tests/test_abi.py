@@ -87,7 +87,7 @@ def test_product_path_does_not_import_oracle():
 def test_host_chunk_plan(lib, M, R):
     """sffn_forward_host's chunk schedule: covers M exactly, no chunk above the stage slot (chunk_rows rounded
     to the rows actually staged), chunk starts on the 2048-row permutation windows when chunk_rows allows it,
-    and ramps (short first and last chunks) when there is room."""
+    and ramps (short first and last chunks: the PCIe pipeline's fill and drain) when there is room."""
     from paper_2603_23198_b200 import sffn
     v = sffn.forward_host_chunks(M, R)
     rows = R if R < M else (M + 127) // 128 * 128

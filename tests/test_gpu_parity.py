@@ -439,18 +439,24 @@ def test_fp32_forward_gaussian(sffn):
 
 
 @pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("M,chunk", [(5000, 2048), (20000, 8192)])
+@pytest.mark.parametrize("M,chunk", [(5000, 2048), (20000, 8192), (33000, 4096)])
 def test_forward_host_pipeline(sffn, algo, M, chunk):
-    """Host-buffer forward (chunked copy/compute overlap; 20000/8192 takes the ramped schedule
-    2048, 4096, 6144, 4096, 3616) == device forward, bit-identical (chunks start on the 2048-row
-    permutation windows)."""
+    """Host-buffer forward (chunked copy/compute overlap; ramped chunk plans, e.g. 20000/8192 -> 2048, 4096, 6144,
+    4096, 3616): every chunk is its own forward, so the result equals the concatenation of per-chunk device forwards
+    bit for bit (and, chunks starting on the 2048-row pi windows, one unchunked forward), and every row is within
+    the per-row Y bar of Eq.3 (oracle)."""
     cfg = synth.CONFIGS["1B"].replace(M=M, K=256, N=1024, Kb=16, sparsity=0.97)
     X, Wg, Wu, Wd = inputs(cfg)
-    ref = sffn.forward(to_dev(X), to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo)
+    Xd, Wgd, Wud, Wdd = (to_dev(a) for a in (X, Wg, Wu, Wd))
+    plan = sffn.forward_host_chunks(M, chunk)
+    assert sum(plan) == M and max(plan) <= chunk and (len(plan) == 1 or plan[0] < chunk)
+    ref = torch.cat([sffn.forward(Xd[r0:r0 + m].contiguous(), Wgd, Wud, Wdd, 256, 8, algo=algo)
+                     for r0, m in zip(np.cumsum([0] + plan[:-1]), plan)])
     xh = torch.from_numpy(X.view(np.int16)).view(torch.bfloat16).pin_memory()
-    yh = sffn.forward_host(xh, to_dev(Wg), to_dev(Wu), to_dev(Wd), 256, 8, algo=algo, chunk_rows=chunk)
-    torch.cuda.synchronize()
+    yh = sffn.forward_host(xh, Wgd, Wud, Wdd, 256, 8, algo=algo, chunk_rows=chunk)
     assert torch.equal(yh.view(torch.int16), ref.cpu().view(torch.int16))
+    wo, counts, n_ov, A = oracle.pack_from_inputs(X, Wg, 256, 8, matmul=True)
+    assert_y(bf16_np(yh), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8))
 
 
 # ----------------------------------------------------------------- non-gated variant (App.C, NEXT-2)
