@@ -44,6 +44,18 @@ template <int EPI, int C>
 __host__ __device__ constexpr int gemm_epi_warp_bytes() {
     return EPI == EPI_TWELL ? 32 * (GEMM_BN / C) * 4 : (EPI == EPI_F32 ? 0 : 32 * 128 * 2);  // GLU/BF16/BF16_MN
 }
+// Epilogue warp groups: 2 for the TwELL epilogue when its staging is small (C >= 8): group g (warps 4+4g .. 7+4g)
+// drains accumulator g, i.e. every other tile, so each group has two mainloops of time per tile.  At K = 2048
+// (1B) the single group did not keep up: the MMA thread spun on the accumulator-free barrier (ncu: 633k spins)
+// and the tensor pipe was 69% active.  Other epilogues: 1 group (warps 4-7, alternating accumulators).
+template <int EPI, int C>
+__host__ __device__ constexpr int gemm_epi_groups() {
+    return (EPI == EPI_TWELL && gemm_epi_warp_bytes<EPI, C>() <= 4096) ? 2 : 1;
+}
+template <int EPI, int C>
+__host__ __device__ constexpr int gemm_threads() {
+    return 128 + 128 * gemm_epi_groups<EPI, C>();
+}
 // PAIR = 2: CTA-pair (cluster of 2, cta_group::2) variant — a 256 x 256 output tile per pair, each CTA loading
 // its own 128 A rows and HALF of the 256 B rows (128), the leader issuing M=256 MMAs that read both CTAs' SMEM.
 // Per SM this cuts the operand stream from 48 KB to 32 KB per k-block (same MMA work).
@@ -53,13 +65,16 @@ __host__ __device__ constexpr int gemm_stage_bytes() {
 }
 template <int EPI, int C, int PAIR = 1>
 __host__ __device__ constexpr int gemm_stages() {
-    return (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / gemm_stage_bytes<PAIR>() > 6
+    return (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_groups<EPI, C>() * gemm_epi_warp_bytes<EPI, C>()) /
+                       gemm_stage_bytes<PAIR>() > 6
                ? 6
-               : (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_warp_bytes<EPI, C>()) / gemm_stage_bytes<PAIR>();
+               : (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_groups<EPI, C>() * gemm_epi_warp_bytes<EPI, C>()) /
+                     gemm_stage_bytes<PAIR>();
 }
 template <int EPI, int C, int PAIR = 1>
 __host__ __device__ constexpr int gemm_smem_bytes() {
-    return 1024 + gemm_stages<EPI, C, PAIR>() * gemm_stage_bytes<PAIR>() + 4 * gemm_epi_warp_bytes<EPI, C>() + 256;
+    return 1024 + gemm_stages<EPI, C, PAIR>() * gemm_stage_bytes<PAIR>() +
+           4 * gemm_epi_groups<EPI, C>() * gemm_epi_warp_bytes<EPI, C>() + 256;
 }
 
 struct GemmArgs {
@@ -100,7 +115,7 @@ __device__ __forceinline__ void gemm_tile_coords(int tile, int num_m, int num_n,
 }
 
 template <int EPI, int C, int PAIR = 1>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmOut,
                    const GemmArgs args) {
@@ -110,6 +125,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     constexpr int STAGE_BYTES = gemm_stage_bytes<PAIR>();
     constexpr int PM = GEMM_BM * PAIR;            // output rows per (pair) tile
     constexpr int GROUP = GEMM_GROUP_M / PAIR;
+    constexpr int NEG = gemm_epi_groups<EPI, C>();  // epilogue warp groups
     static_assert(S >= 2, "not enough shared memory for a 2-stage ring");
     static_assert(PAIR == 1 || PAIR == 2, "PAIR is 1 or 2");
     static_assert(PAIR == 1 || EPI == EPI_TWELL || EPI == EPI_F32 || EPI == EPI_BF16 || EPI == EPI_GLU,
@@ -120,7 +136,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* stA = smem;
     uint8_t* stB = smem + S * GEMM_A_BYTES;
     uint8_t* epi = stB + S * B_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * EWB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(epi + 4 * NEG * EWB);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
@@ -152,8 +168,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         for (int i = 0; i < GT_RING; ++i) {
             mbar_init(&sfull[i], 1);
-            // readers: MMA thread + 4 epilogue warps per CTA (+ the peer's producer in pair mode)
-            mbar_init(&sempty[i], PAIR == 2 ? 10 : 5);
+            // readers: MMA thread + the epilogue warps of every CTA (+ the peer's producer in pair mode)
+            mbar_init(&sempty[i], PAIR == 2 ? 2 + 8 * NEG : 1 + 4 * NEG);
         }
         fence_mbar_init();
     }
@@ -308,9 +324,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue
-        const int ew = warp - 4;  // TMEM lane quarter accessible to this warp (warp % 4)
-        uint8_t* stg = epi + ew * EWB;
-        int acc = 0;
+        const int ew = (warp - 4) & 3;   // TMEM lane quarter accessible to this warp (warp % 4)
+        const int eg = (warp - 4) >> 2;  // epilogue group: with NEG == 2, group g drains accumulator g
+        uint8_t* stg = epi + (warp - 4) * EWB;
+        int acc = NEG == 2 ? eg : 0;
         uint32_t acc_phase = 0;
         const uint32_t tempty_leader = PAIR == 2 ? mapa_shared(tempty, 0) : 0u;
         auto release_acc = [&](int a) {  // lane 0: this warp is done reading accumulator a
@@ -322,6 +339,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int it = 0;; ++it) {
             const int tile = next_tile(it, ridx, rphase, lane == 0);
             if (tile < 0) break;
+            if (NEG == 2 && (it & 1) != eg) continue;  // the other group's tile (accumulator)
             int mb, nb;
             gemm_tile_coords<GROUP>(tile, num_m, args.num_n, mb, nb);
             const int row0 = mb * PM + static_cast<int>(rank) * GEMM_BM + ew * 32;
@@ -368,17 +386,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint32_t mask = 0;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) mask |= (__uint_as_float(v[i]) > 0.0f ? 1u : 0u) << i;
-                    if (mask) {
+                    // columns positive in ANY of the warp's 32 rows (~10 of 32 at 1% density): a warp-uniform
+                    // branch per column skips the rest, so the compaction costs ~ the positives, not 32 columns
+                    // (at K = 2048 the epilogue, not the mainloop, bounded the kernel: tensor pipe 69%, ncu 1B)
+                    const uint32_t any = __reduce_or_sync(0xffffffffu, mask);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
+                    for (int i = 0; i < 32; ++i) {
+                        if ((any >> i) & 1u) {
                             const int slot = z + __popc(mask & ((1u << i) - 1u));
                             if (((mask >> i) & 1u) && slot < cap) {
                                 const uint32_t bf = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(v[i])));
                                 *sword(tbase + 1 + slot) = static_cast<uint32_t>(col_base + tcol + i) | (bf << 16);
                             }
                         }
-                        z += __popc(mask);
                     }
+                    z += __popc(mask);
                     if ((tcol + 32) % T == 0) {
                         *sword(tbase) = static_cast<uint32_t>(z);  // Alg.1 line 17: true count
                         if (z > cap && row_ok && args.overflow) atomicAdd(args.overflow, 1u);
@@ -471,7 +493,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     }
                 }
             }
-            if (++acc == 2) {
+            if (NEG == 2) {
+                acc_phase ^= 1;
+            } else if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }

@@ -113,12 +113,12 @@ int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b
     DevInfo d = dev_info();
     if constexpr (PAIR == 1) {
         const int grid = tiles < d.sms ? tiles : d.sms;
-        { kern<<<grid, GEMM_THREADS, smem, st>>>(a, b, b2, o, args); note_launch(); }
+        { kern<<<grid, gemm_threads<EPI, C>(), smem, st>>>(a, b, b2, o, args); note_launch(); }
     } else {
         const int pairs = tiles < d.sms / 2 ? tiles : d.sms / 2;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * pairs);
-        cfg.blockDim = dim3(GEMM_THREADS);
+        cfg.blockDim = dim3(gemm_threads<EPI, C>());
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute at[1];
