@@ -1,0 +1,232 @@
+// Microbenchmark: per-SM operand feed of the union GEMMs on B200, without the MMAs.
+// One persistent CTA per SM walks "tiles" of 64 k-blocks.  Per k-block (one ring stage):
+//   A: a 128-row x 64-col bf16 tile of X by TMA (128B swizzle, 16 KB), the same token block for all k-blocks of a tile
+//   B: `brows` gathered 128-byte weight-row segments (row = a random unit of the tile, k-slice kb):
+//      bmode 0: cp.async.cg 16 B, 8 lanes per row segment (the union kernels' producer mapping)
+//      bmode 1: one TMA 2-D box {64, 1} per row (128B swizzle by address), issued by the gather warps' lanes
+//      bmode 2: ld.global.v4 to registers + st.shared (LSU round trip) with the stage's mbarrier arrive
+// A consumer thread waits for each stage, spins `delay` SM cycles (the MMA time it would take), frees the stage.
+// Prints achieved bytes per SM cycle and the stage time.  Not part of the library.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/exp_feed tools/exp_feed.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <vector>
+#include <random>
+#include <algorithm>
+#include "../paper_2603_23198_b200/csrc/ptx.cuh"
+
+using namespace sffn;
+constexpr int S = 4, KB = 64, ABYTES = 128 * KB * 2, BMAX = 256 * 128;
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int r) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(r)
+        : "memory");
+}
+
+struct P {
+    int K, ntiles, abytes, brows, bmode, delay, nw;
+    const uint16_t* W;
+    const int* units;   // [ntiles, 256]
+    const int* blocks;  // [ntiles]
+    int* counter;
+    unsigned long long* cycles;
+};
+
+__global__ void __launch_bounds__(32 * 10, 1) k_feed(const __grid_constant__ CUtensorMap tX,
+                                                      const __grid_constant__ CUtensorMap tW, const P p) {
+    extern __shared__ uint8_t sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stA = sm;
+    uint8_t* stB = sm + S * ABYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stB + S * BMAX);
+    uint64_t* empty = full + S;
+    __shared__ int tiles[1024];
+    __shared__ int ntl;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NW = p.nw;
+    const bool lsu_b = p.brows > 0 && p.bmode != 1;
+    if (threadIdx.x == 0) {
+        int n = 0;
+        for (;;) {
+            const int t = atomicAdd(p.counter, 1);
+            if (t >= p.ntiles || n == 1024) break;
+            tiles[n++] = t;
+        }
+        ntl = n;
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1 + (lsu_b ? NW * 32 : 0));
+            mbar_init(&empty[i], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const long long t0 = clock64();
+    const int nt = ntl;
+    if (warp == 0) {
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < nt; ++i) {
+                const int b = p.blocks[tiles[i]];
+                for (int kb = 0; kb < p.K / KB; ++kb) {
+                    mbar_wait_relaxed(&empty[st], ph ^ 1);
+                    const uint32_t tx = p.abytes + (p.bmode == 1 ? p.brows * 128 : 0);
+                    if (tx) mbar_arrive_expect_tx(&full[st], tx); else mbar_arrive(&full[st]);
+                    if (p.abytes) tma_load_2d(stA + st * ABYTES, &tX, &full[st], kb * KB, b * 128, policy_evict_last());
+                    if (++st == S) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < nt; ++i)
+                for (int kb = 0; kb < p.K / KB; ++kb) {
+                    mbar_wait_relaxed(&full[st], ph);
+                    if (p.delay) {
+                        const long long c = clock64();
+                        while (clock64() - c < p.delay) {}
+                    }
+                    mbar_arrive(&empty[st]);
+                    if (++st == S) { st = 0; ph ^= 1; }
+                }
+        }
+    } else if (warp >= 2 && warp < 2 + NW && p.brows > 0) {
+        const int gw = warp - 2;
+        int st = 0;
+        uint32_t ph = 0;
+        for (int i = 0; i < nt; ++i) {
+            const int* u = p.units + static_cast<int64_t>(tiles[i]) * 256;
+            for (int kb = 0; kb < p.K / KB; ++kb) {
+                mbar_wait_relaxed(&empty[st], ph ^ 1);
+                const uint32_t dst = smem_u32(stB + st * BMAX);
+                if (p.bmode == 0) {
+                    const int cl = lane & 7, sub = lane >> 3;
+                    for (int r = 4 * gw + sub; r < p.brows; r += 4 * NW) {
+                        const int n = __ldg(u + r);
+                        cp16(dst + r * 128 + ((cl ^ (r & 7)) << 4), p.W + static_cast<int64_t>(n) * p.K + kb * KB + 8 * cl);
+                    }
+                    cp_arrive(&full[st]);
+                } else if (p.bmode == 1) {
+                    for (int r = 32 * gw + lane; r < p.brows; r += 32 * NW)
+                        tma_row(stB + st * BMAX + r * 128, &tW, &full[st], kb * KB, __ldg(u + r));
+                } else {
+                    const int cl = lane & 7, sub = lane >> 3;
+                    for (int r = 4 * gw + sub; r < p.brows; r += 4 * NW) {
+                        const int n = __ldg(u + r);
+                        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.W + static_cast<int64_t>(n) * p.K + kb * KB + 8 * cl));
+                        *reinterpret_cast<uint4*>(stB + st * BMAX + r * 128 + ((cl ^ (r & 7)) << 4)) = v;
+                    }
+                    mbar_arrive(&full[st]);
+                }
+                if (++st == S) { st = 0; ph ^= 1; }
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(p.cycles, static_cast<unsigned long long>(clock64() - t0));
+}
+
+typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                        const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static void tmap(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    cuuint64_t d[2] = {inner, outer}, s[1] = {inner * 2};
+    cuuint32_t b[2] = {bi, bo}, e[2] = {1, 1};
+    CUresult r = reinterpret_cast<Enc>(f)(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("tmap failed %d\n", r); exit(1); }
+}
+
+int main(int argc, char** argv) {
+    const int M = 32768, K = 4096, N = 14336;
+    const int ntiles = 148 * 12;
+    uint16_t *X, *W;
+    cudaMalloc(&X, size_t(M) * K * 2);
+    cudaMalloc(&W, size_t(N) * K * 2);
+    cudaMemset(X, 0, size_t(M) * K * 2);
+    cudaMemset(W, 0, size_t(N) * K * 2);
+    std::mt19937 rng(1);
+    // unit popularity: a 0.365-N "union" per block drawn from a lognormal-weighted pool, 256 units per tile
+    std::vector<int> units(size_t(ntiles) * 256), blocks(ntiles);
+    for (int t = 0; t < ntiles; ++t) {
+        blocks[t] = t / 20 % 256;
+        std::vector<int> u(N);
+        for (int i = 0; i < N; ++i) u[i] = i;
+        std::shuffle(u.begin(), u.end(), rng);
+        std::sort(u.begin(), u.begin() + 256);
+        std::copy(u.begin(), u.begin() + 256, units.begin() + size_t(t) * 256);
+    }
+    int *du, *db, *cnt;
+    unsigned long long* cyc;
+    cudaMalloc(&du, units.size() * 4);
+    cudaMalloc(&db, blocks.size() * 4);
+    cudaMalloc(&cnt, 4);
+    cudaMalloc(&cyc, 8);
+    cudaMemcpy(du, units.data(), units.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(db, blocks.data(), blocks.size() * 4, cudaMemcpyHostToDevice);
+    CUtensorMap tX, tW;
+    tmap(&tX, X, K, M, 64, 128);
+    tmap(&tW, W, K, N, 64, 1);
+    const int smem = 1024 + S * (ABYTES + BMAX) + 256;
+    cudaFuncSetAttribute(k_feed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    struct Cfg { const char* name; int abytes, brows, bmode, delay, nw; };
+    std::vector<Cfg> cfgs = {
+        {"A only (TMA 16 KB)", ABYTES, 0, 0, 0, 8},
+        {"B 256 rows cp.async (32 KB), 8 warps", 0, 256, 0, 0, 8},
+        {"B 256 rows cp.async, 4 warps", 0, 256, 0, 0, 4},
+        {"B 256 rows ld+st (LSU), 8 warps", 0, 256, 2, 0, 8},
+        {"B 256 rows TMA box{64,1}, 8 warps", 0, 256, 1, 0, 8},
+        {"A + B256 cp.async (48 KB)", ABYTES, 256, 0, 0, 8},
+        {"A + B128 cp.async (32 KB)", ABYTES, 128, 0, 0, 8},
+        {"A + B256 cp.async, delay 512", ABYTES, 256, 0, 512, 8},
+        {"A + B128 cp.async, delay 512", ABYTES, 128, 0, 512, 8},
+        {"A only, delay 512", ABYTES, 0, 0, 512, 8},
+        {"B256 cp.async only, delay 512", 0, 256, 0, 512, 8},
+    };
+    for (auto& c : cfgs) {
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaMemset(cnt, 0, 4);
+            cudaMemset(cyc, 0, 8);
+            P p{K, ntiles, c.abytes, c.brows, c.bmode, c.delay, c.nw, W, du, db, cnt, cyc};
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0);
+            k_feed<<<sms, 32 * 10, smem>>>(tX, tW, p);
+            cudaEventRecord(e1);
+            cudaError_t err = cudaEventSynchronize(e1);
+            if (err != cudaSuccess) { printf("%s: %s\n", c.name, cudaGetErrorString(err)); return 1; }
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            unsigned long long cy;
+            cudaMemcpy(&cy, cyc, 8, cudaMemcpyDeviceToHost);
+            const double stages = double(ntiles) * (K / KB);
+            const double bytes = stages * (c.abytes + c.brows * 128.0);
+            const double avg_cyc = double(cy) / sms;  // cycles per CTA
+            if (rep == 1)
+                printf("%-40s %8.3f ms  %7.1f TB/s  %6.1f B/cyc/SM  %6.0f cyc/stage  (clk %.0f MHz)\n", c.name, ms,
+                       bytes / ms / 1e9, bytes / sms / avg_cyc, avg_cyc / (stages / sms), avg_cyc / ms / 1e3);
+        }
+    }
+    return 0;
+}
