@@ -36,7 +36,7 @@ __device__ __forceinline__ void tma_row(void* dst, const CUtensorMap* m, uint64_
 }
 
 struct P {
-    int K, ntiles, abytes, brows, bmode, delay, nw;
+    int K, ntiles, abytes, brows, bmode, delay, nw, tsplit;
     const uint16_t* W;
     const int* units;   // [ntiles, 256]
     const int* blocks;  // [ntiles]
@@ -44,7 +44,7 @@ struct P {
     unsigned long long* cycles;
 };
 
-__global__ void __launch_bounds__(32 * 10, 1) k_feed(const __grid_constant__ CUtensorMap tX,
+__global__ void __launch_bounds__(32 * 26, 1) k_feed(const __grid_constant__ CUtensorMap tX,
                                                       const __grid_constant__ CUtensorMap tW, const P p) {
     extern __shared__ uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -57,13 +57,11 @@ __global__ void __launch_bounds__(32 * 10, 1) k_feed(const __grid_constant__ CUt
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NW = p.nw;
     const bool lsu_b = p.brows > 0 && p.bmode != 1;
+    const int tma_rows = p.bmode == 1 ? p.brows : (p.bmode == 3 ? p.brows - p.tsplit : 0);
+    const int lsu_rows = p.bmode == 3 ? p.tsplit : p.brows;
     if (threadIdx.x == 0) {
         int n = 0;
-        for (;;) {
-            const int t = atomicAdd(p.counter, 1);
-            if (t >= p.ntiles || n == 1024) break;
-            tiles[n++] = t;
-        }
+        for (int t = blockIdx.x; t < p.ntiles && n < 1024; t += gridDim.x) tiles[n++] = t;  // static: balanced
         ntl = n;
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1 + (lsu_b ? NW * 32 : 0));
@@ -82,7 +80,7 @@ __global__ void __launch_bounds__(32 * 10, 1) k_feed(const __grid_constant__ CUt
                 const int b = p.blocks[tiles[i]];
                 for (int kb = 0; kb < p.K / KB; ++kb) {
                     mbar_wait_relaxed(&empty[st], ph ^ 1);
-                    const uint32_t tx = p.abytes + (p.bmode == 1 ? p.brows * 128 : 0);
+                    const uint32_t tx = p.abytes + tma_rows * 128;
                     if (tx) mbar_arrive_expect_tx(&full[st], tx); else mbar_arrive(&full[st]);
                     if (p.abytes) tma_load_2d(stA + st * ABYTES, &tX, &full[st], kb * KB, b * 128, policy_evict_last());
                     if (++st == S) { st = 0; ph ^= 1; }
@@ -113,12 +111,15 @@ __global__ void __launch_bounds__(32 * 10, 1) k_feed(const __grid_constant__ CUt
             for (int kb = 0; kb < p.K / KB; ++kb) {
                 mbar_wait_relaxed(&empty[st], ph ^ 1);
                 const uint32_t dst = smem_u32(stB + st * BMAX);
-                if (p.bmode == 0) {
+                if (p.bmode == 0 || p.bmode == 3) {
                     const int cl = lane & 7, sub = lane >> 3;
-                    for (int r = 4 * gw + sub; r < p.brows; r += 4 * NW) {
+                    for (int r = 4 * gw + sub; r < lsu_rows; r += 4 * NW) {
                         const int n = __ldg(u + r);
                         cp16(dst + r * 128 + ((cl ^ (r & 7)) << 4), p.W + static_cast<int64_t>(n) * p.K + kb * KB + 8 * cl);
                     }
+                    if (p.bmode == 3)
+                        for (int r = lsu_rows + 32 * gw + lane; r < p.brows; r += 32 * NW)
+                            tma_row(stB + st * BMAX + r * 128, &tW, &full[st], kb * KB, __ldg(u + r));
                     cp_arrive(&full[st]);
                 } else if (p.bmode == 1) {
                     for (int r = 32 * gw + lane; r < p.brows; r += 32 * NW)
@@ -157,7 +158,7 @@ static void tmap(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint
 
 int main(int argc, char** argv) {
     const int M = 32768, K = 4096, N = 14336;
-    const int ntiles = 148 * 12;
+    const int ntiles = 148 * 24;
     uint16_t *X, *W;
     cudaMalloc(&X, size_t(M) * K * 2);
     cudaMalloc(&W, size_t(N) * K * 2);
@@ -166,13 +167,18 @@ int main(int argc, char** argv) {
     std::mt19937 rng(1);
     // unit popularity: a 0.365-N "union" per block drawn from a lognormal-weighted pool, 256 units per tile
     std::vector<int> units(size_t(ntiles) * 256), blocks(ntiles);
+    // lognormal (sigma 1) unit popularity: concurrently running tiles share hot units, as the real unions do
+    std::lognormal_distribution<double> ln(0.0, 1.0);
+    std::vector<double> wgt(N);
+    for (auto& w : wgt) w = ln(rng);
+    std::discrete_distribution<int> pick(wgt.begin(), wgt.end());
     for (int t = 0; t < ntiles; ++t) {
         blocks[t] = t / 20 % 256;
-        std::vector<int> u(N);
-        for (int i = 0; i < N; ++i) u[i] = i;
-        std::shuffle(u.begin(), u.end(), rng);
-        std::sort(u.begin(), u.begin() + 256);
-        std::copy(u.begin(), u.begin() + 256, units.begin() + size_t(t) * 256);
+        std::vector<char> used(N, 0);
+        std::vector<int> u;
+        while ((int)u.size() < 256) { const int n = pick(rng); if (!used[n]) { used[n] = 1; u.push_back(n); } }
+        std::sort(u.begin(), u.end());
+        std::copy(u.begin(), u.end(), units.begin() + size_t(t) * 256);
     }
     int *du, *db, *cnt;
     unsigned long long* cyc;
@@ -189,30 +195,44 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(k_feed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    struct Cfg { const char* name; int abytes, brows, bmode, delay, nw; };
+    struct Cfg { const char* name; int abytes, brows, bmode, delay, nw, tsplit, grid = 0; };
     std::vector<Cfg> cfgs = {
-        {"A only (TMA 16 KB)", ABYTES, 0, 0, 0, 8},
-        {"B 256 rows cp.async (32 KB), 8 warps", 0, 256, 0, 0, 8},
-        {"B 256 rows cp.async, 4 warps", 0, 256, 0, 0, 4},
-        {"B 256 rows ld+st (LSU), 8 warps", 0, 256, 2, 0, 8},
-        {"B 256 rows TMA box{64,1}, 8 warps", 0, 256, 1, 0, 8},
-        {"A + B256 cp.async (48 KB)", ABYTES, 256, 0, 0, 8},
-        {"A + B128 cp.async (32 KB)", ABYTES, 128, 0, 0, 8},
-        {"A + B256 cp.async, delay 512", ABYTES, 256, 0, 512, 8},
-        {"A + B128 cp.async, delay 512", ABYTES, 128, 0, 512, 8},
-        {"A only, delay 512", ABYTES, 0, 0, 512, 8},
-        {"B256 cp.async only, delay 512", 0, 256, 0, 512, 8},
+        {"A + B256 cp.async 16 warps, 148 CTAs", ABYTES, 256, 0, 0, 16, 0, 148},
+        {"A + B256 cp.async 16 warps, 74 CTAs", ABYTES, 256, 0, 0, 16, 0, 74},
+        {"A + B256 cp.async 16 warps, 37 CTAs", ABYTES, 256, 0, 0, 16, 0, 37},
+        {"A + B128 cp.async 16 warps, 74 CTAs", ABYTES, 128, 0, 0, 16, 0, 74},
+        {"A only, 74 CTAs", ABYTES, 0, 0, 0, 8, 0, 74},
+        {"B256 cp.async 16 warps, 74 CTAs", 0, 256, 0, 0, 16, 0, 74},
+        {"A only (TMA 16 KB)", ABYTES, 0, 0, 0, 8, 0},
+        {"B256 cp.async 4 warps", 0, 256, 0, 0, 4, 0},
+        {"B256 cp.async 8 warps", 0, 256, 0, 0, 8, 0},
+        {"B256 cp.async 12 warps", 0, 256, 0, 0, 12, 0},
+        {"B256 cp.async 16 warps", 0, 256, 0, 0, 16, 0},
+        {"B256 cp.async 24 warps", 0, 256, 0, 0, 24, 0},
+        {"B256 TMA box{64,1} 8 warps", 0, 256, 1, 0, 8, 0},
+        {"B256 cp.async 192 + TMA 64, 8 warps", 0, 256, 3, 0, 8, 192},
+        {"B256 cp.async 160 + TMA 96, 8 warps", 0, 256, 3, 0, 8, 160},
+        {"B256 cp.async 192 + TMA 64, 16 warps", 0, 256, 3, 0, 16, 192},
+        {"A + B256 cp.async 8 warps", ABYTES, 256, 0, 0, 8, 0},
+        {"A + B256 cp.async 16 warps", ABYTES, 256, 0, 0, 16, 0},
+        {"A + B256 cp.async 192 + TMA 64, 16 w", ABYTES, 256, 3, 0, 16, 192},
+        {"A + B128 cp.async 8 warps", ABYTES, 128, 0, 0, 8, 0},
+        {"A + B128 cp.async 16 warps", ABYTES, 128, 0, 0, 16, 0},
+        {"A + B128 cp.async 96 + TMA 32, 16 w", ABYTES, 128, 3, 0, 16, 96},
+        {"A + B128 cp.async 16 w, delay 512", ABYTES, 128, 0, 512, 16, 0},
+        {"A + B256 cp.async 16 w, delay 512", ABYTES, 256, 0, 512, 16, 0},
     };
     for (auto& c : cfgs) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaMemset(cnt, 0, 4);
             cudaMemset(cyc, 0, 8);
-            P p{K, ntiles, c.abytes, c.brows, c.bmode, c.delay, c.nw, W, du, db, cnt, cyc};
+            P p{K, ntiles, c.abytes, c.brows, c.bmode, c.delay, c.nw, c.tsplit, W, du, db, cnt, cyc};
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
             cudaEventRecord(e0);
-            k_feed<<<sms, 32 * 10, smem>>>(tX, tW, p);
+            const int g = c.grid ? c.grid : sms;
+            k_feed<<<g, 32 * (2 + c.nw), smem>>>(tX, tW, p);
             cudaEventRecord(e1);
             cudaError_t err = cudaEventSynchronize(e1);
             if (err != cudaSuccess) { printf("%s: %s\n", c.name, cudaGetErrorString(err)); return 1; }
@@ -222,10 +242,10 @@ int main(int argc, char** argv) {
             cudaMemcpy(&cy, cyc, 8, cudaMemcpyDeviceToHost);
             const double stages = double(ntiles) * (K / KB);
             const double bytes = stages * (c.abytes + c.brows * 128.0);
-            const double avg_cyc = double(cy) / sms;  // cycles per CTA
+            const double avg_cyc = double(cy) / g;  // cycles per CTA
             if (rep == 1)
-                printf("%-40s %8.3f ms  %7.1f TB/s  %6.1f B/cyc/SM  %6.0f cyc/stage  (clk %.0f MHz)\n", c.name, ms,
-                       bytes / ms / 1e9, bytes / sms / avg_cyc, avg_cyc / (stages / sms), avg_cyc / ms / 1e3);
+                printf("%-40s %8.3f ms  %7.1f TB/s  %6.1f B/cyc/SM  %6.0f cyc/stage  (CTA-avg clk %.0f MHz)\n", c.name, ms,
+                       bytes / ms / 1e9, bytes / g / avg_cyc, avg_cyc / (stages / g), avg_cyc / ms / 1e3);
         }
     }
     return 0;
