@@ -16,6 +16,7 @@
 #include "fp32_path.cuh"
 #include "gemm_union.cuh"
 #include "gemm_union_pair.cuh"
+#include "prep.cuh"
 #include "hybrid.cuh"
 #include "hybrid_mm.cuh"
 #include "updown.cuh"
@@ -233,7 +234,7 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, udense, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, glist, coff, bctr, total;
+    int64_t hc, ulist, ulen, utot, udense, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, pctr, glist, coff, bctr, total;
     int lmax, nchunk;
 };
 // Token rows per union block: 128 (single-CTA union GEMMs) or 256 (CTA-pair union GEMMs, SFFN_UNION_PAIR=1).
@@ -252,14 +253,17 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8)
     w.ulen = o;  o = align1k(o + NB * 4);
     w.utot = o;  o = align1k(o + NB * 4);
     w.udense = o; o = align1k(o + NB * 4);
-    w.umask = o; o = align1k(o + NB * (N / 32) * 4);
     w.uwoff = o; o = align1k(o + NB * (N / 32) * 4);
     w.chunk = o; o = align1k(o + (NB + 1) * 4);
     w.tiles = o; o = align1k(o + NB * ((N + 255) / 256) * 4);
     w.perm = o;  o = align1k(o + M * 4);
     w.xp = o;    o = align1k(o + M * K * 2);
     w.ctr = o;   o = align1k(o + 64);
-    w.nnz = o;   o = align1k(o + M * 4 + 16);  // + the gate GEMM's tile counter (nnz[M])
+    // zeroed together before each forward (one memset): row counts + the gate GEMM's tile counter (nnz[M]), the
+    // prep kernel's counters, and (split prep only) the merged union masks
+    w.nnz = o;   o = (o + (M + 1) * 4 + 15) & ~int64_t(15);
+    w.pctr = o;  o = (o + (2 + 2 * NB) * 4 + 15) & ~int64_t(15);
+    w.umask = o; o = align1k(o + NB * (N / 32) * 4);
     w.lmax = static_cast<int>((N / T) * (T / C - 1));  // most stored entries a row can have
     w.nchunk = static_cast<int>((N + 255) / 256);
     w.glist = o; o = align1k(o + NB * BR * static_cast<int64_t>(w.lmax) * 4);
@@ -285,6 +289,38 @@ size_t updown_ws_bytes(int64_t M, int64_t N, int64_t K, int algo, int T = 32, in
 // Row nnz buffer of the union workspace (sffn_forward lets the gate GEMM epilogue fill it: nnz_ready)
 int* union_nnz_ptr(void* ws, int64_t M, int64_t N, int64_t K, int T, int C) {
     return reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + union_ws_layout(M, N, K, T, C).nnz);
+}
+
+// tools: per-CTA phase timestamps of the prep kernel (SFFN_PREP_TRACE=1; sffn__prep_trace copies them out)
+unsigned long long* g_prep_trace = nullptr;
+int64_t g_prep_trace_n = 0;
+unsigned long long* prep_trace_buf(int64_t ctas) {
+    static const bool on = env_flag("SFFN_PREP_TRACE", false);
+    if (!on) return nullptr;
+    if (ctas * 8 > g_prep_trace_n) {
+        if (g_prep_trace) cudaFree(g_prep_trace);
+        if (cudaMalloc(&g_prep_trace, static_cast<size_t>(ctas) * 64) != cudaSuccess) return nullptr;
+        g_prep_trace_n = ctas * 8;
+    }
+    cudaMemset(g_prep_trace, 0, static_cast<size_t>(g_prep_trace_n) * 8);
+    return g_prep_trace;
+}
+
+// CTAs per union block of the prep kernel: a power of two (it must divide the block rows), up to ~1.5 waves of CTAs
+int union_prep_split(int64_t NB) {
+    const int sms = dev_info().sms;
+    int split = 1;
+    while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms) split *= 2;
+    return split;
+}
+
+// Bytes to zero before a gated union forward, from the row-count buffer (union_nnz_ptr) on: row counts, the gate
+// GEMM tile counter, the prep kernel's counters and, when the prep kernel splits blocks, the merged masks.
+size_t union_zero_bytes(int64_t M, int64_t N, int64_t K, int T, int C) {
+    const UnionWs L = union_ws_layout(M, N, K, T, C);
+    const int64_t NB = (M + union_brows() - 1) / union_brows();
+    const int64_t end = union_prep_split(NB) > 1 ? L.umask + NB * (N / 32) * 4 : L.pctr + (2 + 2 * NB) * 4;
+    return static_cast<size_t>(end - L.nnz);
 }
 
 // Union size from which a block is made dense (all N units; its weight tiles then come by TMA instead of
@@ -348,7 +384,32 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     int* rnnz = reinterpret_cast<int*>(base + L.nnz);
     int* bctr = reinterpret_cast<int*>(base + L.bctr);  // union_meta_kernel counters (zeroed by union_rank_kernel)
     const int phase = fuse ? fuse->phase : 0;
-    if (phase != 2) {
+    if (phase != 2 && gated) {
+        // one prep launch: pi, unions, work list, gate lists, X in pi order (prep.cuh)
+        if (!nnz_ready) {
+            { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
+            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+            if (cudaMemsetAsync(base + L.pctr, 0, union_zero_bytes(M, N, K, T, C) - static_cast<size_t>(L.pctr - L.nnz),
+                                st) != cudaSuccess)
+                return SFFN_ERR_CUDA;
+        }
+        const int split = union_prep_split(NB);
+        const size_t psmem = prep_smem_bytes(static_cast<int>(N), L.nchunk);
+        static std::once_flag ponce;
+        static cudaError_t pattr = cudaSuccess;
+        std::call_once(ponce, [] {
+            pattr = cudaFuncSetAttribute(union_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(prep_smem_bytes(65536, 256)));
+        });
+        if (pattr != cudaSuccess) return SFFN_ERR_CUDA;
+        const bool tma_dense = BR == 128 && N >= 256;
+        { union_prep_kernel<<<static_cast<unsigned>(NB * split), PREP_THREADS, psmem, st>>>(
+            tw, (int)M, (int)N, T, C, um, perm, rnnz, reinterpret_cast<int*>(base + L.pctr),
+            env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split, union_dense_units(N, tma_dense),
+            union_dense_nnz(N, tma_dense), static_cast<const uint8_t*>(X), K * 2,
+            env_flag("SFFN_PREP_NOCOPY", false) ? nullptr : static_cast<uint8_t*>(xp), prep_trace_buf(NB * split)); note_launch(); }
+        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
+    } else if (phase != 2) {
         if (!nnz_ready) {
             { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
             if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
@@ -582,7 +643,7 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
     if (resolve_algo(algo, N) == SFFN_ALGO_UNION) {
         // the gate GEMM epilogue also counts each row's stored entries (the union path's row order pi)
         int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
-        if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M + 1) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+        if (cudaMemsetAsync(nnz, 0, union_zero_bytes(M, N, K, T, C), S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
         if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz, nnz + M)) != SFFN_OK) return r;
         return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true);
     }
@@ -593,6 +654,14 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
 
 // Internal (not in include/sffn.h): sffn_forward (UNION) whose DOWN GEMM writes the partial Y into this rank's
 // symmetric window (Y) and reduces 2048-row windows across the ranks as they complete (sffn_comm.cu).
+// Internal (tools): the prep kernel's per-CTA phase timestamps of the last traced call (SFFN_PREP_TRACE=1).
+int64_t sffn__prep_trace(unsigned long long* host, int64_t cap) {
+    if (!g_prep_trace) return 0;
+    const int64_t n = cap < g_prep_trace_n ? cap : g_prep_trace_n;
+    if (cudaMemcpy(host, g_prep_trace, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return n;
+}
+
 int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
                         int T, int C, void* Y, void* workspace, size_t ws_bytes, uint32_t* d_overflow,
                         const uint64_t* ptrs, int G, int rank, int phase, void* stream) {
@@ -610,7 +679,7 @@ int sffn__forward_fused(const void* X, const void* Wg, const void* Wu, const voi
     int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
     FuseParams fp{ptrs, G, rank, phase};
     if (phase == 2) return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
-    if (cudaMemsetAsync(nnz, 0, static_cast<size_t>(M + 1) * 4, S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
+    if (cudaMemsetAsync(nnz, 0, union_zero_bytes(M, N, K, T, C), S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz, nnz + M)) != SFFN_OK) return r;
     return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, &fp);
 }

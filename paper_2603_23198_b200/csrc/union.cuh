@@ -106,9 +106,13 @@ __device__ __forceinline__ int tile_count(const uint32_t* __restrict__ row, int 
 
 // UP work list (the former union_scan kernel, now run by the last block CTA of union_meta_kernel): for each group
 // of `group` blocks, chunk-major then block: tiles[] = (b << 8) | c; chunk_off[0] = total tiles; zeroes the two
-// dynamic tile-scheduler counters.  NTH threads, scratch = NTH/32 + 1 ints of shared memory.
-template <int NTH>
-__device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum) {
+// dynamic tile-scheduler counters.  NTH threads (thread ids 0..NTH-1, all in full warps), scratch = NTH/32 + 1 ints of
+// shared memory; `sync` is a barrier over exactly those threads (__syncthreads or a named barrier).
+struct SyncAll {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+template <int NTH, class Sync = SyncAll>
+__device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, Sync sync = Sync()) {
     constexpr int NWP = NTH / 32;
     constexpr int MAXG = UNION_GROUP_MAX;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -134,7 +138,7 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum) {
             if (lane >= off) sc += u;
         }
         if (lane == 31) wsum[warp] = sc;
-        __syncthreads();
+        sync();
         if (warp == 0) {
             const int x = lane < NWP ? wsum[lane] : 0;
             int y = x;
@@ -146,14 +150,14 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum) {
             if (lane < NWP) wsum[lane] = y - x;
             if (lane == 31) wsum[NWP] = y;
         }
-        __syncthreads();
+        sync();
         int pos = carry + wsum[warp] + sc - tot;
         for (int c = 0; c < maxc; ++c)
 #pragma unroll
             for (int j = 0; j < MAXG; ++j)
                 if (c < nchk[j]) um.tiles[pos++] = ((b0 + j) << 8) | c;
         carry += wsum[NWP];
-        __syncthreads();
+        sync();
     }
     if (threadIdx.x == 0) {
         um.chunk_off[0] = carry;
