@@ -92,6 +92,7 @@ struct GemmArgs {
                          // counter (zeroed by the caller); null: static striding (tile += grid)
 };
 constexpr int GT_RING = 4;  // dynamic scheduler: tile ring depth (claims ahead of the slowest reader)
+constexpr int TWELL_SPARSE_MAX = 6;  // TwELL epilogue: chunks whose rows hold <= this many positives take the sparse walk
 
 // MN-major 128B-swizzled operand: 64-column atoms 8 KB apart (LBO), 8-row groups 1 KB apart (SBO)
 __device__ __forceinline__ uint64_t umma_desc_sw128_mn_tc(uint32_t smem_addr) {
@@ -386,18 +387,52 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
                     uint32_t mask = 0;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) mask |= (__uint_as_float(v[i]) > 0.0f ? 1u : 0u) << i;
+#ifdef SFFN_TWELL_PROBE_NOEPI  // timing probe (tools): the compaction skipped, results wrong
+                    if (mask != 0x12345678u) { z += __popc(mask); continue; }
+#endif
                     // columns positive in ANY of the warp's 32 rows (~10 of 32 at 1% density): a warp-uniform
                     // branch per column skips the rest, so the compaction costs ~ the positives, not 32 columns
                     // (at K = 2048 the epilogue, not the mainloop, bounded the kernel: tensor pipe 69%, ncu 1B)
-                    const uint32_t any = __reduce_or_sync(0xffffffffu, mask);
+                    // Sparse chunks (the usual case at >= 99%: at most a few positives per row): walk the row's own set
+                    // bits — a warp-uniform trip count = the most positives any lane has — and pick each value with a
+                    // 5-level select tree over the 32 registers (no dynamic register indexing), so a chunk costs ~the
+                    // positives instead of 32 columns of slot arithmetic.  The k-th positive goes to slot z + k.
+                    const int wmax = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(__popc(mask)));
+                    if (wmax <= TWELL_SPARSE_MAX) {
+                        uint32_t m = mask;
+                        for (int k = 0; k < wmax; ++k) {
+                            if (m) {
+                                const int i = __ffs(m) - 1;
+                                m &= m - 1;
+                                const int slot = z + k;
+                                if (slot < cap) {
+                                    uint32_t a16[16], a8[8], a4[4], a2[2];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        if ((any >> i) & 1u) {
-                            const int slot = z + __popc(mask & ((1u << i) - 1u));
-                            if (((mask >> i) & 1u) && slot < cap) {
-                                const uint32_t bf = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(v[i])));
-                                *sword(tbase + 1 + slot) = static_cast<uint32_t>(col_base + tcol + i) | (bf << 16);
+                                    for (int j = 0; j < 16; ++j) a16[j] = (i & 16) ? v[j + 16] : v[j];
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) a8[j] = (i & 8) ? a16[j + 8] : a16[j];
+#pragma unroll
+                                    for (int j = 0; j < 4; ++j) a4[j] = (i & 4) ? a8[j + 4] : a8[j];
+#pragma unroll
+                                    for (int j = 0; j < 2; ++j) a2[j] = (i & 2) ? a4[j + 2] : a4[j];
+                                    const uint32_t x = (i & 1) ? a2[1] : a2[0];
+                                    const uint32_t bf = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(x)));
+                                    *sword(tbase + 1 + slot) = static_cast<uint32_t>(col_base + tcol + i) | (bf << 16);
+                                }
                             }
+                        }
+                    } else if (mask) {
+                        // dense chunks: every column's store predicated on its bit (no per-column branch; the former
+                        // warp-uniform branch per column cost a BSSY/BSYNC reconvergence each)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int slot = z + __popc(mask & ((1u << i) - 1u));
+                            const bool st = ((mask >> i) & 1u) && slot < cap;
+                            const uint32_t bf = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(v[i])));
+                            uint32_t* dst = sword(tbase + 1 + slot);
+                            const uint32_t w = static_cast<uint32_t>(col_base + tcol + i) | (bf << 16);
+                            asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+                                         ::"r"(smem_u32(dst)), "r"(w), "r"(static_cast<uint32_t>(st)) : "memory");
                         }
                     }
                     z += __popc(mask);

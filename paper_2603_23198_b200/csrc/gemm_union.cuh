@@ -57,7 +57,9 @@ __device__ __forceinline__ void fuse_bf16x8_acc(float (&a)[8], const uint4& v) {
 
 // 16-byte cp.async of a gathered weight-row segment (L2 only: .cg); src_bytes < 16 zero-fills the rest
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+#ifndef SFFN_UG_NOGATHER  // timing probe only (tools): gathers skipped, results wrong
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
