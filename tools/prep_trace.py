@@ -8,6 +8,8 @@ sys.path.insert(0, ROOT)
 import torch, synth
 import paper_2603_23198_b200 as sffn
 cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "7B"]
+if len(sys.argv) > 2:
+    cfg = cfg.replace(M=int(sys.argv[2]))  # e.g. one host-pipeline chunk
 dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
 X = dev(synth.gen_x(cfg)); Wg, Wu, Wd = (dev(synth.gen_w(cfg, w)) for w in "gud")
 for _ in range(3):
