@@ -308,6 +308,8 @@ unsigned long long* prep_trace_buf(int64_t ctas) {
 
 // CTAs per union block of the prep kernel: a power of two (it must divide the block rows), up to ~1.5 waves of CTAs
 int union_prep_split(int64_t NB) {
+    const int forced = env_int("SFFN_PREP_SPLIT", 0);  // tuning override (power of two <= META_SPLIT_MAX)
+    if (forced > 0 && forced <= META_SPLIT_MAX && (forced & (forced - 1)) == 0) return forced;
     const int sms = dev_info().sms;
     int split = 1;
     while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms) split *= 2;
