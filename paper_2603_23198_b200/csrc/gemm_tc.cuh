@@ -92,7 +92,10 @@ struct GemmArgs {
                          // counter (zeroed by the caller); null: static striding (tile += grid)
 };
 constexpr int GT_RING = 4;  // dynamic scheduler: tile ring depth (claims ahead of the slowest reader)
-constexpr int TWELL_SPARSE_MAX = 6;  // TwELL epilogue: chunks whose rows hold <= this many positives take the sparse walk
+#ifndef SFFN_TWELL_SPARSE_MAX
+#define SFFN_TWELL_SPARSE_MAX 10
+#endif
+constexpr int TWELL_SPARSE_MAX = SFFN_TWELL_SPARSE_MAX;  // TwELL epilogue: chunks whose rows hold <= this many positives take the sparse walk
 
 // MN-major 128B-swizzled operand: 64-column atoms 8 KB apart (LBO), 8-row groups 1 KB apart (SBO)
 __device__ __forceinline__ uint64_t umma_desc_sw128_mn_tc(uint32_t smem_addr) {
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
                     // columns positive in ANY of the warp's 32 rows (~10 of 32 at 1% density): a warp-uniform
                     // branch per column skips the rest, so the compaction costs ~ the positives, not 32 columns
                     // (at K = 2048 the epilogue, not the mainloop, bounded the kernel: tensor pipe 69%, ncu 1B)
-                    // Sparse chunks (the usual case at >= 99%: at most a few positives per row): walk the row's own set
+                    // Sparse chunks (at most TWELL_SPARSE_MAX = 10 positives in every row; A/B of 3 / 6 / 10: 10 best at 95% and 99%): walk the row's own set
                     // bits — a warp-uniform trip count = the most positives any lane has — and pick each value with a
                     // 5-level select tree over the 32 registers (no dynamic register indexing), so a chunk costs ~the
                     // positives instead of 32 columns of slot arithmetic.  The k-th positive goes to slot z + k.
