@@ -41,6 +41,10 @@ METRIC = "sparse-FFN fwd tokens/s/GPU @99% sparsity; speedup vs own dense FFN; H
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
 FMA_LANES_PER_SM = 128
 N_SMS = 148
+# per-SM L2->SM ingress ceiling measured on this pool's B200s with the feed microbenchmark (tools/exp_feed.cu,
+# profiles/r02/exp_feed_grid.txt: TMA tiles + cp.async gathers saturate at ~58 B/cycle/SM at 148, 74 and 37 SMs) —
+# the binding limit of the union GEMMs (DESIGN.md §7 "Per-SM feed limits")
+INGRESS_B_PER_CYCLE_SM = 58.0
 
 
 def load_peaks():
@@ -497,6 +501,21 @@ def main():
                               "work": f"4*{br}*sum_b |U_b| * K FLOP executed by the union GEMMs ({br}-row blocks)",
                               "redundancy": tc_flop / max(ud_flop, 1.0)},
             "union_frac_of_N": st["union_sum"] / ((M + br - 1) // br) / Nl, "union_block_rows": br}
+        # the union GEMMs' operand stream (the resource that bounds them): UP reads an A tile (X rows, 128 x 64 bf16)
+        # per k-block of each (block, chunk) tile and every union row of W_u once per block; DOWN an A tile (H_c) per
+        # k-block of each (block, column tile) and every union row of W_d once per block
+        kb_bytes = 128 * 64 * 2
+        ingress = (st["up_tiles"] * (K // 64) * kb_bytes + st["padded_sum"] * K * 2
+                   + ((K + 255) // 256) * (st["padded_sum"] // 64) * kb_bytes + st["padded_sum"] * K * 2)
+        clk_mhz = (clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0))
+        t_ud_gemm = t_ud  # includes the prep kernel: a conservative (lower) fraction
+        kernels["fused_up_down"]["ingress"] = {
+            "bound": "l2_to_sm_ingress", "bytes": ingress, "unit": "B/cycle/SM",
+            "achieved": ingress / t_ud_gemm / (N_SMS * clk_mhz * 1e6), "peak": INGRESS_B_PER_CYCLE_SM,
+            "frac": ingress / t_ud_gemm / (N_SMS * clk_mhz * 1e6) / INGRESS_B_PER_CYCLE_SM,
+            "clock_mhz": clk_mhz,
+            "what": "A tiles + gathered weight rows of both union GEMMs per step over the whole up/down time (prep "
+                    "included) at the bench's median SM clock, vs the measured per-SM ingress ceiling"}
     else:
         kernels["fused_up_down"] = {
             "ms": t_ud * 1e3, "launches": ud_launches, "algo": "gather", "bound": "alu", "achieved": ud_flop / t_ud / 1e12,
