@@ -117,6 +117,12 @@ class Clocks:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a few hundred ms to start sampling: wait for its first line so that even a short
+            # timed region (a few steps) is covered
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.n0 = len(self.lines)
         except OSError:
             self.proc = None
 
@@ -128,6 +134,9 @@ class Clocks:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         time.sleep(0.12)
+        t0 = time.time()
+        while len(self.lines) <= getattr(self, "n0", 0) and time.time() - t0 < 2.0:
+            time.sleep(0.01)  # at least one sample taken after the region started
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
@@ -439,6 +448,15 @@ def main():
     clocks.start()
     ms = timed(step_fn, args.steps, args.warmup)
     clk = clocks.stop()
+    # warm-L2 steps (no flush between them), reported separately; not the headline value
+    barrier()
+    ev_w = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(max(3, args.steps // 4))]
+    for s_, e_ in ev_w:
+        s_.record(stream)
+        step_fn()
+        e_.record(stream)
+    barrier()
+    warm_ms = float(np.median([s_.elapsed_time(e_) for s_, e_ in ev_w]))
     n_ov = sffn.overflow_check(ov)
     t_local = float(np.sum(ms)) / 1e3
     t_max = t_local
@@ -537,6 +555,7 @@ def main():
         else:
             hbm = {"step_dram_bytes": tot, "achieved_gbs": tot / (ms_per_step / 1e3) / 1e9, "peak_gbs": peaks["hbm_gbs"],
                    "frac": tot / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],
+                   "frac_spec_8tbs": tot / (ms_per_step / 1e3) / 1e9 / 8000.0,
                    "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one forward, measured in this run "
                              "(--cache-control none), / the bench step time", "kernels": step_kernels}
             gate = [k for k in step_kernels if "gemm_tc_kernel" in k["kernel"]]
@@ -647,6 +666,7 @@ def main():
                "roofline": roofline, "kernels": kernels, "nnz_per_token": nnz_total / M, "nnz": nnz_stats,
                "overflow_tiles": n_ov, "dense": dense, "e2e": e2e, "cpu_baseline": cpu,
                "hbm": hbm,
+               "warm_l2_ms_per_step": warm_ms,
                "gpu_launches": args.steps * launches_per_step,
                "gpu_launches_per_step": launches_per_step,
                "algo": algo_used,
