@@ -29,6 +29,6 @@ oracle/liboracle.so: oracle/oracle.c
 $(shell mkdir -p build)
 
 clean:
-	rm -f $(LIB) synth/libsynth.so oracle/liboracle.so build/*
+	rm -f $(LIB) synth/libsynth.so oracle/liboracle.so build/*.log build/*.txt
 
 .PHONY: all clean
