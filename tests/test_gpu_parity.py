@@ -764,6 +764,24 @@ def test_union_all_blocks_dense(sffn):
     assert " passed" in r.stdout
 
 
+@pytest.mark.parametrize("M", [300, 5000])
+def test_prep_split_invariance(sffn, monkeypatch, M):
+    """The prep kernel builds the same unions, gate lists and X in pi order whether a block's rows are handled by one
+    CTA or split over 2, 4, 8 CTAs (atomicOr merge of the parts' masks, the last part builds, flag release): Y is
+    bit-identical for every split, and within the per-row bars of Eq.3 (oracle)."""
+    cfg = synth.CONFIGS["1B"].replace(M=M, K=256, N=2048, Kb=16, sparsity=0.99)
+    X, Wg, Wu, Wd = inputs(cfg)
+    Xd, Wgd, Wud, Wdd = (to_dev(a) for a in (X, Wg, Wu, Wd))
+    outs = []
+    for split in ("1", "2", "4", "8"):
+        monkeypatch.setenv("SFFN_PREP_SPLIT", split)
+        outs.append(sffn.forward(Xd, Wgd, Wud, Wdd, 256, 8, algo="union").view(torch.int16).cpu())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    wo, counts, n_ov, A = oracle.pack_from_inputs(X, Wg, 256, 8, matmul=True)
+    assert_y(bf16_np(outs[0].view(torch.bfloat16)), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8))
+
+
 def test_union_pi_order(sffn):
     """The row order pi (descending stored non-zeros per 2048-row window, ties by row index) and the
     128-row block unions built on it: the union sizes the library reports equal those computed here from the
