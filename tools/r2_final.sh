@@ -2,7 +2,7 @@
 # Round-2 evidence on the final build: GPU suite, bench (7B default + 1B + 70B), sparsity sweep, reference arm,
 # the bench's ncu launch list, one ncu --set full capture of every kernel of a 7B forward, CUPTI timelines.
 cd "$(dirname "$0")/.."
-O=gpurun_out/r02; mkdir -p $O
+O=gpurun_out/r02/${TAG:-final}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/gpu.txt 2>&1
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider -rf --durations=15 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench_7B.json 2> $O/bench_7B.err; echo "bench 7B rc=$?"
