@@ -87,11 +87,14 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     const int lid = s_lid;
     if (trace && t == 0) trace[8 * lid] = gtimer();
     const int b = lid / split, part = lid % split;
-    const int r0 = part * PR;                                     // first row of this part within the block
+    // part `part` owns the block rows part, part + split, part + 2 split, ...: the rows are in descending-nnz order,
+    // so interleaving balances the parts' work (contiguous ranges gave part 0 the densest rows and made every
+    // other part wait for it at the merge)
+    auto prow = [&](int r) -> int64_t { return static_cast<int64_t>(b) * BR + static_cast<int64_t>(r) * split + part; };
     const int w0 = (b * BR) / PERM_W * PERM_W;                    // window start row
     const int pb = b * BR - w0;                                   // block start position within the window
     const int wrows = min(PERM_W, M - w0);
-    const int rows = max(0, min(PR, M - b * BR - r0));            // real rows of this part
+    const int rows = max(0, min(PR, (M - b * BR - part + split - 1) / split));  // real rows of this part
 
     // ---------------------------------------------------------------- 1. pi: bitonic sort of the window (descending)
     // thread t holds positions 4t .. 4t+3: partners at distance j = 1, 2 in registers, 4..64 in the warp (shuffle),
@@ -138,19 +141,20 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
             }
         }
     }
-    // this part's rows (positions pb + r0 .. pb + r0 + PR) and the block's stored-entry sum (dense shortcut)
+    // this part's rows (block positions part, part + split, ...) and the block's stored-entry sum (dense shortcut)
     int bs = 0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         const int p = 4 * t + s;
         if (v[s] >= 0 && p >= pb && p < pb + BR) {
             bs += v[s] >> 11;
-            const int r = p - pb - r0;
+            const int br = p - pb;
+            const int r = (br % split == part) ? br / split : -1;
             if (r >= 0 && r < PR) {
                 const int row = w0 + (PERM_W - 1 - (v[s] & (PERM_W - 1)));
                 s_prow[r] = row;
                 s_rcnt[r] = v[s] >> 11;  // stored entries of the row (the gate GEMM's count)
-                perm[static_cast<int64_t>(b) * BR + r0 + r] = row;
+                perm[prow(r)] = row;
             }
         }
     }
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
                 const int64_t off = static_cast<int64_t>(q) * PREP_PIECE;
                 bytes = static_cast<uint32_t>((row_bytes - off < PREP_PIECE ? row_bytes - off : static_cast<int64_t>(PREP_PIECE)));
                 src = X + static_cast<int64_t>(s_prow[r]) * row_bytes + off;
-                dst = Xp + (static_cast<int64_t>(b) * BR + r0 + r) * row_bytes + off;
+                dst = Xp + prow(r) * row_bytes + off;
             };
             auto load = [&](int i) {
                 const uint8_t* src;
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
         for (int q = 0; q < PREP_RR; ++q) {
             const int rq = r + q * PREP_NW;
             rowp[q] = rq < rows ? tw + static_cast<int64_t>(s_prow[rq]) * RW : nullptr;
-            glp[q] = um.glist + (static_cast<int64_t>(b) * BR + r0 + rq) * um.lmax;
+            glp[q] = um.glist + prow(rq) * um.lmax;
             base[q] = 0;
         }
         for (int t0 = 0; t0 < NT; t0 += 32 * PREP_U) {
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     const int nch = um.nchunk;
     int32_t* cc = ccnt + warp * (nch + 1);
     for (int r = warp; r < PR; r += PREP_NW) {
-        const int64_t i = static_cast<int64_t>(b) * BR + r0 + r;  // pi-ordered row
+        const int64_t i = prow(r);  // pi-ordered row
         for (int c = lane; c <= nch; c += 32) cc[c] = 0;
         __syncwarp();
         if (r < rows && !udense) {
