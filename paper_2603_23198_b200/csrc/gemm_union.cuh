@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 int b, cj, len;
                 tile_info(tile, b, cj, len);
                 const int nk = UP ? nk_up : len / UG_BK;
-                // dense block (union forced to all N units, union_meta_kernel): B by TMA tiles, no gathers
+                // dense block (union forced to all N units by the prep kernel): B by TMA tiles, no gathers
                 const bool dense = __ldg(args.um.udense + b) != 0;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait_relaxed(&empty[stage], phase ^ 1);

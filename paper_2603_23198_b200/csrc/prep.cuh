@@ -1,6 +1,6 @@
 // prep.cuh — the union path's metadata in ONE launch (DESIGN.md §7 K2 "prep"): row order pi, block unions, the UP
 // work list, the compact gate lists and X in pi order.  Replaces union_rank_kernel + union_meta_kernel +
-// union_gate_list_kernel (three launches, each re-reading its inputs) on the gated forward.
+// union_gate_list_kernel of round 1 (three launches, each re-reading its inputs).
 //
 // One CTA (PREP_THREADS) per (block of BR pi-ordered rows, part), `split` parts per block for small M.  Per CTA:
 //   1. pi (Alg.2 iterates m in pi(0..M-1); descending stored non-zeros per 2048-row window): every CTA
@@ -8,11 +8,11 @@
 //      window, no cross-CTA wait — and keeps the rows at its block's positions; writes perm for its rows;
 //   2. warp 15 lane 0 streams the CTA's rows of X into pi order (Xp) with 1-D bulk copies (TMA engine, 8 KB pieces
 //      through an 8-slot SMEM ring), asynchronous to everything below;
-//   3. warps 0-14: OR of the rows' stored indices into a SMEM bitmask (as union_meta_kernel); split > 1: merged into
+//   3. warps 0-14: OR of the rows' stored indices into a SMEM bitmask; split > 1: merged into
 //      the block's global mask (atomicOr), the last part builds;
 //   4. the builder: prefix sums -> sorted U_b (padded to a multiple of 64 with unit 0), uwoff / ulen / utot / udense;
 //      releases the block (flag) for the other parts; the last builder overall writes the UP work list;
-//   5. warps 0-14: the gate lists of the CTA's rows (as union_gate_list_kernel) from the block's mask in SMEM.
+//   5. warps 0-14: the gate lists of the CTA's rows from the block's mask in SMEM (gated forward only).
 // Counters (logical CTA ids, per-block arrivals and flags, builders) are zeroed by the caller's memset that also
 // zeroes the gate GEMM's row counts.  Logical CTA ids come from an atomic counter, so a part that waits for its
 // block's builder never waits for a CTA that has not started (the builder is the last part to arrive).
@@ -61,7 +61,8 @@ inline size_t prep_smem_bytes(int N, int nchunk) {
 __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     const uint32_t* __restrict__ tw, int M, int N, int T, int C, UnionMeta um, int32_t* __restrict__ perm,
     const int* __restrict__ rnnz, int* __restrict__ pctr, int up_group, int split, int dense_units, int64_t dense_nnz,
-    const uint8_t* __restrict__ X, int64_t row_bytes, uint8_t* __restrict__ Xp, unsigned long long* trace) {
+    const uint8_t* __restrict__ X, int64_t row_bytes, uint8_t* __restrict__ Xp, int gate_lists,
+    unsigned long long* trace) {
     extern __shared__ uint8_t prep_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(prep_raw) + 1023) & ~uintptr_t(1023));
     int* key = reinterpret_cast<int*>(ring + PREP_SLOTS * PREP_PIECE);  // [2][2048]
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     }
 
     if (builder) {
-        // ---------------------------------------------------------------- 4. U_b (union_meta_kernel's build)
+        // ---------------------------------------------------------------- 4. U_b
         for (int pass = 0; pass < 2; ++pass) {
             const int seg = (NW + PREP_WORK - 1) / PREP_WORK;
             const int wa = t * seg, wb = min(NW, wa + seg);
@@ -407,6 +408,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     }
 
     if (trace && t == 0) trace[8 * lid + 3] = gtimer();
+    if (!gate_lists) return;  // non-gated variant: the union only (H_c is scattered from the TwELL by another kernel)
     // -------------------------------------------------------------------- 5. gate lists of the part's rows
     const bool udense = __ldcg(um.udense + b) != 0;  // identity union: the UP epilogue reads the TwELL directly
     const int nch = um.nchunk;

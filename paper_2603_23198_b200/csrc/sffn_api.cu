@@ -234,7 +234,7 @@ int updown_checks(const void* X, const void* tw, const void* Wu, const void* Wd,
 inline int64_t align1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
 
 struct UnionWs {
-    int64_t hc, ulist, ulen, utot, udense, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, pctr, glist, coff, bctr, total;
+    int64_t hc, ulist, ulen, utot, udense, umask, uwoff, chunk, tiles, perm, xp, ctr, nnz, pctr, glist, coff, total;
     int lmax, nchunk;
 };
 // Token rows per union block: 128 (single-CTA union GEMMs) or 256 (CTA-pair union GEMMs, SFFN_UNION_PAIR=1).
@@ -268,7 +268,6 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8)
     w.nchunk = static_cast<int>((N + 255) / 256);
     w.glist = o; o = align1k(o + NB * BR * static_cast<int64_t>(w.lmax) * 4);
     w.coff = o;  o = align1k(o + NB * BR * static_cast<int64_t>(w.nchunk + 1) * 2);
-    w.bctr = o;  o = align1k(o + (NB + 1) * 4);  // union_meta_kernel: per-block + global completion counters
     w.total = o;
     return w;
 }
@@ -384,10 +383,10 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     void* xp = base + L.xp;
     // row permutation pi (per 2048-row window, descending stored nnz) and the permuted copy of X
     int* rnnz = reinterpret_cast<int*>(base + L.nnz);
-    int* bctr = reinterpret_cast<int*>(base + L.bctr);  // union_meta_kernel counters (zeroed by union_rank_kernel)
     const int phase = fuse ? fuse->phase : 0;
-    if (phase != 2 && gated) {
-        // one prep launch: pi, unions, work list, gate lists, X in pi order (prep.cuh)
+    if (phase != 2) {
+        // one prep launch: pi, unions, work list, gate lists and X in pi order (prep.cuh); the non-gated variant needs
+        // neither gate lists nor X and scatters the TwELL values into H_c instead (no UP GEMM)
         if (!nnz_ready) {
             { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
             if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
@@ -408,35 +407,10 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         { union_prep_kernel<<<static_cast<unsigned>(NB * split), PREP_THREADS, psmem, st>>>(
             tw, (int)M, (int)N, T, C, um, perm, rnnz, reinterpret_cast<int*>(base + L.pctr),
             env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split, union_dense_units(N, tma_dense),
-            union_dense_nnz(N, tma_dense), static_cast<const uint8_t*>(X), K * 2,
-            env_flag("SFFN_PREP_NOCOPY", false) ? nullptr : static_cast<uint8_t*>(xp), prep_trace_buf(NB * split)); note_launch(); }
+            union_dense_nnz(N, tma_dense), gated ? static_cast<const uint8_t*>(X) : nullptr, K * 2,
+            (gated && !env_flag("SFFN_PREP_NOCOPY", false)) ? static_cast<uint8_t*>(xp) : nullptr, gated ? 1 : 0,
+            prep_trace_buf(NB * split)); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-    } else if (phase != 2) {
-        if (!nnz_ready) {
-            { row_nnz_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(tw, (int)M, (int)N, T, C, rnnz); note_launch(); }
-            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-        }
-        { union_rank_kernel<<<static_cast<unsigned>((M + PERM_W - 1) / PERM_W), PERM_THREADS, 0,
-                            st>>>(rnnz, (int)M, perm, um.umask, NB * (N / 32), bctr, (int)NB + 1); note_launch(); }
-        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-
-        // union lists + the UP work list (one launch), then the compact gate lists (gated) or the scattered G (non-gated)
-        const int ub_smem = static_cast<int>((2 * (N / 32) + UB_THREADS / 32 + 1) * 4);
-        const int sms_meta = dev_info().sms;
-        // CTAs per union block: a power of two (it must divide the block rows), up to ~1.5 waves of CTAs
-        int split = 1;
-        while (split < META_SPLIT_MAX && 2 * NB * split < 3 * sms_meta) split *= 2;
-        { union_meta_kernel<<<static_cast<unsigned>(NB * split), UB_THREADS, ub_smem, st>>>(
-            tw, (int)M, (int)N, T, C, um, perm, bctr, env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split,
-            union_dense_units(N, BR == 128 && N >= 256), rnnz, union_dense_nnz(N, BR == 128 && N >= 256)); note_launch(); }
-        if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-        if (gated) {
-            // also writes X in pi order (the UP GEMM's A operand)
-            { union_gate_list_kernel<<<static_cast<unsigned>(NB * BR * 32 / 256), 256, 8 * (L.nchunk + 1) * 4, st>>>(
-                tw, (int)M, (int)N, T, C, um, perm, static_cast<const uint4*>(X), (int)(K / 8),
-                static_cast<uint4*>(xp)); note_launch(); }
-            if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
-        }
         if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)
             { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (BR / GS_ROWS)), 256, 0, st>>>(
                 tw, (int)M, (int)N, T, C, um, static_cast<uint16_t*>(hc), perm); note_launch(); }
