@@ -120,7 +120,8 @@ int sffn_up_down(const void* X, const uint32_t* twell, const void* Wu, const voi
  * sffn_forward — the whole sparse FFN forward: sffn_pack into `workspace` (>= sffn_forward_workspace_bytes)
  * then sffn_up_down with the rest of the workspace.  GATHER = the paper's two launches; UNION
  * launches 4 kernels (gate GEMM; one metadata kernel: row order pi, block unions, gate lists, X in pi order;
- * UP and DOWN GEMMs; sffn_launch_count reports them) plus one memset of the row counts / counters.  The TwELL left at the start of the workspace
+ * UP and DOWN GEMMs; sffn_launch_count reports them) plus one memset of the row counts / counters.
+ * The TwELL left at the start of the workspace
  * is valid after the call (stream-ordered).
  */
 int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, int64_t M, int64_t K, int64_t N,
