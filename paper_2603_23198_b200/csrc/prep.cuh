@@ -27,6 +27,8 @@ constexpr int PREP_NW = PREP_WORK / 32;
 constexpr int PREP_SLOTS = 8, PREP_PIECE = 8192;  // X copy ring
 constexpr int PREP_U = 2;   // TwELL tiles per lane per row in flight (56 tiles per row at N = 14336, T = 256)
 constexpr int PREP_RR = 2;  // rows per warp in flight in the OR pass
+constexpr int PREP_UD = 1;  // dense path: tiles per lane in flight (4 x 16 bytes each)
+constexpr int PREP_DENSE_ROW = 3;  // mean stored entries per tile above which a block's rows take the one-row dense path
 struct PrepCtr {         // int offsets into the prep counter block (zeroed by the caller)
     static constexpr int lid = 0, built = 1, arrive = 2;  // arrive[NB], then flag[NB]
 };
@@ -222,8 +224,64 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     // lane per tile, PREP_U tiles in flight per lane (count + first three entries in one 16-byte load); the warp
     // prefix of the tile counts gives each entry its place in the row's ascending list, stashed raw (unit | gate)
     // in the row's gate list and turned into union positions in step 5 (no second pass over the TwELL)
+    // Dense rows (the first blocks of each window: several stored entries per tile) would need dependent loads past
+    // entry 6 of most tiles; rows with more than PREP_DENSE_ROW entries per tile on average take a one-row path that
+    // loads count + 15 entries of every tile up front (4 x 16 bytes per lane and tile), the others the two-row path.
+    const bool dense_rows = (WPT & 3) == 0 && WPT >= 16 && !dense_block &&
+                            static_cast<int64_t>(s_bsum) > static_cast<int64_t>(PREP_DENSE_ROW) * NT * BR;
+    for (int r = warp; r < (dense_rows ? rows : 0); r += PREP_NW) {
+        const uint32_t* row = tw + static_cast<int64_t>(s_prow[r]) * RW;
+        uint32_t* glr = um.glist + prow(r) * um.lmax;
+        int base = 0;
+        for (int t0 = 0; t0 < NT; t0 += 32 * PREP_UD) {
+            uint4 a[PREP_UD][4];
+#pragma unroll
+            for (int u = 0; u < PREP_UD; ++u) {
+                const int tt = t0 + 32 * u + lane;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    a[u][q] = make_uint4(0, 0, 0, 0);
+                    if (tt < NT) a[u][q] = __ldg(reinterpret_cast<const uint4*>(row + static_cast<int64_t>(tt) * WPT + 4 * q));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PREP_UD; ++u) {
+                const int tt = t0 + 32 * u + lane;
+                const int cnt = tt < NT ? min(static_cast<int>(a[u][0].x), cap) : 0;
+                int inc = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int x = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += x;
+                }
+                uint32_t* dst = glr + base + inc - cnt;
+                auto put = [&](uint32_t w, int e) {
+                    const uint32_t n = w & 0xFFFFu;
+                    atomicOr(&mask[n >> 5], 1u << (n & 31));
+                    dst[e] = w;
+                };
+                // entries 0..14 from the four registers (word 1 + e of the tile), the rest by further loads
+#pragma unroll
+                for (int e = 0; e < 15; ++e) {
+                    const int wi = 1 + e;
+                    const uint4& q4 = a[u][wi >> 2];
+                    const uint32_t w = (wi & 3) == 0 ? q4.x : (wi & 3) == 1 ? q4.y : (wi & 3) == 2 ? q4.z : q4.w;
+                    if (e < cnt) put(w, e);
+                }
+                if (tt < NT)
+                    for (int e4 = 16; e4 <= cnt; e4 += 4) {
+                        const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(row + static_cast<int64_t>(tt) * WPT + e4));
+                        put(v4.x, e4 - 1);
+                        if (e4 + 1 <= cnt) put(v4.y, e4);
+                        if (e4 + 2 <= cnt) put(v4.z, e4 + 1);
+                        if (e4 + 3 <= cnt) put(v4.w, e4 + 2);
+                    }
+                base += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+    }
     // PREP_RR rows per warp in flight (their tile loads issued together)
-    for (int r = warp; r < (dense_block ? 0 : rows); r += PREP_RR * PREP_NW) {
+    for (int r = warp; r < ((dense_block || dense_rows) ? 0 : rows); r += PREP_RR * PREP_NW) {
         const uint32_t* rowp[PREP_RR];
         uint32_t* glp[PREP_RR];
         int base[PREP_RR];
