@@ -136,13 +136,29 @@ constexpr int UG_GATHER = 32 * UG_GW;
 constexpr int UG_EWB = 8192;  // epilogue staging per warp
 constexpr int UG_SMEM = 1024 + UG_STAGES * UG_STAGE_BYTES + 4 * UG_EWB + 1024;
 constexpr int UG_RING = 8;       // tile-scheduler ring depth
-constexpr int UG_READERS = UG_GW + 5;  // gather warps + MMA thread + 4 epilogue warps
+constexpr int UG_READERS = UG_GW + 5;  // gather warps + MMA thread + 4 epilogue warps (pair kernels)
+// Epilogue warp groups of the single-CTA union GEMMs: with 2, warps 4-7 drain columns 0-127 of an accumulator and
+// warps 8+UG_GW..+3 columns 128-255 at the same time (4 KB of staging each, 64-column passes): the epilogue takes
+// half as long.  At K = 2048 (1B) one group's UP epilogue was slower than a tile's mainloop: without the gathers the
+// MMA thread spent its time waiting for the accumulator (ncu, tools/prof_union_src.sh).  The fused all-reduce DOWN
+// (which counts 4 epilogue arrivals per tile at the window owner) keeps one group.
+#ifndef SFFN_UG_EPI_GROUPS
+#define SFFN_UG_EPI_GROUPS 2
+#endif
+constexpr int UG_EG = SFFN_UG_EPI_GROUPS;
+static_assert(UG_EG == 1 || UG_EG == 2, "1 or 2 epilogue groups");
+constexpr int UG_THREADS2 = UG_THREADS + 128 * (UG_EG - 1);  // single-CTA (non-fused) union GEMMs
 
 template <bool UP, bool FUSED = false>
-__global__ void __launch_bounds__(UG_THREADS, 1)
+__global__ void __launch_bounds__(FUSED ? UG_THREADS : UG_THREADS2, 1)
     union_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmOut, const UnionArgs args) {
     constexpr int S = UG_STAGES;
+    constexpr int EG = FUSED ? 1 : UG_EG;        // epilogue warp groups (column halves)
+    constexpr int EWB = UG_EWB / EG;             // staging bytes per epilogue warp
+    constexpr int PC = EWB / 64;                 // columns per staging pass (32 rows x PC bf16 = EWB bytes)
+    constexpr int GC = 256 / EG;                 // columns per group
+    constexpr int READERS = UG_GW + 1 + 4 * EG;  // gather warps + MMA thread + epilogue warps
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stA = smem;
@@ -175,12 +191,12 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 4 * EG);
         }
         for (int i = 0; i < 4; ++i) mbar_init(&gbar[i], 1);
         for (int i = 0; i < UG_RING; ++i) {
             mbar_init(&sfull[i], 1);
-            mbar_init(&sempty[i], UG_READERS);
+            mbar_init(&sempty[i], READERS);
         }
         fence_mbar_init();
     }
@@ -269,7 +285,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= 8) {
+    } else if (warp >= 8 && warp < 8 + UG_GW) {
         // ------------------------------------------------------------ B operand: gathered weight rows
         // UP (K-major): LPR consecutive lanes copy one UG_ROWB-byte row segment (16 B each), RPI rows per warp
         // instruction; DOWN (MN-major, 128-byte swizzle): one neuron row's 4 adjacent 64-column atoms (512 B) per
@@ -502,9 +518,11 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             }
         }
     } else if (warp >= 4) {
-        // ------------------------------------------------------------ epilogue
-        const int ew = warp - 4;
-        uint8_t* stg = epi + ew * UG_EWB;
+        // ------------------------------------------------------------ epilogue (EG groups of 4 warps)
+        const int ew = warp & 3;                   // TMEM lane quarter: a warp reads lanes 32 (warp % 4) .. + 31
+        const int eg = warp >= 8 ? 1 : 0;          // column half (EG = 2)
+        const int g0 = eg * GC;                    // first accumulator column of this group
+        uint8_t* stg = epi + (eg * 4 + ew) * EWB;
         int acc = 0;
         uint32_t acc_phase = 0;
         int ridx = 0;
@@ -543,27 +561,29 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 // staging <- this row's gate values for the chunk (from the compact gate list, zero elsewhere),
                 // then H = G * (X W_u^T) in place, then TMA store of the H_c tile.
                 const int p0 = 256 * cj;
+                bool released = false;
 #pragma unroll 1
-                for (int h = 0; h < 2 && 128 * h < len; ++h) {
-                    const int nbox = min(2, (len - 128 * h) / 64);
+                for (int h = 0; h < GC / PC && g0 + PC * h < len; ++h) {
+                    const int c0 = g0 + PC * h;  // first column of this pass within the tile
+                    const int nbox = min(PC / 64, (len - c0) / 64);
                     if (lane == 0) bulk_wait_read0();  // previous TMA store has finished reading the staging buffer
                     __syncwarp();
 #pragma unroll
-                    for (int q = 0; q < 2; ++q)
+                    for (int q = 0; q < PC / 64; ++q)
 #pragma unroll
                         for (int c16 = 0; c16 < 8; ++c16)
                             *reinterpret_cast<uint4*>(stg + q * 4096 + lane * 128 + ((c16 ^ (lane & 7)) << 4)) =
                                 make_uint4(0, 0, 0, 0);  // XOR: conflict-free 16-byte stores
                     auto put_g = [&](uint32_t w) {
-                        const int j = static_cast<int>(w >> 16) - p0 - 128 * h;
-                        if (j >= 0 && j < 128)
+                        const int j = static_cast<int>(w >> 16) - p0 - c0;
+                        if (j >= 0 && j < PC)
                             *reinterpret_cast<uint16_t*>(stg + (j >> 6) * 4096 + sw128_off(lane, j & 63)) =
                                 static_cast<uint16_t>(w & 0xFFFFu);
                     };
                     if (dense_blk) {
                         if (twrow) {  // TwELL tiles covering units [p0 + 128 h, p0 + 128 h + 128)
                             const int WPT = args.T / args.C, cap = WPT - 1;
-                            const int t0 = (p0 + 128 * h) / args.T, t1 = min(N, p0 + 128 * h + 128 + args.T - 1) / args.T;
+                            const int t0 = (p0 + c0) / args.T, t1 = min(N, p0 + c0 + PC + args.T - 1) / args.T;
                             for (int t = t0; t < t1 && t < N / args.T; ++t) {
                                 const uint32_t* blk = twrow + static_cast<int64_t>(t) * WPT;
                                 const int cnt = min(static_cast<int>(__ldg(blk)), cap);
@@ -582,7 +602,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
 #pragma unroll 1
                     for (int q32 = 0; q32 < 2 * nbox; ++q32) {
                         uint32_t v[32];
-                        tmem_ld32(tb + 128 * h + 32 * q32, v);
+                        tmem_ld32(tb + c0 + 32 * q32, v);
                         tmem_wait_ld();
 #pragma unroll
                         for (int p = 0; p < 16; ++p) {
@@ -597,17 +617,23 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                             }
                         }
                     }
-                    if (h == 1 || 128 * (h + 1) >= len) {
+                    if (h == GC / PC - 1 || c0 + PC >= len) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[acc]);
+                        released = true;
                     }
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int q = 0; q < nbox; ++q) tma_store_2d(&tmOut, stg + q * 4096, p0 + 128 * h + 64 * q, row0);
+                        for (int q = 0; q < nbox; ++q) tma_store_2d(&tmOut, stg + q * 4096, p0 + c0 + 64 * q, row0);
                         bulk_commit();
                     }
+                }
+                if (!released) {  // a chunk narrower than this group's first column: nothing to store
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
             } else {
                 // DOWN: rows were processed in pi order; row i of the tile goes to Y[perm[row0 + i]].
@@ -616,36 +642,39 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
                 // 32 rows x 128 columns (bf16) per half in SMEM (conflict-free rotated 16-byte stores), then the
                 // warp writes two rows per instruction with coalesced 16-byte global stores (LSU, not per-row
                 // bulk copies: those were 256 small TMA requests per tile competing with the A-tile loads).
-                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * 64;
+                constexpr int RB = PC * 2;            // staging bytes per row
+                constexpr int LPR = RB / 16;          // lanes per row in the row writes (16 B each)
+                uint32_t* srow = reinterpret_cast<uint32_t*>(stg) + lane * (RB / 4);
                 const int prow_l = row0 + lane;
                 const int64_t yrow_l = prow_l < args.M ? static_cast<int64_t>(__ldg(args.perm + prow_l)) : -1;
 #pragma unroll 1
-                for (int half = 0; half < 2; ++half) {
-                    const int c0 = cj * 256 + half * 128;
-                    const int nc = min(128, args.K - c0);
+                for (int h = 0; h < GC / PC; ++h) {
+                    const int ct = g0 + PC * h;          // column within the tile
+                    const int c0 = cj * 256 + ct;        // output column
+                    const int nc = min(PC, args.K - c0);
 #pragma unroll 1
-                    for (int ch = 0; ch < 4; ++ch) {
+                    for (int ch = 0; ch < PC / 32; ++ch) {
                         uint32_t v[32];
-                        tmem_ld32(tb + half * 128 + ch * 32, v);
+                        tmem_ld32(tb + ct + ch * 32, v);
                         tmem_wait_ld();
                         st_row32_bf16(srow + ch * 16, v, lane);
                     }
-                    if (half == 1) {
+                    if (h == GC / PC - 1) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[acc]);
                     }
                     __syncwarp();
-                    const int chunk = lane & 15;
+                    const int chunk = lane % LPR;
 #pragma unroll 4
-                    for (int it = 0; it < 16; ++it) {
-                        const int r = 2 * it + (lane >> 4);
+                    for (int it = 0; it < LPR; ++it) {
+                        const int r = (32 / LPR) * it + lane / LPR;
                         const int64_t yrow = __shfl_sync(0xffffffffu, yrow_l, r);
-                        const uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + chunk * 16);
+                        const uint4 val = *reinterpret_cast<const uint4*>(stg + r * RB + chunk * 16);
                         if (yrow >= 0 && chunk * 8 < nc)
                             *reinterpret_cast<uint4*>(args.Y + yrow * args.K + c0 + chunk * 8) = val;
                     }
-                    __syncwarp();  // staging rows read before the next half overwrites them
+                    __syncwarp();  // staging rows read before the next pass overwrites them
                 }
                 if constexpr (FUSED) {
                     // this warp's 32 rows x 256 columns are in the local window: count them at the window's owner

@@ -497,7 +497,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
     if (gated && phase != 2) {
         // UP: the number of (block, chunk) tiles is only known on the device; persistent grid.  For the
         // non-gated variant H_c already holds h = relu(x W_u) (the scattered TwELL values): no UP GEMM.
-        { union_gemm_kernel<true><<<sms, UG_THREADS, UG_SMEM, st>>>(tx, twu, thc_st, ua); note_launch(); }
+        { union_gemm_kernel<true><<<sms, UG_THREADS2, UG_SMEM, st>>>(tx, twu, thc_st, ua); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
     }
     const int g2 = static_cast<int>(dtiles < sms ? dtiles : sms);
@@ -508,7 +508,7 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         ud.rank = fuse->rank;
         { union_gemm_kernel<false, true><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
     } else {
-        { union_gemm_kernel<false><<<g2, UG_THREADS, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
+        { union_gemm_kernel<false><<<g2, UG_THREADS2, UG_SMEM, st>>>(thc_ld, twd, ty, ud); note_launch(); }
     }
     return cudaGetLastError() == cudaSuccess ? SFFN_OK : SFFN_ERR_CUDA;
 }
