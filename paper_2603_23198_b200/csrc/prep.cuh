@@ -60,9 +60,44 @@ inline size_t prep_smem_bytes(int N, int nchunk) {
     return 1024 + PREP_SLOTS * PREP_PIECE + 2 * 2048 * 4 + 2 * (N / 32) * 4 + PREP_NW * (nchunk + 1) * 4 + 64 * 4;
 }
 
+// Parts (CTAs) per block: the base split (small M) times a boost for the densest blocks of each 2048-row window —
+// the rows are in descending stored-nnz order, so a window's first blocks carry 2-3x the entries of its median block
+// and set the kernel's span (per-CTA phase trace, DESIGN.md §7 "prep").  boost 0: uniform; 1: x2 for window positions
+// 0-1; 2: x4 for position 0, x2 for 1-2.  The host picks the strongest boost whose CTAs fit in one wave.
+__host__ __device__ inline int prep_parts(int bw, int base, int boost) {
+    const int m = boost == 2 ? (bw == 0 ? 4 : (bw < 3 ? 2 : 1)) : (boost == 1 ? (bw < 2 ? 2 : 1) : 1);
+    return min(META_SPLIT_MAX, base * m);
+}
+// logical CTA lid -> (block b, part); returns the block's part count (0 past the end).  Order: window position
+// major (every window's densest block first, the sparsest last), then window, then part — the heavy CTAs start in
+// the first wave and a block's parts have consecutive ids (a waiting part never waits for an unstarted builder).
+__host__ __device__ inline int prep_map(int lid, int NB, int WB, int base, int boost, int* b, int* part) {
+    const int NWIN = (NB + WB - 1) / WB;
+    int rem = lid;
+    for (int bw = 0; bw < WB; ++bw) {
+        const int nw = NWIN - 1 + (((NWIN - 1) * WB + bw < NB) ? 1 : 0);  // windows that have position bw
+        const int sp = prep_parts(bw, base, boost);
+        if (rem < nw * sp) {
+            *b = (rem / sp) * WB + bw;
+            *part = rem % sp;
+            return sp;
+        }
+        rem -= nw * sp;
+    }
+    *b = -1;
+    *part = 0;
+    return 0;
+}
+inline int prep_ctas(int NB, int WB, int base, int boost) {
+    int n = 0;
+    const int NWIN = (NB + WB - 1) / WB;
+    for (int bw = 0; bw < WB; ++bw) n += (NWIN - 1 + (((NWIN - 1) * WB + bw < NB) ? 1 : 0)) * prep_parts(bw, base, boost);
+    return n;
+}
+
 __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     const uint32_t* __restrict__ tw, int M, int N, int T, int C, UnionMeta um, int32_t* __restrict__ perm,
-    const int* __restrict__ rnnz, int* __restrict__ pctr, int up_group, int split, int dense_units, int64_t dense_nnz,
+    const int* __restrict__ rnnz, int* __restrict__ pctr, int up_group, int split_base, int split_boost, int dense_units, int64_t dense_nnz,
     const uint8_t* __restrict__ X, int64_t row_bytes, uint8_t* __restrict__ Xp, int gate_lists,
     unsigned long long* trace) {
     extern __shared__ uint8_t prep_raw[];
@@ -77,7 +112,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     __shared__ int s_prow[256], s_rcnt[256];
     __shared__ int s_lid, s_last, s_bsum;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
-    const int BR = um.brows, PR = BR / split;
+    const int BR = um.brows;
     const int NB = (M + BR - 1) / BR;
 
     if (t == 0) {
@@ -89,7 +124,9 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     __syncthreads();
     const int lid = s_lid;
     if (trace && t == 0) trace[8 * lid] = gtimer();
-    const int b = lid / split, part = lid % split;
+    int b, part;
+    const int split = prep_map(lid, NB, PERM_W / BR, split_base, split_boost, &b, &part);
+    const int PR = BR / split;
     // part `part` owns the block rows part, part + split, part + 2 split, ...: the rows are in descending-nnz order,
     // so interleaving balances the parts' work (contiguous ranges gave part 0 the densest rows and made every
     // other part wait for it at the merge)

@@ -306,6 +306,18 @@ unsigned long long* prep_trace_buf(int64_t ctas) {
 }
 
 // CTAs per union block of the prep kernel: a power of two (it must divide the block rows), up to ~1.5 waves of CTAs
+// densest-blocks-first split of the prep kernel (prep_parts): the strongest boost whose CTAs fit in one wave of 2 CTAs
+// per SM; SFFN_PREP_BOOST=0/1/2 forces one (A/B)
+int union_prep_split(int64_t NB);
+int union_prep_boost(int64_t NB, int BR) {
+    const char* e = std::getenv("SFFN_PREP_BOOST");
+    if (e && *e) return std::min(2, std::max(0, std::atoi(e)));
+    const int base = union_prep_split(NB), sms = dev_info().sms;
+    for (int b = 2; b > 0; --b)
+        if (prep_ctas(static_cast<int>(NB), PERM_W / BR, base, b) <= 2 * sms) return b;
+    return 0;
+}
+
 int union_prep_split(int64_t NB) {
     const int forced = env_int("SFFN_PREP_SPLIT", 0);  // tuning override (power of two <= META_SPLIT_MAX)
     if (forced > 0 && forced <= META_SPLIT_MAX && (forced & (forced - 1)) == 0) return forced;
@@ -320,7 +332,7 @@ int union_prep_split(int64_t NB) {
 size_t union_zero_bytes(int64_t M, int64_t N, int64_t K, int T, int C) {
     const UnionWs L = union_ws_layout(M, N, K, T, C);
     const int64_t NB = (M + union_brows() - 1) / union_brows();
-    const int64_t end = union_prep_split(NB) > 1 ? L.umask + NB * (N / 32) * 4 : L.pctr + (2 + 2 * NB) * 4;
+    const int64_t end = (union_prep_split(NB) > 1 || union_prep_boost(NB, union_brows())) ? L.umask + NB * (N / 32) * 4 : L.pctr + (2 + 2 * NB) * 4;
     return static_cast<size_t>(end - L.nnz);
 }
 
@@ -394,7 +406,8 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
                                 st) != cudaSuccess)
                 return SFFN_ERR_CUDA;
         }
-        const int split = union_prep_split(NB);
+        const int split = union_prep_split(NB), boost = union_prep_boost(NB, BR);
+        const int pctas = prep_ctas(static_cast<int>(NB), PERM_W / BR, split, boost);
         const size_t psmem = prep_smem_bytes(static_cast<int>(N), L.nchunk);
         static std::once_flag ponce;
         static cudaError_t pattr = cudaSuccess;
@@ -404,12 +417,12 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         });
         if (pattr != cudaSuccess) return SFFN_ERR_CUDA;
         const bool tma_dense = BR == 128 && N >= 256;
-        { union_prep_kernel<<<static_cast<unsigned>(NB * split), PREP_THREADS, psmem, st>>>(
+        { union_prep_kernel<<<static_cast<unsigned>(pctas), PREP_THREADS, psmem, st>>>(
             tw, (int)M, (int)N, T, C, um, perm, rnnz, reinterpret_cast<int*>(base + L.pctr),
-            env_int("SFFN_UP_GROUP", UNION_GROUP_UP), split, union_dense_units(N, tma_dense),
+            env_int("SFFN_UP_GROUP", union_group_up(NB)), split, boost, union_dense_units(N, tma_dense),
             union_dense_nnz(N, tma_dense), gated ? static_cast<const uint8_t*>(X) : nullptr, K * 2,
             (gated && !env_flag("SFFN_PREP_NOCOPY", false)) ? static_cast<uint8_t*>(xp) : nullptr, gated ? 1 : 0,
-            prep_trace_buf(NB * split)); note_launch(); }
+            prep_trace_buf(pctas)); note_launch(); }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
         if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)
             { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (BR / GS_ROWS)), 256, 0, st>>>(

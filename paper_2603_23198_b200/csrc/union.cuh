@@ -32,9 +32,12 @@ struct UnionMeta {
     int brows;           // token rows per union block: 128 (one tcgen05 M tile) or 256 (a CTA pair's M=256 tile)
 };
 
-constexpr int UNION_GROUP_UP = 8;    // token blocks whose up-GEMM tiles run together (L2 working set)
+// token blocks whose up-GEMM tiles run together (chunk-major within the group): NB / 8 clamped to [8, 32] — interleaved
+// A/B (profiles/r02/s3/ab_up_*.json): 32 vs 8 is 1.2-2% faster at 7B (NB = 256) and 70B (NB = 512), equal at 1B
+// (NB = 128, 16 there), and 8 stays best for the 4096-row chunks of the host pipeline (NB = 32)
+__host__ __device__ constexpr int union_group_up(int64_t NB) { return NB / 8 < 8 ? 8 : (NB / 8 > 32 ? 32 : static_cast<int>(NB / 8)); }
 constexpr int UNION_GROUP_DOWN = 4;   // token blocks whose down-GEMM tiles run together (4 vs 16: -0.9% forward, -2% e2e)
-constexpr int UNION_GROUP_MAX = 16;   // largest UP group the work-list builder supports
+constexpr int UNION_GROUP_MAX = 64;   // largest UP group the work-list builder supports
 
 // CTAs per union block of the prep kernel when M is small (a power of two dividing the block rows)
 constexpr int META_SPLIT_MAX = 8;
@@ -124,15 +127,9 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, Sync
     for (int base = 0; base < NG; base += NTH) {
         const int g = base + static_cast<int>(threadIdx.x);
         const int b0 = g * group;
-        int nchk[MAXG];  // chunks of each block of the group (registers: no dependent loads in the write loop)
-        int tot = 0, maxc = 0;
-#pragma unroll
-        for (int j = 0; j < MAXG; ++j) {
-            const int bb = b0 + j;
-            nchk[j] = (g < NG && j < group && bb < NB) ? (__ldcg(um.ulen + bb) + 255) / 256 : 0;
-            tot += nchk[j];
-            maxc = max(maxc, nchk[j]);
-        }
+        int tot = 0;  // tiles of this thread's group
+        if (g < NG)
+            for (int j = 0; j < group && b0 + j < NB; ++j) tot += (__ldcg(um.ulen + b0 + j) + 255) / 256;
         int sc = tot;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -153,11 +150,25 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, Sync
             if (lane == 31) wsum[NWP] = y;
         }
         sync();
-        int pos = carry + wsum[warp] + sc - tot;
-        for (int c = 0; c < maxc; ++c)
-#pragma unroll
-            for (int j = 0; j < MAXG; ++j)
-                if (c < nchk[j]) um.tiles[pos++] = ((b0 + j) << 8) | c;
+        const int pos = carry + wsum[warp] + sc - tot;  // first tile of this thread's group
+        // the warp writes its 32 groups one after the other: lane j (and j + 32) holds block j's chunk count, one
+        // ballot per chunk index places the group's blocks that have that chunk (chunk-major, block ascending)
+        const unsigned lt = (1u << lane) - 1u;
+        for (int i = 0; i < 32; ++i) {
+            const int gi = base + warp * 32 + i;
+            if (gi >= NG) break;  // warp-uniform
+            int p = __shfl_sync(0xffffffffu, pos, i);
+            const int bi = gi * group;
+            const int n0 = (lane < group && bi + lane < NB) ? (__ldcg(um.ulen + bi + lane) + 255) / 256 : 0;
+            const int n1 = (lane + 32 < group && bi + lane + 32 < NB) ? (__ldcg(um.ulen + bi + lane + 32) + 255) / 256 : 0;
+            const int mc = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(max(n0, n1))));
+            for (int c = 0; c < mc; ++c) {
+                const unsigned m0 = __ballot_sync(0xffffffffu, c < n0), m1 = __ballot_sync(0xffffffffu, c < n1);
+                if (c < n0) um.tiles[p + __popc(m0 & lt)] = ((bi + lane) << 8) | c;
+                if (c < n1) um.tiles[p + __popc(m0) + __popc(m1 & lt)] = ((bi + lane + 32) << 8) | c;
+                p += __popc(m0) + __popc(m1);
+            }
+        }
         carry += wsum[NWP];
         sync();
     }

@@ -1,5 +1,6 @@
-"""Interleaved A/B of a run-time env switch of the library (read per call, e.g. SFFN_GATE_DYN=0/1): the 7B
-forward (resident inputs, L2 flushed) and forward_host (e2e), alternating the setting every repetition."""
+"""Interleaved A/B of run-time env switches of the library (read per call, e.g. SFFN_GATE_DYN=0/1): the forward
+(resident inputs, L2 flushed) and forward_host (e2e) of config $CFG (default 7B), alternating the setting every
+repetition.  --var V --values a,b,c sweeps one variable; --arms "A=1,B=0;A=2,B=1" sets several per arm."""
 import argparse, json, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -12,9 +13,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--var", default="SFFN_GATE_DYN")
 ap.add_argument("--values", default="0,1")
 ap.add_argument("--reps", type=int, default=12)
+ap.add_argument("--arms", default="", help='";"-separated arms of ","-separated VAR=value settings')
 ap.add_argument("--rows", type=int, default=0, help="also time the forward on the first ROWS rows")
 a = ap.parse_args()
-cfg = synth.CONFIGS["7B"]
+cfg = synth.CONFIGS[os.environ.get("CFG", "7B")]
 M, K, N, T, C = cfg.M, cfg.K, cfg.N, cfg.T, cfg.C
 Xn = synth.gen_x(cfg, p=synth.token_targets(cfg))
 dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
@@ -27,7 +29,16 @@ Yh = torch.empty((M, K), dtype=torch.bfloat16).pin_memory()
 w1 = sffn.workspace_bytes(4096, K, N, T, C, "union")
 wsh = torch.empty((w1 + 1023) // 1024 * 1024 + w1, dtype=torch.uint8, device="cuda")
 flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
-vals = a.values.split(",")
+vals = a.arms.split(";") if a.arms else a.values.split(",")
+
+
+def setenv(v):
+    if a.arms:
+        for kv in v.split(","):
+            k, x = kv.split("=")
+            os.environ[k] = x
+    else:
+        os.environ[a.var] = v
 arms = {"forward": lambda: sffn.forward(X, Wg, Wu, Wd, T, C, out=Y, workspace=ws, algo="union"),
         "e2e": lambda: sffn.forward_host(Xh, Wg, Wu, Wd, T, C, out=Yh, workspace=wsh, algo="union")}
 if a.rows:
@@ -45,16 +56,16 @@ def once(fn):
 
 res = {(k, v): [] for k in arms for v in vals}
 for v in vals:
-    os.environ[a.var] = v
+    setenv(v)
     for f in arms.values():
         f(); f()
 torch.cuda.synchronize()
 for r in range(a.reps):
     for v in (vals if r % 2 == 0 else vals[::-1]):
-        os.environ[a.var] = v
+        setenv(v)
         for k, f in arms.items():
             res[(k, v)].append(once(f))
-out = {"var": a.var, "reps": a.reps}
+out = {"var": a.arms or a.var, "reps": a.reps, "config": os.environ.get("CFG", "7B")}
 for (k, v), t in res.items():
     out[f"{k}[{v}]_ms"] = round(float(np.median(t)), 4)
 print(json.dumps(out), flush=True)
