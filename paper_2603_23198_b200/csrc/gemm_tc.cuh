@@ -108,6 +108,12 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn_tc(uint32_t smem_addr) {
     return d;
 }
 
+#ifdef SFFN_GEMM_EPI_TRACE  // probe builds only (tools/s3_epi_trace.py): cycle sums of the roles per tile
+// [0] epilogue warp cycles (tfull passed -> accumulator released), [1] epilogue warp-tiles, [2] MMA cycles per tile
+// (tempty passed -> last commit issued), [3] tiles, [4] MMA thread cycles waiting on tempty
+static __device__ unsigned long long g_gemm_trace[8];
+#endif
+
 template <int GROUP = GEMM_GROUP_M>
 __device__ __forceinline__ void gemm_tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
     const int group = tile / (GROUP * num_n);
@@ -291,8 +297,14 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
             for (int it = 0;; ++it) {
                 const int tile = next_tile(it, ridx, rphase, true);
                 if (tile < 0) break;
+#ifdef SFFN_GEMM_EPI_TRACE
+                const long long tw0 = clock64();
+#endif
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
+#ifdef SFFN_GEMM_EPI_TRACE
+                const long long tm0 = clock64();
+#endif
                 const uint32_t d = tmem_base + static_cast<uint32_t>(acc * GEMM_BN);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
@@ -320,6 +332,14 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
                 }
                 if (PAIR == 2) umma_commit_pair(&tfull[acc]);
                 else umma_commit(&tfull[acc]);
+#ifdef SFFN_GEMM_EPI_TRACE
+                if (EPI == EPI_TWELL) {
+                    const long long tm1 = clock64();
+                    atomicAdd(&g_gemm_trace[2], static_cast<unsigned long long>(tm1 - tm0));
+                    atomicAdd(&g_gemm_trace[3], 1ull);
+                    atomicAdd(&g_gemm_trace[4], static_cast<unsigned long long>(tm0 - tw0));
+                }
+#endif
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -349,6 +369,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
             const int row0 = mb * PM + static_cast<int>(rank) * GEMM_BM + ew * 32;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+#ifdef SFFN_GEMM_EPI_TRACE
+            const long long te0 = clock64();
+#endif
             const uint32_t tb = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * GEMM_BN);
             if (EPI != EPI_F32) {
                 if (lane == 0) bulk_wait_read0();  // staging buffer free (previous TMA store has read it)
@@ -449,6 +472,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(acc);
+#ifdef SFFN_GEMM_EPI_TRACE
+                if (lane == 0) {
+                    atomicAdd(&g_gemm_trace[0], static_cast<unsigned long long>(clock64() - te0));
+                    atomicAdd(&g_gemm_trace[1], 1ull);
+                }
+#endif
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {

@@ -644,6 +644,14 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
 // Internal (not in include/sffn.h): sffn_forward (UNION) whose DOWN GEMM writes the partial Y into this rank's
 // symmetric window (Y) and reduces 2048-row windows across the ranks as they complete (sffn_comm.cu).
 // Internal (tools): the prep kernel's per-CTA phase timestamps of the last traced call (SFFN_PREP_TRACE=1).
+#ifdef SFFN_GEMM_EPI_TRACE
+// Internal (probe builds): the gate GEMM role cycle sums (g_gemm_trace), copied out and reset
+int sffn__gemm_trace(unsigned long long* host) {
+    if (cudaMemcpyFromSymbol(host, g_gemm_trace, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(g_gemm_trace, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif
 int64_t sffn__prep_trace(unsigned long long* host, int64_t cap) {
     if (!g_prep_trace) return 0;
     const int64_t n = cap < g_prep_trace_n ? cap : g_prep_trace_n;
