@@ -5,6 +5,8 @@
 //      bmode 0: cp.async.cg 16 B, 8 lanes per row segment (the union kernels' producer mapping)
 //      bmode 1: one TMA 2-D box {64, 1} per row (128B swizzle by address), issued by the gather warps' lanes
 //      bmode 2: ld.global.v4 to registers + st.shared (LSU round trip) with the stage's mbarrier arrive
+//      bmode 4: as 2 with 4 independent 16-byte loads per lane in flight before the stores (batched LSU)
+//      bmode 5: 256-bit loads (ld.global.nc.v8, 4 lanes per 128-byte row segment), 4 per lane in flight, 2 x st.shared.v4
 // A consumer thread waits for each stage, spins `delay` SM cycles (the MMA time it would take), frees the stage.
 // Prints achieved bytes per SM cycle and the stage time.  Not part of the library.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/exp_feed tools/exp_feed.cu
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__(32 * 26, 1) k_feed(const __grid_constant__ CUt
     __shared__ int ntl;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NW = p.nw;
-    const bool lsu_b = p.brows > 0 && p.bmode != 1;
+    const bool lsu_b = p.brows > 0 && p.bmode != 1;  // bmodes 0, 2, 3, 4, 5: every gather thread arrives
     const int tma_rows = p.bmode == 1 ? p.brows : (p.bmode == 3 ? p.brows - p.tsplit : 0);
     const int lsu_rows = p.bmode == 3 ? p.tsplit : p.brows;
     if (threadIdx.x == 0) {
@@ -124,6 +126,49 @@ __global__ void __launch_bounds__(32 * 26, 1) k_feed(const __grid_constant__ CUt
                 } else if (p.bmode == 1) {
                     for (int r = 32 * gw + lane; r < p.brows; r += 32 * NW)
                         tma_row(stB + st * BMAX + r * 128, &tW, &full[st], kb * KB, __ldg(u + r));
+                } else if (p.bmode == 4) {
+                    const int cl = lane & 7, sub = lane >> 3;
+                    for (int r0 = 4 * gw + sub; r0 < p.brows; r0 += 16 * NW) {
+                        uint4 v[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = r0 + 4 * NW * j;
+                            if (r < p.brows)
+                                v[j] = __ldcg(reinterpret_cast<const uint4*>(p.W + static_cast<int64_t>(__ldg(u + r)) * p.K + kb * KB + 8 * cl));
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = r0 + 4 * NW * j;
+                            if (r < p.brows) *reinterpret_cast<uint4*>(stB + st * BMAX + r * 128 + ((cl ^ (r & 7)) << 4)) = v[j];
+                        }
+                    }
+                    mbar_arrive(&full[st]);
+                } else if (p.bmode == 5) {
+                    const int cl = lane & 3, sub = lane >> 2;
+                    for (int r0 = 8 * gw + sub; r0 < p.brows; r0 += 32 * NW) {
+                        uint32_t v[4][8];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = r0 + 8 * NW * j;
+                            if (r < p.brows) {
+                                const uint16_t* src = p.W + static_cast<int64_t>(__ldg(u + r)) * p.K + kb * KB + 16 * cl;
+                                asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                             : "=r"(v[j][0]), "=r"(v[j][1]), "=r"(v[j][2]), "=r"(v[j][3]), "=r"(v[j][4]),
+                                               "=r"(v[j][5]), "=r"(v[j][6]), "=r"(v[j][7])
+                                             : "l"(src));
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = r0 + 8 * NW * j;
+                            if (r < p.brows) {
+                                uint8_t* rb = stB + st * BMAX + r * 128;
+                                *reinterpret_cast<uint4*>(rb + (((2 * cl) ^ (r & 7)) << 4)) = make_uint4(v[j][0], v[j][1], v[j][2], v[j][3]);
+                                *reinterpret_cast<uint4*>(rb + (((2 * cl + 1) ^ (r & 7)) << 4)) = make_uint4(v[j][4], v[j][5], v[j][6], v[j][7]);
+                            }
+                        }
+                    }
+                    mbar_arrive(&full[st]);
                 } else {
                     const int cl = lane & 7, sub = lane >> 3;
                     for (int r = 4 * gw + sub; r < p.brows; r += 4 * NW) {
@@ -197,6 +242,20 @@ int main(int argc, char** argv) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     struct Cfg { const char* name; int abytes, brows, bmode, delay, nw, tsplit, grid = 0; };
     std::vector<Cfg> cfgs = {
+        {"B256 cp.async 8 warps", 0, 256, 0, 0, 8, 0},
+        {"B256 cp.async 16 warps", 0, 256, 0, 0, 16, 0},
+        {"B256 LSU 16B x1 8 warps", 0, 256, 2, 0, 8, 0},
+        {"B256 LSU 16B x4 8 warps", 0, 256, 4, 0, 8, 0},
+        {"B256 LSU 16B x4 16 warps", 0, 256, 4, 0, 16, 0},
+        {"B256 LSU 32B x4 8 warps", 0, 256, 5, 0, 8, 0},
+        {"B256 LSU 32B x4 16 warps", 0, 256, 5, 0, 16, 0},
+        {"A + B256 cp.async 8 warps", ABYTES, 256, 0, 0, 8, 0},
+        {"A + B256 LSU 16B x4 8 warps", ABYTES, 256, 4, 0, 8, 0},
+        {"A + B256 LSU 32B x4 8 warps", ABYTES, 256, 5, 0, 8, 0},
+        {"A + B256 LSU 32B x4 16 warps", ABYTES, 256, 5, 0, 16, 0},
+        {"A + B128 LSU 32B x4 8 warps", ABYTES, 128, 5, 0, 8, 0},
+    };
+    if (argc > 1) cfgs.insert(cfgs.end(), {
         {"A + B256 cp.async 16 warps, 148 CTAs", ABYTES, 256, 0, 0, 16, 0, 148},
         {"A + B256 cp.async 16 warps, 74 CTAs", ABYTES, 256, 0, 0, 16, 0, 74},
         {"A + B256 cp.async 16 warps, 37 CTAs", ABYTES, 256, 0, 0, 16, 0, 37},
@@ -221,7 +280,7 @@ int main(int argc, char** argv) {
         {"A + B128 cp.async 96 + TMA 32, 16 w", ABYTES, 128, 3, 0, 16, 96},
         {"A + B128 cp.async 16 w, delay 512", ABYTES, 128, 0, 512, 16, 0},
         {"A + B256 cp.async 16 w, delay 512", ABYTES, 256, 0, 512, 16, 0},
-    };
+    });
     for (auto& c : cfgs) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaMemset(cnt, 0, 4);
