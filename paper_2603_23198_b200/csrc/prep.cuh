@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     if (trace && t == 0) trace[8 * lid] = gtimer();
     int b, part;
     const int split = prep_map(lid, NB, PERM_W / BR, split_base, split_boost, &b, &part);
+    if (split == 0) return;  // more CTAs than prep_ctas() (launch error): uniform across the CTA, nothing to do
     const int PR = BR / split;
     // part `part` owns the block rows part, part + split, part + 2 split, ...: the rows are in descending-nnz order,
     // so interleaving balances the parts' work (contiguous ranges gave part 0 the densest rows and made every
