@@ -111,13 +111,14 @@ __device__ __forceinline__ int tile_count(const uint32_t* __restrict__ row, int 
 
 // UP work list (run by the last block builder of the prep kernel): for each group
 // of `group` blocks, chunk-major then block: tiles[] = (b << 8) | c; chunk_off[0] = total tiles; zeroes the two
-// dynamic tile-scheduler counters.  NTH threads (thread ids 0..NTH-1, all in full warps), scratch = NTH/32 + 1 ints of
-// shared memory; `sync` is a barrier over exactly those threads (__syncthreads or a named barrier).
+// dynamic tile-scheduler counters.  NTH threads (thread ids 0..NTH-1, all in full warps), scratch wsum = NTH/32 + 1
+// and goff = NTH ints of shared memory; `sync` is a barrier over exactly those threads (__syncthreads or a named
+// barrier).
 struct SyncAll {
     __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
 template <int NTH, class Sync = SyncAll>
-__device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, Sync sync = Sync()) {
+__device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, int* goff, Sync sync = Sync()) {
     constexpr int NWP = NTH / 32;
     constexpr int MAXG = UNION_GROUP_MAX;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -127,9 +128,18 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, Sync
     for (int base = 0; base < NG; base += NTH) {
         const int g = base + static_cast<int>(threadIdx.x);
         const int b0 = g * group;
-        int tot = 0;  // tiles of this thread's group
+        int tot = 0;  // tiles of this thread's group (16 independent loads in flight per batch)
         if (g < NG)
-            for (int j = 0; j < group && b0 + j < NB; ++j) tot += (__ldcg(um.ulen + b0 + j) + 255) / 256;
+            for (int j0 = 0; j0 < group; j0 += 16) {
+                int l[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int bb = b0 + j0 + j;
+                    l[j] = (j0 + j < group && bb < NB) ? (__ldcg(um.ulen + bb) + 255) / 256 : 0;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) tot += l[j];
+            }
         int sc = tot;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -150,14 +160,14 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, Sync
             if (lane == 31) wsum[NWP] = y;
         }
         sync();
-        const int pos = carry + wsum[warp] + sc - tot;  // first tile of this thread's group
-        // the warp writes its 32 groups one after the other: lane j (and j + 32) holds block j's chunk count, one
+        goff[threadIdx.x] = carry + wsum[warp] + sc - tot;  // first tile of this thread's group
+        sync();
+        // warp w writes groups w, w + NWP, ... of this round: lane j (and j + 32) holds block j's chunk count, one
         // ballot per chunk index places the group's blocks that have that chunk (chunk-major, block ascending)
         const unsigned lt = (1u << lane) - 1u;
-        for (int i = 0; i < 32; ++i) {
-            const int gi = base + warp * 32 + i;
-            if (gi >= NG) break;  // warp-uniform
-            int p = __shfl_sync(0xffffffffu, pos, i);
+        for (int i = warp; i < NTH && base + i < NG; i += NWP) {
+            const int gi = base + i;
+            int p = goff[i];
             const int bi = gi * group;
             const int n0 = (lane < group && bi + lane < NB) ? (__ldcg(um.ulen + bi + lane) + 255) / 256 : 0;
             const int n1 = (lane + 32 < group && bi + lane + 32 < NB) ? (__ldcg(um.ulen + bi + lane + 32) + 255) / 256 : 0;
