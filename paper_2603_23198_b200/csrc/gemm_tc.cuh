@@ -44,13 +44,20 @@ template <int EPI, int C>
 __host__ __device__ constexpr int gemm_epi_warp_bytes() {
     return EPI == EPI_TWELL ? 32 * (GEMM_BN / C) * 4 : (EPI == EPI_F32 ? 0 : 32 * 128 * 2);  // GLU/BF16/BF16_MN
 }
-// Epilogue warp groups: 2 for the TwELL epilogue when its staging is small (C >= 8): group g (warps 4+4g .. 7+4g)
-// drains accumulator g, i.e. every other tile, so each group has two mainloops of time per tile.  At K = 2048
-// (1B) the single group did not keep up: the MMA thread spun on the accumulator-free barrier (ncu: 633k spins)
-// and the tensor pipe was 69% active.  Other epilogues: 1 group (warps 4-7, alternating accumulators).
+// Epilogue warp groups: SFFN_TWELL_EPI_GROUPS = 2 gives the TwELL epilogue (C >= 8) two groups — group g (warps
+// 4+4g .. 7+4g) drains accumulator g, i.e. every other tile, two mainloops of time per tile.  Round 2 needed it at
+// K = 2048 (1B) before the sparse set-bit walk: one group did not keep up (MMA thread spinning on the accumulator-free
+// barrier, ncu 633k spins; tensor pipe 69%).  Other epilogues: 1 group (warps 4-7, alternating accumulators).
+// Session 3: ONE group — a TwELL epilogue warp-tile takes 9.45 K cycles against a 35.5 K-cycle pair-tile mainloop at
+// K = 4096 (18.5 K at K = 2048), so one group keeps up since the sparse set-bit walk; with one group and 5 ring stages
+// the gate GEMM runs 0.6% (7B) / 3.9% (70B) faster (ncu, profiles/r02/s3/ncu_gate_epi.txt) and leaves 16 KB of SMEM
+// and 128 threads' registers per SM free
+#ifndef SFFN_TWELL_EPI_GROUPS
+#define SFFN_TWELL_EPI_GROUPS 1
+#endif
 template <int EPI, int C>
 __host__ __device__ constexpr int gemm_epi_groups() {
-    return (EPI == EPI_TWELL && gemm_epi_warp_bytes<EPI, C>() <= 4096) ? 2 : 1;
+    return (EPI == EPI_TWELL && gemm_epi_warp_bytes<EPI, C>() <= 4096) ? SFFN_TWELL_EPI_GROUPS : 1;
 }
 template <int EPI, int C>
 __host__ __device__ constexpr int gemm_threads() {
@@ -63,11 +70,21 @@ template <int PAIR>
 __host__ __device__ constexpr int gemm_stage_bytes() {
     return GEMM_A_BYTES + GEMM_B_BYTES / PAIR;
 }
+#ifndef SFFN_GEMM_STAGES_MAX
+#define SFFN_GEMM_STAGES_MAX 6
+#endif
+#ifndef SFFN_TWELL_STAGES_MAX
+#define SFFN_TWELL_STAGES_MAX 5  // gate GEMM ring: 5 stages measured as fast as 6 (4: +1%), session 3
+#endif
+template <int EPI>
+__host__ __device__ constexpr int gemm_stages_max() {
+    return EPI == EPI_TWELL ? SFFN_TWELL_STAGES_MAX : SFFN_GEMM_STAGES_MAX;
+}
 template <int EPI, int C, int PAIR = 1>
 __host__ __device__ constexpr int gemm_stages() {
     return (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_groups<EPI, C>() * gemm_epi_warp_bytes<EPI, C>()) /
-                       gemm_stage_bytes<PAIR>() > 6
-               ? 6
+                       gemm_stage_bytes<PAIR>() > gemm_stages_max<EPI>()
+               ? gemm_stages_max<EPI>()
                : (GEMM_SMEM_LIMIT - 1024 - 256 - 4 * gemm_epi_groups<EPI, C>() * gemm_epi_warp_bytes<EPI, C>()) /
                      gemm_stage_bytes<PAIR>();
 }
