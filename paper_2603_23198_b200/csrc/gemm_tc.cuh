@@ -107,6 +107,9 @@ struct GemmArgs {
     int* row_nnz;        // EPI_TWELL, may be null: += stored entries (min(count, cap)) of each row (zeroed by caller)
     int* tile_ctr;       // optional dynamic tile scheduler: tiles claimed in raster order by atomicAdd on this
                          // counter (zeroed by the caller); null: static striding (tile += grid)
+    int* win_done;       // EPI_TWELL, may be null: per 2048-row window, += 1 per epilogue warp-tile whose TwELL store
+                         // and row counts are complete and visible (the prep kernel, launched as a programmatic
+                         // dependent, starts a window when its count reaches ceil(rows / 32) * num_n)
 };
 constexpr int GT_RING = 4;  // dynamic scheduler: tile ring depth (claims ahead of the slowest reader)
 #ifndef SFFN_TWELL_SPARSE_MAX
@@ -179,6 +182,9 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
     const int nk = (args.K + GEMM_BK - 1) / GEMM_BK;
     const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0u;  // CTA rank in the pair (0 = leader / MMA issuer)
     const int first_tile = blockIdx.x / PAIR, tile_step = gridDim.x / PAIR;
+    // programmatic dependent launch: once every CTA is resident, a dependent kernel (the prep kernel, which waits on
+    // win_done per window instead of on this grid's completion) may be scheduled on the remaining SM resources
+    if (args.win_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmA);
@@ -486,6 +492,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
                     }
                 }
                 if (args.row_nnz && row_ok && stored) atomicAdd(args.row_nnz + row0 + lane, stored);
+                if (args.win_done) __threadfence();  // the row counts before the window signal below
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(acc);
@@ -507,6 +514,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI, C>(), 1)
                         tma_store_2d_hint(&tmOut, stg, nb * ROW_WORDS, row0, policy_evict_first());
                     }
                     bulk_commit();
+                    if (args.win_done && row0 < args.M) {
+                        // the store complete (writes performed), ordered before the generic-proxy signal, released
+                        bulk_wait0();
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        __threadfence();
+                        atomicAdd(args.win_done + (row0 >> 11), 1);
+                    }
                 }
             } else if constexpr (EPI == EPI_F32) {
                 const int row = row0 + lane;

@@ -24,7 +24,7 @@ namespace sffn {
 constexpr int PREP_THREADS = 512;
 constexpr int PREP_WORK = PREP_THREADS - 32;  // warps 0-14: OR / build / gate lists; warp 15: X copy
 constexpr int PREP_NW = PREP_WORK / 32;
-constexpr int PREP_SLOTS = 8, PREP_PIECE = 8192;  // X copy ring
+constexpr int PREP_SLOTS = 8, PREP_PIECE = 8192;  // X copy ring: 8 slots of `piece` bytes (8 KB standalone)
 constexpr int PREP_U = 2;   // TwELL tiles per lane per row in flight (56 tiles per row at N = 14336, T = 256)
 constexpr int PREP_RR = 2;  // rows per warp in flight in the OR pass
 constexpr int PREP_UD = 1;  // dense path: tiles per lane in flight (4 x 16 bytes each)
@@ -54,10 +54,20 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 
-// dynamic SMEM: ring PREP_SLOTS x 8 KB | keys 2048 x 2 ints | mask NW | woff NW | gate-list chunk counters
-// PREP_NW x (nchunk + 1) | wsum
-inline size_t prep_smem_bytes(int N, int nchunk) {
-    return 1024 + PREP_SLOTS * PREP_PIECE + 2 * 2048 * 4 + 2 * (N / 32) * 4 + PREP_NW * (nchunk + 1) * 4 + 64 * 4;
+// dynamic SMEM: ring PREP_SLOTS x piece (the sort's keys, 2 x 2048 ints, live in it before the X copy starts: piece
+// >= 2 KB) | mask NW | woff NW | gate-list chunk counters PREP_NW x (nchunk + 1) | wsum | work-list group offsets
+inline size_t prep_smem_bytes(int N, int nchunk, int piece = PREP_PIECE) {
+    return 1024 + static_cast<size_t>(PREP_SLOTS) * piece + 2 * (N / 32) * 4 + PREP_NW * (nchunk + 1) * 4 + 64 * 4 +
+           PREP_WORK * 4;
+}
+// static SMEM of the prep kernel (mbarriers, per-row tables, scalars), for the host's co-residency budget
+constexpr int PREP_STATIC_SMEM = PREP_SLOTS * 8 + 2 * 256 * 4 + 16;
+// loads of what the gate GEMM wrote (TwELL, row counts): read-only path standalone; L2 (coherent) when the prep
+// kernel runs concurrently with the gate GEMM (OV), whose writes it observes through the window counters
+template <bool OV, class Tp>
+__device__ __forceinline__ Tp pld(const Tp* p) {
+    if constexpr (OV) return __ldcg(p);
+    else return __ldg(p);
 }
 
 // Parts (CTAs) per block: the base split (small M) times a boost for the densest blocks of each 2048-row window —
@@ -88,6 +98,41 @@ __host__ __device__ inline int prep_map(int lid, int NB, int WB, int base, int b
     *part = 0;
     return 0;
 }
+// Overlapped prep (OV): window-major ids (window w's CTAs start before window w+1's, so the CTAs resident beside the
+// gate GEMM are those of the windows it finishes first), each window's blocks in position order; the windows of the
+// gate GEMM's last raster group (w >= tail_w0: they complete when the GEMM ends and are then the critical path) get
+// tail_split parts per block, the others prep_parts(bw, base, boost)
+__host__ __device__ inline int prep_map_ov(int lid, int NB, int WB, int base, int boost, int tail_w0, int tail_split,
+                                           int* b, int* part) {
+    const int NWIN = (NB + WB - 1) / WB;
+    int rem = lid;
+    for (int w = 0; w < NWIN; ++w) {
+        const int nbw = min(WB, NB - w * WB);
+        int wp = 0;
+        for (int bw = 0; bw < nbw; ++bw) wp += w >= tail_w0 ? tail_split : prep_parts(bw, base, boost);
+        if (rem >= wp) {
+            rem -= wp;
+            continue;
+        }
+        for (int bw = 0; bw < nbw; ++bw) {
+            const int sp = w >= tail_w0 ? tail_split : prep_parts(bw, base, boost);
+            if (rem < sp) {
+                *b = w * WB + bw;
+                *part = rem;
+                return sp;
+            }
+            rem -= sp;
+        }
+    }
+    *b = -1;
+    *part = 0;
+    return 0;
+}
+inline int prep_ctas_ov(int NB, int WB, int base, int boost, int tail_w0, int tail_split) {
+    int n = 0;
+    for (int b = 0; b < NB; ++b) n += (b / WB) >= tail_w0 ? tail_split : prep_parts(b % WB, base, boost);
+    return n;
+}
 inline int prep_ctas(int NB, int WB, int base, int boost) {
     int n = 0;
     const int NWIN = (NB + WB - 1) / WB;
@@ -95,19 +140,29 @@ inline int prep_ctas(int NB, int WB, int base, int boost) {
     return n;
 }
 
+// OV: launched as a programmatic dependent of the gate GEMM (which must have been given win_done); every CTA waits
+// for its window's count before reading the window's row counts and TwELL rows
+struct PrepOv {
+    const int* win_done;  // per 2048-row window: epilogue warp-tiles done (gate GEMM), null standalone
+    int win_n;            // gate GEMM N-tiles (a window is complete at ceil(rows / 32) * win_n)
+    int tail_w0, tail_split;
+};
+template <bool OV>
 __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     const uint32_t* __restrict__ tw, int M, int N, int T, int C, UnionMeta um, int32_t* __restrict__ perm,
-    const int* __restrict__ rnnz, int* __restrict__ pctr, int up_group, int split_base, int split_boost, int dense_units, int64_t dense_nnz,
+    const int* __restrict__ rnnz, int* __restrict__ pctr, int up_group, int split_base, int split_boost, int piece,
+    PrepOv ov, int dense_units, int64_t dense_nnz,
     const uint8_t* __restrict__ X, int64_t row_bytes, uint8_t* __restrict__ Xp, int gate_lists,
     unsigned long long* trace) {
     extern __shared__ uint8_t prep_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(prep_raw) + 1023) & ~uintptr_t(1023));
-    int* key = reinterpret_cast<int*>(ring + PREP_SLOTS * PREP_PIECE);  // [2][2048]
+    int* key = reinterpret_cast<int*>(ring);  // [2][2048], in the ring until the X copy starts (after the OR pass)
     const int NW = N >> 5;
-    uint32_t* mask = reinterpret_cast<uint32_t*>(key + 2 * PERM_W);       // [NW]
+    uint32_t* mask = reinterpret_cast<uint32_t*>(ring + PREP_SLOTS * piece);  // [NW]
     int32_t* woff = reinterpret_cast<int32_t*>(mask + NW);                // [NW]
     int32_t* ccnt = woff + NW;                                            // [PREP_NW][nchunk + 1]
     int32_t* wsum = ccnt + PREP_NW * (um.nchunk + 1);                     // [PREP_NW + 1]
+    int32_t* goff = wsum + 64;                                            // [PREP_WORK] work-list group offsets
     __shared__ uint64_t full[PREP_SLOTS];
     __shared__ int s_prow[256], s_rcnt[256];
     __shared__ int s_lid, s_last, s_bsum;
@@ -125,9 +180,25 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
     const int lid = s_lid;
     if (trace && t == 0) trace[8 * lid] = gtimer();
     int b, part;
-    const int split = prep_map(lid, NB, PERM_W / BR, split_base, split_boost, &b, &part);
+    const int split = OV ? prep_map_ov(lid, NB, PERM_W / BR, split_base, split_boost, ov.tail_w0, ov.tail_split, &b, &part)
+                         : prep_map(lid, NB, PERM_W / BR, split_base, split_boost, &b, &part);
     if (split == 0) return;  // more CTAs than prep_ctas() (launch error): uniform across the CTA, nothing to do
     const int PR = BR / split;
+    if constexpr (OV) {
+        // the window's TwELL rows and row counts are complete once every epilogue warp-tile of its rows has signalled
+        // (gate GEMM: TMA store waited, fenced, then the atomic); acquire, then L2 loads (pld<true>)
+        if (t == 0) {
+            const int w = (b * BR) / PERM_W;
+            const int need = ((min(PERM_W, M - w * PERM_W) + 31) / 32) * ov.win_n;
+            int v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ov.win_done + w) : "memory");
+                if (v >= need) break;
+                __nanosleep(500);
+            }
+        }
+        __syncthreads();
+    }
     // part `part` owns the block rows part, part + split, part + 2 split, ...: the rows are in descending-nnz order,
     // so interleaving balances the parts' work (contiguous ranges gave part 0 the densest rows and made every
     // other part wait for it at the merge)
@@ -145,7 +216,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         const int i = 4 * t + s;
-        v[s] = i < wrows ? (__ldg(rnnz + w0 + i) << 11) | (PERM_W - 1 - i) : -1;
+        v[s] = i < wrows ? (pld<OV>(rnnz + w0 + i) << 11) | (PERM_W - 1 - i) : -1;
     }
     {
         auto cx = [](int p, int j, int k, int mine, int other) {
@@ -214,12 +285,12 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
         if (lane == 0 && Xp && rows > 0) {
             constexpr int LA = PREP_SLOTS - 2;  // loads in flight; the slot reused next was stored 2 pieces ago
             const uint64_t pol = policy_evict_first();  // X is read once here
-            const int per_row = static_cast<int>((row_bytes + PREP_PIECE - 1) / PREP_PIECE);
+            const int per_row = static_cast<int>((row_bytes + piece - 1) / piece);
             const int n = rows * per_row;
-            auto piece = [&](int i, const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
+            auto piece_at = [&](int i, const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
                 const int r = i / per_row, q = i % per_row;
-                const int64_t off = static_cast<int64_t>(q) * PREP_PIECE;
-                bytes = static_cast<uint32_t>((row_bytes - off < PREP_PIECE ? row_bytes - off : static_cast<int64_t>(PREP_PIECE)));
+                const int64_t off = static_cast<int64_t>(q) * piece;
+                bytes = static_cast<uint32_t>((row_bytes - off < piece ? row_bytes - off : static_cast<int64_t>(piece)));
                 src = X + static_cast<int64_t>(s_prow[r]) * row_bytes + off;
                 dst = Xp + prow(r) * row_bytes + off;
             };
@@ -227,10 +298,10 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
                 const uint8_t* src;
                 uint8_t* dst;
                 uint32_t bytes;
-                piece(i, src, dst, bytes);
+                piece_at(i, src, dst, bytes);
                 const int sl = i % PREP_SLOTS;
                 mbar_arrive_expect_tx(&full[sl], bytes);
-                bulk_g2s(ring + sl * PREP_PIECE, src, bytes, &full[sl], pol);
+                bulk_g2s(ring + sl * piece, src, bytes, &full[sl], pol);
             };
             for (int i = 0; i < min(n, LA); ++i) load(i);
             for (int i = 0; i < n; ++i) {
@@ -241,8 +312,16 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
                 const uint8_t* src;
                 uint8_t* dst;
                 uint32_t bytes;
-                piece(i, src, dst, bytes);
-                bulk_s2g(dst, ring + sl * PREP_PIECE, bytes);
+                piece_at(i, src, dst, bytes);
+                if constexpr (OV) {
+                    // beside the gate GEMM: keep its X / W_g tiles in L2 (X_pi is re-read only after the GEMM)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                                     dst),
+                                 "r"(smem_u32(ring + sl * piece)), "r"(bytes), "l"(pol)
+                                 : "memory");
+                } else {
+                    bulk_s2g(dst, ring + sl * piece, bytes);
+                }
                 bulk_commit();
                 if (i + LA < n) {
                     bulk_wait_read<PREP_SLOTS - LA>();  // the store of piece i + LA - PREP_SLOTS has read its slot
@@ -279,7 +358,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     a[u][q] = make_uint4(0, 0, 0, 0);
-                    if (tt < NT) a[u][q] = __ldg(reinterpret_cast<const uint4*>(row + static_cast<int64_t>(tt) * WPT + 4 * q));
+                    if (tt < NT) a[u][q] = pld<OV>(reinterpret_cast<const uint4*>(row + static_cast<int64_t>(tt) * WPT + 4 * q));
                 }
             }
 #pragma unroll
@@ -308,7 +387,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
                 }
                 if (tt < NT)
                     for (int e4 = 16; e4 <= cnt; e4 += 4) {
-                        const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(row + static_cast<int64_t>(tt) * WPT + e4));
+                        const uint4 v4 = pld<OV>(reinterpret_cast<const uint4*>(row + static_cast<int64_t>(tt) * WPT + e4));
                         put(v4.x, e4 - 1);
                         if (e4 + 1 <= cnt) put(v4.y, e4);
                         if (e4 + 2 <= cnt) put(v4.z, e4 + 1);
@@ -343,10 +422,10 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
                     if (tt < NT && rowp[q]) {
                         const uint32_t* blk = rowp[q] + static_cast<int64_t>(tt) * WPT;
                         if ((WPT & 3) == 0) {
-                            a[q][u] = __ldg(reinterpret_cast<const uint4*>(blk));
-                            if (WPT >= 8) a2[q][u] = __ldg(reinterpret_cast<const uint4*>(blk + 4));
+                            a[q][u] = pld<OV>(reinterpret_cast<const uint4*>(blk));
+                            if (WPT >= 8) a2[q][u] = pld<OV>(reinterpret_cast<const uint4*>(blk + 4));
                         } else {
-                            a[q][u].x = __ldg(blk);
+                            a[q][u].x = pld<OV>(blk);
                         }
                     }
                 }
@@ -379,14 +458,14 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
                             if (cnt >= 6) put(a2[q][u].z, 5);
                             if (cnt >= 7) put(a2[q][u].w, 6);
                             for (int e4 = 8; e4 <= cnt; e4 += 4) {
-                                const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(blk + e4));
+                                const uint4 v4 = pld<OV>(reinterpret_cast<const uint4*>(blk + e4));
                                 put(v4.x, e4 - 1);
                                 if (e4 + 1 <= cnt) put(v4.y, e4);
                                 if (e4 + 2 <= cnt) put(v4.z, e4 + 1);
                                 if (e4 + 3 <= cnt) put(v4.w, e4 + 2);
                             }
                         } else {
-                            for (int e = 0; e < cnt; ++e) put(__ldg(blk + 1 + e), e);
+                            for (int e = 0; e < cnt; ++e) put(pld<OV>(blk + 1 + e), e);
                         }
                     }
                     base[q] += __shfl_sync(0xffffffffu, inc, 31);
@@ -487,7 +566,7 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
         prep_sync();
         if (s_last) {  // the last block built: the UP work list from every block's ulen
             __threadfence();
-            union_scan_body<PREP_WORK>(um, NB, up_group, wsum, key, PrepSync());  // key: free after the sort
+            union_scan_body<PREP_WORK>(um, NB, up_group, wsum, goff, PrepSync());
         }
     } else {
         // wait for the block's builder (it is running: it arrived after this part), then its mask and offsets

@@ -105,7 +105,12 @@ int launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& b
     constexpr int smem = gemm_smem_bytes<EPI, C, PAIR>();
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (attr_err == cudaSuccess)  // the same carveout as the overlapped prep kernel (co-residency)
+            attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared);
+    });
     if (attr_err != cudaSuccess) return SFFN_ERR_CUDA;
     args.num_m = (args.M + GEMM_BM * PAIR - 1) / (GEMM_BM * PAIR);
     args.num_n = (args.N + n_tile_cols - 1) / n_tile_cols;
@@ -143,7 +148,8 @@ int check_device() {
 }
 
 int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, int T, int C, uint32_t* twell,
-              uint32_t* d_overflow, cudaStream_t st, int* row_nnz = nullptr, int* tile_ctr = nullptr) {
+              uint32_t* d_overflow, cudaStream_t st, int* row_nnz = nullptr, int* tile_ctr = nullptr,
+              int* win_done = nullptr) {
     // CTA-pair gate GEMM by default (SFFN_GATE_PAIR=0 selects the single-CTA kernel)
     static const bool pair = env_flag("SFFN_GATE_PAIR", true);
     CUtensorMap ta, tb, to;
@@ -163,6 +169,7 @@ int pack_impl(const void* X, const void* Wg, int64_t M, int64_t K, int64_t N, in
     args.overflow = d_overflow;
     args.row_nnz = row_nnz;
     args.tile_ctr = env_flag("SFFN_GATE_DYN", false) ? tile_ctr : nullptr;  // measured neutral: off
+    args.win_done = win_done;
 #define SFFN_PACK_CASE(CC)                                                                              \
     case CC:                                                                                            \
         return pair ? launch_gemm<EPI_TWELL, CC, 2>(ta, tb, tb, to, args, GEMM_BN, st)                  \
@@ -262,7 +269,7 @@ UnionWs union_ws_layout(int64_t M, int64_t N, int64_t K, int T = 256, int C = 8)
     // zeroed together before each forward (one memset): row counts + the gate GEMM's tile counter (nnz[M]), the
     // prep kernel's counters, and (split prep only) the merged union masks
     w.nnz = o;   o = (o + (M + 1) * 4 + 15) & ~int64_t(15);
-    w.pctr = o;  o = (o + (2 + 2 * NB) * 4 + 15) & ~int64_t(15);
+    w.pctr = o;  o = (o + (2 + 2 * NB + (M + 2047) / 2048) * 4 + 15) & ~int64_t(15);  // + gate->prep window counters
     w.umask = o; o = align1k(o + NB * (N / 32) * 4);
     w.lmax = static_cast<int>((N / T) * (T / C - 1));  // most stored entries a row can have
     w.nchunk = static_cast<int>((N + 255) / 256);
@@ -327,12 +334,43 @@ int union_prep_split(int64_t NB) {
     return split;
 }
 
+// Overlapped prep (session 3): the gate GEMM signals per 2048-row window (GemmArgs::win_done) and starts the prep
+// kernel as a programmatic dependent; prep CTAs run beside the gate GEMM (one per SM: 256 + 512 threads, 28.7 K + 32 K
+// registers, 181 KB + the prep's SMEM) and wait per window.  SFFN_PREP_OVERLAP=0/1 (A/B; default below).
+#ifndef SFFN_PREP_OVERLAP_DEFAULT
+#define SFFN_PREP_OVERLAP_DEFAULT 0
+#endif
+bool union_prep_overlap_enabled() { return env_flag("SFFN_PREP_OVERLAP", SFFN_PREP_OVERLAP_DEFAULT != 0); }
+constexpr int PREP_TAIL_SPLIT = 8;  // parts per block of the windows the gate GEMM finishes last
+// X-copy ring piece that lets a prep CTA sit beside a gate GEMM CTA (0: does not fit -> no overlap)
+int prep_overlap_piece(int64_t N, int nchunk, int C) {
+    int gsmem = 0;
+    switch (C) {
+        case 1: gsmem = gemm_smem_bytes<EPI_TWELL, 1, 2>(); break;
+        case 2: gsmem = gemm_smem_bytes<EPI_TWELL, 2, 2>(); break;
+        case 4: gsmem = gemm_smem_bytes<EPI_TWELL, 4, 2>(); break;
+        case 8: gsmem = gemm_smem_bytes<EPI_TWELL, 8, 2>(); break;
+        default: gsmem = gemm_smem_bytes<EPI_TWELL, 16, 2>(); break;
+    }
+    const int64_t budget = 233472 - 2 * 1024 - gsmem - PREP_STATIC_SMEM;  // 228 KB per SM, 1 KB reserved per CTA
+    for (int piece : {8192, 6144, 4096, 3072, 2048})
+        if (static_cast<int64_t>(prep_smem_bytes(static_cast<int>(N), nchunk, piece)) <= budget) return piece;
+    return 0;
+}
+// the gate GEMM's last raster group (GEMM_GROUP_M / 2 pair-M-tiles) -> first window it covers
+int prep_tail_w0(int64_t M) {
+    const int64_t pm = (M + 255) / 256, grp = GEMM_GROUP_M / 2;
+    return static_cast<int>(((pm - 1) / grp) * grp * 256 / 2048);
+}
+
 // Bytes to zero before a gated union forward, from the row-count buffer (union_nnz_ptr) on: row counts, the gate
 // GEMM tile counter, the prep kernel's counters and, when the prep kernel splits blocks, the merged masks.
 size_t union_zero_bytes(int64_t M, int64_t N, int64_t K, int T, int C) {
     const UnionWs L = union_ws_layout(M, N, K, T, C);
     const int64_t NB = (M + union_brows() - 1) / union_brows();
-    const int64_t end = (union_prep_split(NB) > 1 || union_prep_boost(NB, union_brows())) ? L.umask + NB * (N / 32) * 4 : L.pctr + (2 + 2 * NB) * 4;
+    const int64_t end = (union_prep_split(NB) > 1 || union_prep_boost(NB, union_brows()) || union_prep_overlap_enabled())
+                            ? L.umask + NB * (N / 32) * 4
+                            : L.pctr + (2 + 2 * NB + (M + 2047) / 2048) * 4;
     return static_cast<size_t>(end - L.nnz);
 }
 
@@ -368,9 +406,11 @@ struct FuseParams {
     int phase;  // 0: the whole up/down; 1: everything before the DOWN kernel; 2: the DOWN kernel only
 };
 
+// ov_piece > 0: the gate GEMM was launched with win_done = the prep counters' window block (union_win_done) and the
+// prep kernel is launched as its programmatic dependent with an X-copy ring of 8 x ov_piece bytes (prep_overlap_piece)
 int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const void* Wd, int64_t M, int64_t K,
                       int64_t N, int T, int C, void* Y, void* ws, cudaStream_t st, bool gated = true,
-                      bool nnz_ready = false, const FuseParams* fuse = nullptr) {
+                      bool nnz_ready = false, const FuseParams* fuse = nullptr, int ov_piece = 0) {
     const int BR = union_brows();
     const int64_t NB = (M + BR - 1) / BR;
     UnionWs L = union_ws_layout(M, N, K, T, C);
@@ -406,23 +446,66 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
                                 st) != cudaSuccess)
                 return SFFN_ERR_CUDA;
         }
-        const int split = union_prep_split(NB), boost = union_prep_boost(NB, BR);
-        const int pctas = prep_ctas(static_cast<int>(NB), PERM_W / BR, split, boost);
-        const size_t psmem = prep_smem_bytes(static_cast<int>(N), L.nchunk);
+        const bool ovl = ov_piece > 0;
+        const int split = union_prep_split(NB), boost = ovl ? 1 : union_prep_boost(NB, BR);
+        PrepOv ov{};
+        int pctas;
+        if (ovl) {
+            ov.win_done = reinterpret_cast<const int*>(base + L.pctr) + 2 + 2 * NB;
+            ov.win_n = static_cast<int>((N + GEMM_BN - 1) / GEMM_BN);
+            ov.tail_w0 = prep_tail_w0(M);
+            ov.tail_split = std::max(split, PREP_TAIL_SPLIT);
+            pctas = prep_ctas_ov(static_cast<int>(NB), PERM_W / BR, split, boost, ov.tail_w0, ov.tail_split);
+        } else {
+            pctas = prep_ctas(static_cast<int>(NB), PERM_W / BR, split, boost);
+        }
+        const int piece = ovl ? ov_piece : PREP_PIECE;
+        const size_t psmem = prep_smem_bytes(static_cast<int>(N), L.nchunk, piece);
         static std::once_flag ponce;
         static cudaError_t pattr = cudaSuccess;
         std::call_once(ponce, [] {
-            pattr = cudaFuncSetAttribute(union_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            pattr = cudaFuncSetAttribute(union_prep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(prep_smem_bytes(65536, 256)));
+            if (pattr == cudaSuccess)
+                pattr = cudaFuncSetAttribute(union_prep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(prep_smem_bytes(65536, 256)));
+            // the overlapped prep must use the gate GEMM's shared-memory carveout (the maximum), else an SM running a
+            // gate GEMM CTA cannot also host a prep CTA
+            if (pattr == cudaSuccess)
+                pattr = cudaFuncSetAttribute(union_prep_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             cudaSharedmemCarveoutMaxShared);
         });
         if (pattr != cudaSuccess) return SFFN_ERR_CUDA;
         const bool tma_dense = BR == 128 && N >= 256;
-        { union_prep_kernel<<<static_cast<unsigned>(pctas), PREP_THREADS, psmem, st>>>(
-            tw, (int)M, (int)N, T, C, um, perm, rnnz, reinterpret_cast<int*>(base + L.pctr),
-            env_int("SFFN_UP_GROUP", union_group_up(NB)), split, boost, union_dense_units(N, tma_dense),
-            union_dense_nnz(N, tma_dense), gated ? static_cast<const uint8_t*>(X) : nullptr, K * 2,
-            (gated && !env_flag("SFFN_PREP_NOCOPY", false)) ? static_cast<uint8_t*>(xp) : nullptr, gated ? 1 : 0,
-            prep_trace_buf(pctas)); note_launch(); }
+        const int up_group = env_int("SFFN_UP_GROUP", union_group_up(NB));
+        const uint8_t* xin = gated ? static_cast<const uint8_t*>(X) : nullptr;
+        uint8_t* xout = (gated && !env_flag("SFFN_PREP_NOCOPY", false)) ? static_cast<uint8_t*>(xp) : nullptr;
+        int* pc = reinterpret_cast<int*>(base + L.pctr);
+        const int dunits = union_dense_units(N, tma_dense);
+        const int64_t dnnz = union_dense_nnz(N, tma_dense);
+        unsigned long long* trace = prep_trace_buf(pctas);
+        if (ovl) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>(pctas));
+            cfg.blockDim = dim3(PREP_THREADS);
+            cfg.dynamicSmemBytes = psmem;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = env_flag("SFFN_PREP_OV_NOPDL", false) ? 0 : 1;  // diagnostic: signals without the overlap
+            if (cudaLaunchKernelEx(&cfg, union_prep_kernel<true>, tw, (int)M, (int)N, T, C, um, perm,
+                                   static_cast<const int*>(rnnz), pc, up_group, split, boost, piece, ov, dunits, dnnz,
+                                   xin, static_cast<int64_t>(K * 2), xout, gated ? 1 : 0, trace) != cudaSuccess)
+                return SFFN_ERR_CUDA;
+            note_launch();
+        } else {
+            union_prep_kernel<false><<<static_cast<unsigned>(pctas), PREP_THREADS, psmem, st>>>(
+                tw, (int)M, (int)N, T, C, um, perm, rnnz, pc, up_group, split, boost, piece, ov, dunits, dnnz, xin,
+                K * 2, xout, gated ? 1 : 0, trace);
+            note_launch();
+        }
         if (cudaGetLastError() != cudaSuccess) return SFFN_ERR_CUDA;
         if (!gated) {  // non-gated: H_c = the scattered TwELL values (no up GEMM)
             { union_gate_scatter_kernel<<<static_cast<unsigned>(NB * (BR / GS_ROWS)), 256, 0, st>>>(
@@ -633,8 +716,14 @@ int sffn_forward(const void* X, const void* Wg, const void* Wu, const void* Wd, 
         // the gate GEMM epilogue also counts each row's stored entries (the union path's row order pi)
         int* nnz = union_nnz_ptr(udws, M, N, K, T, C);
         if (cudaMemsetAsync(nnz, 0, union_zero_bytes(M, N, K, T, C), S(stream)) != cudaSuccess) return SFFN_ERR_CUDA;
-        if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz, nnz + M)) != SFFN_OK) return r;
-        return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true);
+        // overlapped prep: CTA-pair gate GEMM, 128-row union blocks, and room for a prep CTA beside a gate GEMM CTA
+        static const bool gate_pair = env_flag("SFFN_GATE_PAIR", true);
+        const UnionWs L = union_ws_layout(M, N, K, T, C);
+        const int ov_piece = (union_prep_overlap_enabled() && gate_pair && union_brows() == 128)
+                                 ? prep_overlap_piece(N, L.nchunk, C) : 0;
+        int* win_done = ov_piece > 0 ? reinterpret_cast<int*>(udws + L.pctr) + 2 + 2 * ((M + 127) / 128) : nullptr;
+        if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream), nnz, nnz + M, win_done)) != SFFN_OK) return r;
+        return union_updown_impl(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, S(stream), true, true, nullptr, ov_piece);
     }
     if ((r = pack_impl(X, Wg, M, K, N, T, C, tw, d_overflow, S(stream))) != SFFN_OK) return r;
     return updown_dispatch(X, tw, Wu, Wd, M, K, N, T, C, Y, udws, ws_bytes - static_cast<size_t>(tw_bytes), algo,

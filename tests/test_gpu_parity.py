@@ -787,6 +787,41 @@ def test_prep_split_invariance(sffn, monkeypatch, M):
     assert_y(bf16_np(outs[0].view(torch.bfloat16)), oracle.ffn_twell(X, wo, Wu, Wd, cfg.N, 256, 8))
 
 
+@pytest.mark.parametrize("M,K,N", [(300, 256, 2048), (5000, 256, 2048), (4224, 1024, 4096), (12288, 512, 14336)])
+def test_prep_overlap(sffn, monkeypatch, M, K, N):
+    """Overlapped prep (the gate GEMM signals per 2048-row window and starts the prep kernel as a programmatic
+    dependent; prep CTAs wait per window and run beside the gate GEMM; the windows of the gate GEMM's last raster group
+    take 8 parts per block): Y and the union sizes are bit-identical to the standalone prep, eagerly and replayed
+    from a CUDA graph (as bench.py runs it), and Y is within the per-row bars of Eq.3 (oracle).  M = 5000 and 4224
+    end in partial windows; 12288 rows give background windows and a tail group."""
+    cfg = synth.CONFIGS["1B"].replace(M=M, K=K, N=N, Kb=16, sparsity=0.99)
+    X, Wg, Wu, Wd = inputs(cfg)
+    Xd, Wgd, Wud, Wdd = (to_dev(a) for a in (X, Wg, Wu, Wd))
+    ws = torch.empty(sffn.workspace_bytes(M, K, N, 256, 8, "union"), dtype=torch.uint8, device="cuda")
+    outs = []
+    for ov in ("0", "1", "1"):
+        monkeypatch.setenv("SFFN_PREP_OVERLAP", ov)
+        Y = sffn.forward(Xd, Wgd, Wud, Wdd, 256, 8, workspace=ws, algo="union")
+        torch.cuda.synchronize()
+        outs.append(Y.view(torch.int16).cpu())
+    monkeypatch.setenv("SFFN_PREP_OVERLAP", "1")
+    Yg = torch.empty((M, K), dtype=torch.bfloat16, device="cuda")
+    sffn.forward(Xd, Wgd, Wud, Wdd, 256, 8, out=Yg, workspace=ws, algo="union")  # kernel attributes outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        sffn.forward(Xd, Wgd, Wud, Wdd, 256, 8, out=Yg, workspace=ws, algo="union")
+    for _ in range(3):
+        Yg.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        outs.append(Yg.view(torch.int16).cpu())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    wo, counts, n_ov, A = oracle.pack_from_inputs(X, Wg, 256, 8, matmul=True)
+    assert_y(bf16_np(outs[0].view(torch.bfloat16)), oracle.ffn_twell(X, wo, Wu, Wd, N, 256, 8))
+
+
 def test_union_pi_order(sffn):
     """The row order pi (descending stored non-zeros per 2048-row window, ties by row index) and the
     128-row block unions built on it: the union sizes the library reports equal those computed here from the
