@@ -118,7 +118,8 @@ struct SyncAll {
     __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
 template <int NTH, class Sync = SyncAll>
-__device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, int* goff, Sync sync = Sync()) {
+__device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, int* goff, Sync sync = Sync(),
+                                bool order_by_fraction = false) {
     constexpr int NWP = NTH / 32;
     constexpr int MAXG = UNION_GROUP_MAX;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -172,11 +173,26 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, int*
             const int n0 = (lane < group && bi + lane < NB) ? (__ldcg(um.ulen + bi + lane) + 255) / 256 : 0;
             const int n1 = (lane + 32 < group && bi + lane + 32 < NB) ? (__ldcg(um.ulen + bi + lane + 32) + 255) / 256 : 0;
             const int mc = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(max(n0, n1))));
-            for (int c = 0; c < mc; ++c) {
-                const unsigned m0 = __ballot_sync(0xffffffffu, c < n0), m1 = __ballot_sync(0xffffffffu, c < n1);
-                if (c < n0) um.tiles[p + __popc(m0 & lt)] = ((bi + lane) << 8) | c;
-                if (c < n1) um.tiles[p + __popc(m0) + __popc(m1 & lt)] = ((bi + lane + 32) << 8) | c;
-                p += __popc(m0) + __popc(m1);
+            if (!order_by_fraction) {
+                for (int c = 0; c < mc; ++c) {
+                    const unsigned m0 = __ballot_sync(0xffffffffu, c < n0), m1 = __ballot_sync(0xffffffffu, c < n1);
+                    if (c < n0) um.tiles[p + __popc(m0 & lt)] = ((bi + lane) << 8) | c;
+                    if (c < n1) um.tiles[p + __popc(m0) + __popc(m1 & lt)] = ((bi + lane + 32) << 8) | c;
+                    p += __popc(m0) + __popc(m1);
+                }
+            } else {
+                // slot s emits chunk floor(s * n / mc) of a block with n chunks when it changes: every block's chunks
+                // advance at the same rate through its union, so concurrent tiles cover similar unit ranges (the
+                // union of a block is spread evenly over N) and share gathered weight rows in L2
+                for (int t = 0; t < mc; ++t) {
+                    const int c0 = t * n0 / mc, c1 = t * n1 / mc;
+                    const bool e0 = n0 > 0 && (t == 0 || c0 != (t - 1) * n0 / mc);
+                    const bool e1 = n1 > 0 && (t == 0 || c1 != (t - 1) * n1 / mc);
+                    const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
+                    if (e0) um.tiles[p + __popc(m0 & lt)] = ((bi + lane) << 8) | c0;
+                    if (e1) um.tiles[p + __popc(m0) + __popc(m1 & lt)] = ((bi + lane + 32) << 8) | c1;
+                    p += __popc(m0) + __popc(m1);
+                }
             }
         }
         carry += wsum[NWP];
