@@ -32,10 +32,16 @@ struct UnionMeta {
     int brows;           // token rows per union block: 128 (one tcgen05 M tile) or 256 (a CTA pair's M=256 tile)
 };
 
-// token blocks whose up-GEMM tiles run together (chunk-major within the group): NB / 8 clamped to [8, 32] — interleaved
-// A/B (profiles/r02/s3/ab_up_*.json): 32 vs 8 is 1.2-2% faster at 7B (NB = 256) and 70B (NB = 512), equal at 1B
-// (NB = 128, 16 there), and 8 stays best for the 4096-row chunks of the host pipeline (NB = 32)
-__host__ __device__ constexpr int union_group_up(int64_t NB) { return NB / 8 < 8 ? 8 : (NB / 8 > 32 ? 32 : static_cast<int>(NB / 8)); }
+// token blocks whose up-GEMM tiles run together: min(NB / 8, the blocks whose X rows fill 32 MB), clamped to [8, 32].
+// With the fraction-ordered work list the group's X tiles are the L2 working set that grows with the group (ncu,
+// profiles/r02/s3/ncu_up_group_order.txt: UP fastest at 32 blocks for 7B (1 MB of X per block), 16 for 70B (2 MB), within
+// 1.3% for 1B); interleaved A/B without the ordering: 32 vs 8 was 1.2-2% faster at 7B / 70B, and 8 stays best for
+// the 4096-row chunks of the host pipeline (NB = 32)
+__host__ __device__ constexpr int union_group_up(int64_t NB, int64_t K) {
+    const int64_t by_x = (int64_t(32) << 20) / (128 * K * 2);
+    const int64_t g = NB / 8 < by_x ? NB / 8 : by_x;
+    return g < 8 ? 8 : (g > 32 ? 32 : static_cast<int>(g));
+}
 constexpr int UNION_GROUP_DOWN = 4;   // token blocks whose down-GEMM tiles run together (4 vs 16: -0.9% forward, -2% e2e)
 constexpr int UNION_GROUP_MAX = 64;   // largest UP group the work-list builder supports
 
