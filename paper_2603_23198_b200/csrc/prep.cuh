@@ -566,7 +566,8 @@ __global__ void __launch_bounds__(PREP_THREADS, 2) union_prep_kernel(
         prep_sync();
         if (s_last) {  // the last block built: the UP work list from every block's ulen
             __threadfence();
-            union_scan_body<PREP_WORK>(um, NB, up_group < 0 ? -up_group : up_group, wsum, goff, PrepSync(), up_group < 0);
+            const int ug = up_group & 0xFFFF, uflags = up_group >> 16;  // flags: 1 fraction order, 2 snake
+            union_scan_body<PREP_WORK>(um, NB, ug, wsum, goff, PrepSync(), (uflags & 1) != 0, (uflags & 2) != 0);
         }
     } else {
         // wait for the block's builder (it is running: it arrived after this part), then its mask and offsets

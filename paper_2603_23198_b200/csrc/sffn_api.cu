@@ -477,9 +477,10 @@ int union_updown_impl(const void* X, const uint32_t* tw, const void* Wu, const v
         });
         if (pattr != cudaSuccess) return SFFN_ERR_CUDA;
         const bool tma_dense = BR == 128 && N >= 256;
-        // negative: the work list orders each group's tiles by their fraction of the block's union (default; chunk-major
+        // bits 16+: the work list orders each group's tiles by their fraction of the block's union (default; chunk-major
         // with SFFN_UP_ORDER=0) — ncu: 7B UP DRAM reads 2.0 -> 1.2 GB, 1.133 -> 1.105 ms; 70B 34 -> 21 GB, 9.54 -> 8.85 ms
-        const int up_group = env_int("SFFN_UP_GROUP", union_group_up(NB, K)) * (env_flag("SFFN_UP_ORDER", true) ? -1 : 1);
+        const int up_group = env_int("SFFN_UP_GROUP", union_group_up(NB, K)) |
+                             (env_flag("SFFN_UP_ORDER", true) ? 1 << 16 : 0) | (env_flag("SFFN_UP_SNAKE", true) ? 2 << 16 : 0);
         const uint8_t* xin = gated ? static_cast<const uint8_t*>(X) : nullptr;
         uint8_t* xout = (gated && !env_flag("SFFN_PREP_NOCOPY", false)) ? static_cast<uint8_t*>(xp) : nullptr;
         int* pc = reinterpret_cast<int*>(base + L.pctr);

@@ -125,7 +125,7 @@ struct SyncAll {
 };
 template <int NTH, class Sync = SyncAll>
 __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, int* goff, Sync sync = Sync(),
-                                bool order_by_fraction = false) {
+                                bool order_by_fraction = false, bool snake = false) {
     constexpr int NWP = NTH / 32;
     constexpr int MAXG = UNION_GROUP_MAX;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -190,10 +190,14 @@ __device__ void union_scan_body(UnionMeta um, int NB, int group, int* wsum, int*
                 // slot s emits chunk floor(s * n / mc) of a block with n chunks when it changes: every block's chunks
                 // advance at the same rate through its union, so concurrent tiles cover similar unit ranges (the
                 // union of a block is spread evenly over N) and share gathered weight rows in L2
-                for (int t = 0; t < mc; ++t) {
+                // snake (default; SFFN_UP_SNAKE=0 disables): odd groups walk their unions backwards, so a group starts
+                // on the unit range the previous group ended on (ncu: UP DRAM -5-7%, time -0.1% 7B / -0.4% 70B)
+                const bool rev = snake && (gi & 1);
+                for (int s_ = 0; s_ < mc; ++s_) {
+                    const int t = rev ? mc - 1 - s_ : s_, tp = rev ? t + 1 : t - 1;
                     const int c0 = t * n0 / mc, c1 = t * n1 / mc;
-                    const bool e0 = n0 > 0 && (t == 0 || c0 != (t - 1) * n0 / mc);
-                    const bool e1 = n1 > 0 && (t == 0 || c1 != (t - 1) * n1 / mc);
+                    const bool e0 = n0 > 0 && (s_ == 0 || c0 != tp * n0 / mc);
+                    const bool e1 = n1 > 0 && (s_ == 0 || c1 != tp * n1 / mc);
                     const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
                     if (e0) um.tiles[p + __popc(m0 & lt)] = ((bi + lane) << 8) | c0;
                     if (e1) um.tiles[p + __popc(m0) + __popc(m1 & lt)] = ((bi + lane + 32) << 8) | c1;

@@ -770,18 +770,20 @@ def test_prep_split_invariance(sffn, monkeypatch, M):
     CTA or split over 2, 4, 8 CTAs (atomicOr merge of the parts' masks, the last part builds, flag release), with or
     without the densest-blocks-first boost (x2 / x4 parts for a window's first blocks, window-position-major CTA ids;
     M = 5000 ends in a partial window), and whatever the UP work-list raster group (1, 8, 64 blocks) and tile order
-    (chunk-major or by fraction of the union): Y is
+    (chunk-major, by fraction of the union, snake): Y is
     bit-identical for every setting, and within the per-row bars of Eq.3 (oracle)."""
     cfg = synth.CONFIGS["1B"].replace(M=M, K=256, N=2048, Kb=16, sparsity=0.99)
     X, Wg, Wu, Wd = inputs(cfg)
     Xd, Wgd, Wud, Wdd = (to_dev(a) for a in (X, Wg, Wu, Wd))
     outs = []
     for split, boost, group, order in [(s_, b_, "8", "0") for s_ in ("1", "2", "4", "8") for b_ in ("0", "1", "2")] + \
-            [("1", "1", "1", "0"), ("2", "2", "64", "0"), ("1", "1", "32", "1"), ("4", "1", "8", "1")]:
+            [("1", "1", "1", "0"), ("2", "2", "64", "0"), ("1", "1", "32", "1"), ("4", "1", "8", "1"),
+             ("1", "1", "1", "3"), ("2", "1", "8", "3")]:
         monkeypatch.setenv("SFFN_PREP_SPLIT", split)
         monkeypatch.setenv("SFFN_PREP_BOOST", boost)
         monkeypatch.setenv("SFFN_UP_GROUP", group)
-        monkeypatch.setenv("SFFN_UP_ORDER", order)
+        monkeypatch.setenv("SFFN_UP_ORDER", "1" if order != "0" else "0")
+        monkeypatch.setenv("SFFN_UP_SNAKE", "1" if order == "3" else "0")
         outs.append(sffn.forward(Xd, Wgd, Wud, Wdd, 256, 8, algo="union").view(torch.int16).cpu())
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
