@@ -61,6 +61,21 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 #endif
 }
+// UP gathers (row-major W_u: the row's next k-block is the next 128 bytes): optional L2 prefetch-size hint
+#ifndef SFFN_UP_L2PF
+#define SFFN_UP_L2PF 0
+#endif
+__device__ __forceinline__ void cp_async16_up(uint32_t dst, const void* src) {
+#ifndef SFFN_UG_NOGATHER
+#if SFFN_UP_L2PF == 256
+    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#elif SFFN_UP_L2PF == 128
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#endif
+#endif
+}
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -330,8 +345,8 @@ __global__ void __launch_bounds__(FUSED ? UG_THREADS : UG_THREADS2, 1)
                     for (int i = 0; i < NP; ++i) {
                         const int r = RPI * UG_GW * i + RPI * gw + sub;
                         if (nidx[i] >= 0)
-                            cp_async16(dst + ug_kmajor_off(r, cl),
-                                       args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * UG_BK + 8 * cl, 16);
+                            cp_async16_up(dst + ug_kmajor_off(r, cl),
+                                          args.wsrc + static_cast<int64_t>(nidx[i]) * args.K + kb * UG_BK + 8 * cl);
                     }
                     cp_async_arrive_noinc(&full[stage]);
                     if (++stage == S) {
