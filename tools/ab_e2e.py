@@ -23,6 +23,8 @@ Xh = torch.from_numpy(Xn.view(np.int16)).view(torch.bfloat16).pin_memory()
 Yh = torch.empty((M, K), dtype=torch.bfloat16).pin_memory()
 ref = None
 plans = [(c, s) for c, s in itertools.product([2048, 4096, 6144, 8192], [2, 3, 99])]
+if os.environ.get("PLANS"):  # e.g. PLANS="4096:2,2048:99,4096:99"
+    plans = [tuple(int(v) for v in p.split(":")) for p in os.environ["PLANS"].split(",")]
 res = {pl: [] for pl in plans}
 bufs = {}
 for c, s in plans:
@@ -33,7 +35,7 @@ for c, s in plans:
     bufs[(c, s)] = (torch.empty((wsz + 1023) // 1024 * 1024 + wsz, dtype=torch.uint8, device="cuda"),
                     torch.empty(int(sffn.sffn.lib().sffn_forward_host_stage_bytes(K, rows)) * slots // 2,
                                 dtype=torch.uint8, device="cuda"), slots)
-for rep in range(6):
+for rep in range(int(os.environ.get("REPS", "6"))):
     for pl in (plans if rep % 2 == 0 else plans[::-1]):
         ws, st, slots = bufs[pl]
         for it in range(3):
